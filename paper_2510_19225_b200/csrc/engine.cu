@@ -1,0 +1,799 @@
+// The rollout instance: one per GPU, behind the rlb_* C ABI (include/rlb.h).
+//
+// It replaces the reference's simulated rollout instance -- GenUnit's
+// continuous-batching state, the FIFO prefill lane and the analytic decode
+// rate (pkg/src/spotrl/sim/engine.py:63-83,699-811,
+// pkg/src/spotrl/sim/models.py:39-48) -- with a real Qwen2-shape decoder:
+//
+//   * requests live in device slots: token buffer [max_slots][max_seq]
+//     (prompt + generated = the response buffer, K6), length, target, and a
+//     page table into a paged KV pool (64-token pages, allocated for the whole
+//     request at admission);
+//   * admission runs one varlen prefill (K4) over prompt + prefix tokens of
+//     every newly admitted request -- resume after migration is the same call
+//     (the `generate{prompt_tokens, prefix_tokens}` message,
+//     pkg/src/spotrl/protocol.py:75-81);
+//   * a decode step is [prepare rows -> 28 x (RMSNorm, QKV GEMM+bias, RoPE+KV
+//     append, split-K paged attention, O GEMM+residual, RMSNorm, gate_up GEMM
+//     +SwiGLU, down GEMM+residual) -> final norm -> lm_head -> argmax+append],
+//     captured `graph_steps` steps per CUDA graph;
+//   * new token ids land in a [steps][slots] ring flushed with one D2H copy per
+//     rlb_step call, which the host turns into bulk on_tokens(count=k)
+//     (pkg/src/spotrl/manager.py:295-314).
+#include "internal.h"
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <deque>
+#include <map>
+#include <unordered_map>
+
+namespace rlb {
+
+thread_local std::string g_err;
+void set_error(const std::string& m) { g_err = m; }
+
+struct Req {
+  uint64_t key = 0;
+  std::vector<int32_t> tokens;  // prompt + generated (host mirror, exact after each rlb_step)
+  int32_t n_prompt = 0;
+  int32_t target_len = 0;       // generated tokens at completion (prefix included)
+  int32_t slot = -1;
+  int32_t reported = 0;         // generated tokens already handed to the caller
+  bool prefilled = false;
+  int32_t generated() const { return static_cast<int32_t>(tokens.size()) - n_prompt; }
+  bool complete() const { return generated() >= target_len; }
+};
+
+struct LayerW {
+  bf16 *ln1, *wqkv, *bqkv, *wo, *ln2, *wgu, *wdown;
+  CUtensorMap m_qkv, m_o, m_gu, m_down;
+};
+
+// GEMM tile widths per projection (N-tile of the 128 x BN UMMA tile).
+constexpr int BN_QKV = 128, BN_O = 64, BN_GU = 256, BN_DOWN = 64, BN_LM = 256;
+constexpr int RING_ROWS = 512;
+
+template <typename T>
+static int dalloc(T** p, size_t n) {
+  RLB_CUDA(cudaMalloc(reinterpret_cast<void**>(p), n * sizeof(T)));
+  return RLB_OK;
+}
+
+}  // namespace rlb
+
+using namespace rlb;
+
+struct rlb_instance {
+  int device = 0;
+  rlb_model_cfg m{};
+  rlb_engine_cfg e{};
+  cudaStream_t st = nullptr;
+  int NQ = 0, NKV = 0, D = 0, H = 0, F = 0, V = 0, QKV = 0;
+  int max_slots = 0, max_seq = 0, pps = 0, num_pages = 0, max_rows = 0, max_splits = 0;
+  int prefill_rows = 0;
+  // weights
+  uint8_t* arena = nullptr;
+  int64_t arena_bytes = 0;
+  uint64_t version = 0;
+  bool has_weights = false;
+  bf16 *embed = nullptr, *norm = nullptr, *lm_head = nullptr;
+  std::vector<LayerW> L;
+  CUtensorMap m_lm;
+  // KV
+  bf16* kv = nullptr;
+  size_t layer_stride = 0;  // elements
+  int* d_bt = nullptr;
+  std::vector<int> h_bt;
+  std::vector<int> free_pages;
+  // slots
+  int32_t *d_seq_tokens = nullptr, *d_seq_len = nullptr, *d_seq_target = nullptr;
+  std::vector<int32_t> h_seq_len, h_seq_target;
+  std::vector<int> free_slots;
+  std::vector<Req*> slot_req;
+  bool slots_dirty = true;
+  // rows
+  int *d_row_tok = nullptr, *d_row_pos = nullptr, *d_row_slot = nullptr, *d_logit_src = nullptr,
+      *d_logit_slot = nullptr, *d_dec_slots = nullptr;
+  int* h_stage = nullptr;  // pinned: prefill row staging
+  size_t stage_cap = 0;
+  float* d_h = nullptr;
+  bf16 *d_xn = nullptr, *d_qkv = nullptr, *d_q = nullptr, *d_attn = nullptr, *d_act = nullptr;
+  float* d_logits = nullptr;
+  float* d_ws = nullptr;
+  CUtensorMap m_xn, m_attn, m_act;
+  int32_t *d_ring = nullptr, *d_ring_ctr = nullptr, *d_ring_cur = nullptr, *h_ring = nullptr;
+  float2* d_rope = nullptr;
+  // requests
+  std::deque<Req*> pending;
+  std::unordered_map<uint64_t, Req*> reqs;
+  std::vector<int> dec_list;
+  std::map<int, cudaGraphExec_t> graphs;
+  int graph_built_for_version = -1;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+
+  ~rlb_instance();
+  int init();
+  int bind_arena();
+  int forward_layers(int R);
+  int head(int Lrows, bool append);
+  int decode_step_launch(int R);
+  int admit_and_prefill(int* rows_run);
+  int run_decode(int steps, int* steps_run);
+  int flush(rlb_token_batch* out);
+  int upload_slots();
+  void release(Req* r);
+};
+
+rlb_instance::~rlb_instance() {
+  cudaSetDevice(device);
+  if (st) cudaStreamSynchronize(st);
+  for (auto& g : graphs) cudaGraphExecDestroy(g.second);
+  void* bufs[] = {arena, kv, d_bt, d_seq_tokens, d_seq_len, d_seq_target, d_row_tok, d_row_pos,
+                  d_row_slot, d_logit_src, d_logit_slot, d_dec_slots, d_h, d_xn, d_qkv, d_q,
+                  d_attn, d_act, d_logits, d_ws, d_ring, d_ring_ctr, d_ring_cur, d_rope};
+  for (void* b : bufs)
+    if (b) cudaFree(b);
+  if (h_stage) cudaFreeHost(h_stage);
+  if (h_ring) cudaFreeHost(h_ring);
+  if (ev0) cudaEventDestroy(ev0);
+  if (ev1) cudaEventDestroy(ev1);
+  if (st) cudaStreamDestroy(st);
+  for (auto& kv_ : reqs) delete kv_.second;
+}
+
+int rlb_instance::init() {
+  NQ = m.n_q_heads;
+  NKV = m.n_kv_heads;
+  D = m.head_dim;
+  H = m.hidden;
+  F = m.ffn;
+  V = m.vocab;
+  QKV = (NQ + 2 * NKV) * D;
+  RLB_CHECK(D == 64 || D == 128, RLB_ERR_ARG, "head_dim must be 64 or 128");
+  RLB_CHECK(NQ % NKV == 0 && NQ / NKV <= 8, RLB_ERR_ARG, "unsupported GQA group");
+  RLB_CHECK(H % 64 == 0 && F % 64 == 0 && (NQ * D) % 64 == 0 && V % 16 == 0 && QKV % 128 == 0,
+            RLB_ERR_ARG, "model dims not tileable");
+  max_slots = e.max_slots;
+  max_seq = e.max_seq_len;
+  RLB_CHECK(max_slots > 0 && max_seq > 0, RLB_ERR_ARG, "max_slots/max_seq_len must be positive");
+  pps = (max_seq + PAGE - 1) / PAGE;
+  num_pages = e.num_pages > 0 ? e.num_pages : max_slots * pps;
+  max_splits = (max_seq + SPLIT - 1) / SPLIT;
+  const size_t ws_row = static_cast<size_t>(NQ) * max_splits * (D + 2) * sizeof(float);
+  const size_t ws_budget = static_cast<size_t>(1) << 30;
+  prefill_rows = e.max_prefill_rows > 0 ? e.max_prefill_rows : 16384;
+  prefill_rows = static_cast<int>(std::min<size_t>(prefill_rows, ws_budget / ws_row));
+  prefill_rows = std::max(prefill_rows, 128);
+  max_rows = std::max(prefill_rows, max_slots);
+  max_rows = (max_rows + 127) / 128 * 128;
+
+  RLB_CUDA(cudaSetDevice(device));
+  RLB_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  RLB_CUDA(cudaEventCreate(&ev0));
+  RLB_CUDA(cudaEventCreate(&ev1));
+
+  arena_bytes = rlb::arena_bytes(m);
+  int rc;
+  if ((rc = dalloc(&arena, arena_bytes))) return rc;
+  RLB_CUDA(cudaMemset(arena, 0, arena_bytes));
+  layer_stride = static_cast<size_t>(num_pages) * NKV * 2 * PAGE * D;
+  if ((rc = dalloc(&kv, layer_stride * m.layers))) return rc;
+  if ((rc = dalloc(&d_bt, static_cast<size_t>(max_slots) * pps))) return rc;
+  h_bt.assign(static_cast<size_t>(max_slots) * pps, 0);
+  RLB_CUDA(cudaMemset(d_bt, 0, sizeof(int) * h_bt.size()));
+  free_pages.resize(num_pages);
+  for (int i = 0; i < num_pages; ++i) free_pages[i] = num_pages - 1 - i;
+  if ((rc = dalloc(&d_seq_tokens, static_cast<size_t>(max_slots) * max_seq))) return rc;
+  if ((rc = dalloc(&d_seq_len, max_slots))) return rc;
+  if ((rc = dalloc(&d_seq_target, max_slots))) return rc;
+  h_seq_len.assign(max_slots, 1);
+  h_seq_target.assign(max_slots, 0);
+  slot_req.assign(max_slots, nullptr);
+  for (int s = max_slots - 1; s >= 0; --s) free_slots.push_back(s);
+  RLB_CUDA(cudaMemset(d_seq_tokens, 0, sizeof(int32_t) * max_slots * static_cast<size_t>(max_seq)));
+
+  const size_t R = max_rows;
+  if ((rc = dalloc(&d_row_tok, R)) || (rc = dalloc(&d_row_pos, R)) || (rc = dalloc(&d_row_slot, R)) ||
+      (rc = dalloc(&d_logit_src, R)) || (rc = dalloc(&d_logit_slot, R)) ||
+      (rc = dalloc(&d_dec_slots, max_slots)))
+    return rc;
+  if ((rc = dalloc(&d_h, R * H)) || (rc = dalloc(&d_xn, R * H)) || (rc = dalloc(&d_qkv, R * QKV)) ||
+      (rc = dalloc(&d_q, R * NQ * D)) || (rc = dalloc(&d_attn, R * NQ * D)) ||
+      (rc = dalloc(&d_act, R * F)))
+    return rc;
+  RLB_CUDA(cudaMemset(d_xn, 0, R * H * sizeof(bf16)));
+  RLB_CUDA(cudaMemset(d_attn, 0, R * NQ * D * sizeof(bf16)));
+  RLB_CUDA(cudaMemset(d_act, 0, R * F * sizeof(bf16)));
+  const int logit_rows = (max_slots + 127) / 128 * 128;
+  if ((rc = dalloc(&d_logits, static_cast<size_t>(logit_rows) * V))) return rc;
+  if ((rc = dalloc(&d_ws, R * ws_row / sizeof(float)))) return rc;
+  if ((rc = dalloc(&d_ring, static_cast<size_t>(RING_ROWS) * max_slots))) return rc;
+  if ((rc = dalloc(&d_ring_ctr, 1)) || (rc = dalloc(&d_ring_cur, 1))) return rc;
+  RLB_CUDA(cudaMemset(d_ring, 0xff, sizeof(int32_t) * RING_ROWS * max_slots));
+  RLB_CUDA(cudaMemset(d_ring_ctr, 0, sizeof(int32_t)));
+  RLB_CUDA(cudaMallocHost(reinterpret_cast<void**>(&h_ring),
+                          sizeof(int32_t) * RING_ROWS * static_cast<size_t>(max_slots)));
+  stage_cap = static_cast<size_t>(max_slots) * max_seq;
+  RLB_CUDA(cudaMallocHost(reinterpret_cast<void**>(&h_stage), sizeof(int) * 5 * stage_cap));
+
+  // RoPE table in double precision, stored fp32 (cos, sin).
+  const int half = D / 2;
+  std::vector<float2> rope(static_cast<size_t>(max_seq) * half);
+  for (int p = 0; p < max_seq; ++p)
+    for (int j = 0; j < half; ++j) {
+      const double inv = std::pow(static_cast<double>(m.rope_theta), -2.0 * j / D);
+      const double a = static_cast<double>(static_cast<float>(p * inv));
+      rope[static_cast<size_t>(p) * half + j] = make_float2(static_cast<float>(std::cos(a)),
+                                                            static_cast<float>(std::sin(a)));
+    }
+  if ((rc = dalloc(&d_rope, rope.size()))) return rc;
+  RLB_CUDA(cudaMemcpy(d_rope, rope.data(), rope.size() * sizeof(float2), cudaMemcpyHostToDevice));
+
+  if ((rc = gemm_prepare())) return rc;
+  if ((rc = make_kmajor_map(&m_xn, d_xn, R, H, 128))) return rc;
+  if ((rc = make_kmajor_map(&m_attn, d_attn, R, NQ * D, 128))) return rc;
+  if ((rc = make_kmajor_map(&m_act, d_act, R, F, 128))) return rc;
+  return bind_arena();
+}
+
+int rlb_instance::bind_arena() {
+  // carve order: paper_2510_19225_b200/shapes.py engine_layout()
+  int64_t off = 0;
+  auto put = [&](int64_t elems) {
+    bf16* p = reinterpret_cast<bf16*>(arena + off);
+    off = (off + 2 * elems + 255) / 256 * 256;
+    return p;
+  };
+  embed = put(static_cast<int64_t>(V) * H);
+  L.resize(m.layers);
+  int rc;
+  for (int i = 0; i < m.layers; ++i) {
+    LayerW& w = L[i];
+    w.ln1 = put(H);
+    w.wqkv = put(static_cast<int64_t>(QKV) * H);
+    w.bqkv = put(QKV);
+    w.wo = put(static_cast<int64_t>(H) * NQ * D);
+    w.ln2 = put(H);
+    w.wgu = put(static_cast<int64_t>(2) * F * H);
+    w.wdown = put(static_cast<int64_t>(H) * F);
+    if ((rc = make_kmajor_map(&w.m_qkv, w.wqkv, QKV, H, BN_QKV))) return rc;
+    if ((rc = make_kmajor_map(&w.m_o, w.wo, H, NQ * D, BN_O))) return rc;
+    if ((rc = make_kmajor_map(&w.m_gu, w.wgu, 2 * F, H, BN_GU))) return rc;
+    if ((rc = make_kmajor_map(&w.m_down, w.wdown, H, F, BN_DOWN))) return rc;
+  }
+  norm = put(H);
+  lm_head = m.tied ? embed : put(static_cast<int64_t>(V) * H);
+  RLB_CHECK(off == arena_bytes, RLB_ERR_STATE, "arena carve mismatch");
+  return make_kmajor_map(&m_lm, lm_head, V, H, BN_LM);
+}
+
+int rlb_instance::forward_layers(int R) {
+  int rc;
+  if ((rc = embed_launch(embed, H, d_row_tok, R, d_h, st))) return rc;
+  for (int l = 0; l < m.layers; ++l) {
+    const LayerW& w = L[l];
+    bf16* kv_l = kv + layer_stride * l;
+    if ((rc = rmsnorm_launch(d_h, H, nullptr, R, w.ln1, H, m.rms_eps, d_xn, H, st))) return rc;
+    GemmParams p{R, QKV, H, w.bqkv, d_qkv, QKV};
+    if ((rc = gemm_launch(m_xn, w.m_qkv, BN_QKV, EPI_BF16, p, st))) return rc;
+    if ((rc = rope_append_launch(d_qkv, QKV, d_row_slot, d_row_pos, R, d_rope, NQ, NKV, D, d_q,
+                                 NQ * D, kv_l, d_bt, pps, st)))
+      return rc;
+    AttnArgs a{d_q, NQ * D, kv_l, d_bt, pps, d_row_slot, d_row_pos, R, NQ, NKV, D, max_splits,
+               d_ws, d_attn, NQ * D};
+    if ((rc = attention_launch(a, st))) return rc;
+    GemmParams po{R, H, NQ * D, nullptr, d_h, H};
+    if ((rc = gemm_launch(m_attn, w.m_o, BN_O, EPI_RESADD, po, st))) return rc;
+    if ((rc = rmsnorm_launch(d_h, H, nullptr, R, w.ln2, H, m.rms_eps, d_xn, H, st))) return rc;
+    GemmParams pg{R, 2 * F, H, nullptr, d_act, F};
+    if ((rc = gemm_launch(m_xn, w.m_gu, BN_GU, EPI_SWIGLU, pg, st))) return rc;
+    GemmParams pd{R, H, F, nullptr, d_h, H};
+    if ((rc = gemm_launch(m_act, w.m_down, BN_DOWN, EPI_RESADD, pd, st))) return rc;
+  }
+  return RLB_OK;
+}
+
+// Final norm over the rows listed in d_logit_src, lm_head, and (optionally)
+// argmax + append into the slots listed in d_logit_slot.
+int rlb_instance::head(int Lrows, bool append) {
+  if (Lrows <= 0) return RLB_OK;
+  int rc;
+  if ((rc = rmsnorm_launch(d_h, H, d_logit_src, Lrows, norm, H, m.rms_eps, d_xn, H, st))) return rc;
+  GemmParams p{Lrows, V, H, nullptr, d_logits, V};
+  if ((rc = gemm_launch(m_xn, m_lm, BN_LM, EPI_F32, p, st))) return rc;
+  if (!append) return RLB_OK;
+  return argmax_append_launch(d_logits, V, Lrows, d_logit_slot, d_seq_tokens, d_seq_len,
+                              d_seq_target, max_seq, d_ring, d_ring_cur, max_slots, st);
+}
+
+int rlb_instance::decode_step_launch(int R) {
+  int rc;
+  if ((rc = decode_prepare_launch(d_dec_slots, R, d_seq_tokens, d_seq_len, max_seq, d_row_tok,
+                                  d_row_pos, d_row_slot, d_logit_src, d_logit_slot, d_ring_ctr,
+                                  d_ring_cur, st)))
+    return rc;
+  if ((rc = forward_layers(R))) return rc;
+  return head(R, true);
+}
+
+int rlb_instance::upload_slots() {
+  if (!slots_dirty) return RLB_OK;
+  RLB_CUDA(cudaMemcpyAsync(d_seq_len, h_seq_len.data(), sizeof(int32_t) * max_slots,
+                           cudaMemcpyHostToDevice, st));
+  RLB_CUDA(cudaMemcpyAsync(d_seq_target, h_seq_target.data(), sizeof(int32_t) * max_slots,
+                           cudaMemcpyHostToDevice, st));
+  RLB_CUDA(cudaMemcpyAsync(d_bt, h_bt.data(), sizeof(int) * h_bt.size(), cudaMemcpyHostToDevice, st));
+  RLB_CUDA(cudaStreamSynchronize(st));  // host vectors are pageable; keep them stable
+  slots_dirty = false;
+  return RLB_OK;
+}
+
+void rlb_instance::release(Req* r) {
+  if (r->slot >= 0) {
+    const int s = r->slot;
+    const int total = r->n_prompt + r->target_len;
+    const int np = (total + PAGE - 1) / PAGE;
+    for (int i = 0; i < np; ++i) free_pages.push_back(h_bt[static_cast<size_t>(s) * pps + i]);
+    slot_req[s] = nullptr;
+    h_seq_len[s] = 1;
+    h_seq_target[s] = 0;
+    free_slots.push_back(s);
+    slots_dirty = true;
+    r->slot = -1;
+  }
+}
+
+// Admit pending requests (FIFO) into free slots, then run the varlen prefill
+// over prompt + prefix of every newly admitted request.
+int rlb_instance::admit_and_prefill(int* rows_run) {
+  *rows_run = 0;
+  std::vector<Req*> admitted;
+  while (!pending.empty() && !free_slots.empty()) {
+    Req* r = pending.front();
+    const int total = r->n_prompt + r->target_len;
+    const int np = (total + PAGE - 1) / PAGE;
+    if (static_cast<int>(free_pages.size()) < np) break;
+    pending.pop_front();
+    const int s = free_slots.back();
+    free_slots.pop_back();
+    r->slot = s;
+    slot_req[s] = r;
+    for (int i = 0; i < np; ++i) {
+      h_bt[static_cast<size_t>(s) * pps + i] = free_pages.back();
+      free_pages.pop_back();
+    }
+    h_seq_len[s] = static_cast<int32_t>(r->tokens.size());
+    h_seq_target[s] = total;
+    slots_dirty = true;
+    if (!r->complete()) admitted.push_back(r);
+  }
+  int rc;
+  if ((rc = upload_slots())) return rc;
+  if (admitted.empty()) return RLB_OK;
+
+  // rows: (tok, pos, slot); logits for each sequence's last row.
+  size_t total_rows = 0;
+  for (Req* r : admitted) total_rows += r->tokens.size();
+  RLB_CHECK(total_rows <= stage_cap, RLB_ERR_CAPACITY, "prefill staging overflow");
+  int* tok = h_stage;
+  int* pos = h_stage + stage_cap;
+  int* slot = h_stage + 2 * stage_cap;
+  int* lsrc = h_stage + 3 * stage_cap;
+  int* lslot = h_stage + 4 * stage_cap;
+  size_t at = 0;
+  for (Req* r : admitted)
+    for (size_t i = 0; i < r->tokens.size(); ++i, ++at) {
+      tok[at] = r->tokens[i];
+      pos[at] = static_cast<int>(i);
+      slot[at] = r->slot;
+    }
+  size_t beg = 0;
+  size_t ri = 0;          // request whose rows are being placed
+  size_t rrow = 0;        // rows of admitted[ri] already placed
+  while (beg < total_rows) {
+    const size_t n = std::min<size_t>(prefill_rows, total_rows - beg);
+    // logits rows: sequences whose last row falls inside [beg, beg+n)
+    int nl = 0;
+    size_t cursor = beg;
+    while (ri < admitted.size()) {
+      const size_t left = admitted[ri]->tokens.size() - rrow;
+      if (cursor + left <= beg + n) {
+        lsrc[beg + nl] = static_cast<int>(cursor + left - 1 - beg);
+        lslot[beg + nl] = admitted[ri]->slot;
+        ++nl;
+        cursor += left;
+        ++ri;
+        rrow = 0;
+      } else {
+        rrow += beg + n - cursor;
+        break;
+      }
+    }
+    RLB_CUDA(cudaMemcpyAsync(d_row_tok, tok + beg, n * sizeof(int), cudaMemcpyHostToDevice, st));
+    RLB_CUDA(cudaMemcpyAsync(d_row_pos, pos + beg, n * sizeof(int), cudaMemcpyHostToDevice, st));
+    RLB_CUDA(cudaMemcpyAsync(d_row_slot, slot + beg, n * sizeof(int), cudaMemcpyHostToDevice, st));
+    if (nl) {
+      RLB_CUDA(cudaMemcpyAsync(d_logit_src, lsrc + beg, nl * sizeof(int), cudaMemcpyHostToDevice, st));
+      RLB_CUDA(cudaMemcpyAsync(d_logit_slot, lslot + beg, nl * sizeof(int), cudaMemcpyHostToDevice, st));
+    }
+    if ((rc = seed_tokens_launch(d_row_tok, d_row_pos, d_row_slot, static_cast<int>(n), d_seq_tokens,
+                                 max_seq, st)))
+      return rc;
+    if ((rc = ring_advance_launch(d_ring_ctr, d_ring_cur, st))) return rc;
+    if ((rc = forward_layers(static_cast<int>(n)))) return rc;
+    if ((rc = head(nl, true))) return rc;
+    beg += n;
+  }
+  for (Req* r : admitted) r->prefilled = true;
+  *rows_run = static_cast<int>(total_rows);
+  return RLB_OK;
+}
+
+int rlb_instance::run_decode(int steps, int* steps_run) {
+  *steps_run = 0;
+  int rc;
+  while (*steps_run < steps) {
+    dec_list.clear();
+    int min_left = 1 << 30;
+    for (int s = 0; s < max_slots; ++s) {
+      Req* r = slot_req[s];
+      if (r && r->prefilled && h_seq_len[s] < h_seq_target[s]) {
+        dec_list.push_back(s);
+        min_left = std::min(min_left, h_seq_target[s] - h_seq_len[s]);
+      }
+    }
+    const int R = static_cast<int>(dec_list.size());
+    if (R == 0) break;
+    RLB_CUDA(cudaMemcpyAsync(d_dec_slots, dec_list.data(), R * sizeof(int), cudaMemcpyHostToDevice, st));
+    int burst = std::min(steps - *steps_run, min_left);
+    const int gs = e.graph_steps;
+    while (burst > 0) {
+      if (gs > 0 && burst >= gs) {
+        auto it = graphs.find(R);
+        if (it == graphs.end()) {
+          cudaGraph_t g;
+          RLB_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+          for (int k = 0; k < gs; ++k)
+            if ((rc = decode_step_launch(R))) {
+              cudaStreamEndCapture(st, &g);
+              return rc;
+            }
+          RLB_CUDA(cudaStreamEndCapture(st, &g));
+          cudaGraphExec_t ge;
+          RLB_CUDA(cudaGraphInstantiate(&ge, g, 0));
+          RLB_CUDA(cudaGraphDestroy(g));
+          it = graphs.emplace(R, ge).first;
+        }
+        RLB_CUDA(cudaGraphLaunch(it->second, st));
+        burst -= gs;
+        *steps_run += gs;
+        for (int s : dec_list) h_seq_len[s] += gs;
+      } else {
+        if ((rc = decode_step_launch(R))) return rc;
+        burst -= 1;
+        *steps_run += 1;
+        for (int s : dec_list) h_seq_len[s] += 1;
+      }
+    }
+  }
+  return RLB_OK;
+}
+
+// Pull the token ring to the host, extend each request's host mirror and fill
+// the caller's batch.  Completed requests free their slot and pages.
+int rlb_instance::flush(rlb_token_batch* out) {
+  int32_t rows = 0;
+  RLB_CUDA(cudaMemcpyAsync(&rows, d_ring_ctr, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+  RLB_CUDA(cudaStreamSynchronize(st));
+  if (rows > 0) {
+    RLB_CUDA(cudaMemcpyAsync(h_ring, d_ring, sizeof(int32_t) * rows * static_cast<size_t>(max_slots),
+                             cudaMemcpyDeviceToHost, st));
+    RLB_CUDA(cudaMemsetAsync(d_ring, 0xff, sizeof(int32_t) * rows * static_cast<size_t>(max_slots), st));
+    RLB_CUDA(cudaMemsetAsync(d_ring_ctr, 0, sizeof(int32_t), st));
+    RLB_CUDA(cudaStreamSynchronize(st));
+    for (int row = 0; row < rows; ++row) {
+      const int32_t* rr = h_ring + static_cast<size_t>(row) * max_slots;
+      for (int s = 0; s < max_slots; ++s)
+        if (rr[s] >= 0 && slot_req[s]) slot_req[s]->tokens.push_back(rr[s]);
+    }
+  }
+  // the device length is authoritative; keep the mirror equal to it
+  for (int s = 0; s < max_slots; ++s)
+    if (slot_req[s]) h_seq_len[s] = static_cast<int32_t>(slot_req[s]->tokens.size());
+  int n = 0;
+  int64_t nt = 0;
+  std::vector<Req*> finished;
+  for (int s = 0; s < max_slots; ++s) {
+    Req* r = slot_req[s];
+    if (!r) continue;
+    const int newc = r->generated() - r->reported;
+    const bool done = r->complete();
+    if (newc <= 0 && !done) continue;
+    if (out) {
+      RLB_CHECK(n < out->cap_entries && nt + newc <= out->cap_tokens, RLB_ERR_CAPACITY,
+                "token batch capacity exceeded");
+      out->keys[n] = r->key;
+      out->counts[n] = newc;
+      out->done[n] = done ? 1 : 0;
+      std::memcpy(out->tokens + nt, r->tokens.data() + r->n_prompt + r->reported,
+                  sizeof(int32_t) * newc);
+    }
+    ++n;
+    nt += newc;
+    r->reported += newc;
+    if (done) finished.push_back(r);
+  }
+  for (Req* r : finished) {
+    release(r);
+    reqs.erase(r->key);
+    delete r;
+  }
+  if (out) {
+    out->n_entries = n;
+    out->n_tokens = nt;
+  }
+  return RLB_OK;
+}
+
+// ====================================================================== C ABI
+
+extern "C" {
+
+const char* rlb_last_error(void) { return g_err.c_str(); }
+
+int rlb_instance_create(int device, const rlb_model_cfg* model, const rlb_engine_cfg* engine,
+                        rlb_instance** out) {
+  RLB_CHECK(model && engine && out, RLB_ERR_ARG, "null argument");
+  rlb_instance* h = new rlb_instance();
+  h->device = device;
+  h->m = *model;
+  h->e = *engine;
+  const int rc = h->init();
+  if (rc) {
+    const std::string msg = g_err;
+    delete h;
+    g_err = msg;
+    return rc;
+  }
+  *out = h;
+  return RLB_OK;
+}
+
+int rlb_instance_destroy(rlb_instance* h) {
+  delete h;
+  return RLB_OK;
+}
+
+int rlb_load_weights(rlb_instance* h, const void* const* hf_ptrs, int32_t n_tensors,
+                     uint64_t version, rlb_pull_stats* stats) {
+  RLB_CHECK(h && hf_ptrs, RLB_ERR_ARG, "null argument");
+  RLB_CHECK(!h->has_weights || version >= h->version, RLB_ERR_ARG,
+            "weight version " + std::to_string(version) + " < " + std::to_string(h->version));
+  RLB_CUDA(cudaSetDevice(h->device));
+  RLB_CUDA(cudaEventRecord(h->ev0, h->st));
+  int rc = relayout_copy(h->m, hf_ptrs, n_tensors, h->arena, h->st);
+  if (rc) return rc;
+  RLB_CUDA(cudaEventRecord(h->ev1, h->st));
+  RLB_CUDA(cudaEventSynchronize(h->ev1));
+  float ms = 0.f;
+  RLB_CUDA(cudaEventElapsedTime(&ms, h->ev0, h->ev1));
+  if (stats) {
+    stats->bytes = h->arena_bytes;
+    int64_t moved = 0;
+    std::vector<Segment> segs;
+    relayout_segments(h->m, &segs);
+    for (const Segment& s : segs) moved += s.bytes;
+    stats->bytes = moved;
+    stats->seconds = ms * 1e-3;
+  }
+  h->version = version;
+  h->has_weights = true;
+  return RLB_OK;
+}
+
+int rlb_weights_arena(rlb_instance* h, void** arena, int64_t* bytes) {
+  RLB_CHECK(h, RLB_ERR_ARG, "null handle");
+  if (arena) *arena = h->arena;
+  if (bytes) *bytes = h->arena_bytes;
+  return RLB_OK;
+}
+
+static int submit_one(rlb_instance* h, uint64_t key, const int32_t* toks, int32_t n_prompt,
+                      int32_t n_total, int32_t target_len) {
+  RLB_CHECK(n_prompt >= 1, RLB_ERR_ARG, "empty prompt");
+  RLB_CHECK(target_len >= 1 && n_total - n_prompt <= target_len, RLB_ERR_ARG,
+            "prefix longer than target_len");
+  RLB_CHECK(n_prompt + target_len <= h->max_seq, RLB_ERR_CAPACITY,
+            "prompt + target_len exceeds max_seq_len");
+  RLB_CHECK(h->reqs.find(key) == h->reqs.end(), RLB_ERR_STATE,
+            "duplicate request key " + std::to_string(key));
+  for (int32_t i = 0; i < n_total; ++i)
+    RLB_CHECK(toks[i] >= 0 && toks[i] < h->V, RLB_ERR_ARG, "token id out of vocabulary");
+  Req* r = new Req();
+  r->key = key;
+  r->tokens.assign(toks, toks + n_total);
+  r->n_prompt = n_prompt;
+  r->target_len = target_len;
+  r->reported = n_total - n_prompt;  // the prefix is already known to the caller
+  h->reqs[key] = r;
+  h->pending.push_back(r);
+  return RLB_OK;
+}
+
+int rlb_submit(rlb_instance* h, uint64_t key, const int32_t* prompt, int32_t n_prompt,
+               const int32_t* prefix, int32_t n_prefix, int32_t target_len) {
+  RLB_CHECK(h && prompt && (n_prefix == 0 || prefix), RLB_ERR_ARG, "null argument");
+  std::vector<int32_t> all(prompt, prompt + n_prompt);
+  if (n_prefix > 0) all.insert(all.end(), prefix, prefix + n_prefix);
+  return submit_one(h, key, all.data(), n_prompt, n_prompt + n_prefix, target_len);
+}
+
+int rlb_submit_varlen(rlb_instance* h, int32_t n, const uint64_t* keys, const int32_t* tokens,
+                      const int64_t* cu_lens, const int32_t* n_prompt, const int32_t* target_len) {
+  RLB_CHECK(h && keys && tokens && cu_lens && n_prompt && target_len, RLB_ERR_ARG, "null argument");
+  for (int32_t i = 0; i < n; ++i) {
+    const int rc = submit_one(h, keys[i], tokens + cu_lens[i], n_prompt[i],
+                              static_cast<int32_t>(cu_lens[i + 1] - cu_lens[i]), target_len[i]);
+    if (rc) return rc;
+  }
+  return RLB_OK;
+}
+
+int rlb_step(rlb_instance* h, int32_t n_steps, rlb_token_batch* out) {
+  RLB_CHECK(h, RLB_ERR_ARG, "null handle");
+  RLB_CHECK(h->has_weights, RLB_ERR_STATE, "no weights loaded");
+  RLB_CUDA(cudaSetDevice(h->device));
+  int rows = 0, steps = 0, rc;
+  if ((rc = h->admit_and_prefill(&rows))) return rc;
+  const int max_steps = RING_ROWS - 1 - (rows + h->prefill_rows - 1) / h->prefill_rows;
+  if ((rc = h->run_decode(std::min<int>(std::max(n_steps, 0), max_steps), &steps))) return rc;
+  if ((rc = h->flush(out))) return rc;
+  if (out) {
+    out->steps_run = steps;
+    out->prefill_rows = rows;
+  }
+  return RLB_OK;
+}
+
+int rlb_cancel(rlb_instance* h, uint64_t key, int32_t* out_tokens, int32_t cap, int32_t* out_len) {
+  RLB_CHECK(h, RLB_ERR_ARG, "null handle");
+  auto it = h->reqs.find(key);
+  RLB_CHECK(it != h->reqs.end(), RLB_ERR_STATE, "unknown request key " + std::to_string(key));
+  Req* r = it->second;
+  const int gen = r->generated();
+  if (out_len) *out_len = gen;
+  if (out_tokens) {
+    RLB_CHECK(gen <= cap, RLB_ERR_CAPACITY, "cancel output capacity");
+    std::memcpy(out_tokens, r->tokens.data() + r->n_prompt, sizeof(int32_t) * gen);
+  }
+  if (r->slot < 0) {
+    for (auto p = h->pending.begin(); p != h->pending.end(); ++p)
+      if (*p == r) {
+        h->pending.erase(p);
+        break;
+      }
+  }
+  h->release(r);
+  h->reqs.erase(it);
+  delete r;
+  return RLB_OK;
+}
+
+int rlb_export_partials(rlb_instance* h, int32_t n, const uint64_t* keys, int32_t* out_tokens,
+                        int64_t cap, int64_t* out_cu_lens, int32_t* out_n_prompt) {
+  RLB_CHECK(h && keys && out_tokens && out_cu_lens, RLB_ERR_ARG, "null argument");
+  RLB_CUDA(cudaSetDevice(h->device));
+  std::vector<Req*> rs(n);
+  std::vector<int64_t> cu(n + 1, 0);
+  for (int32_t i = 0; i < n; ++i) {
+    auto it = h->reqs.find(keys[i]);
+    RLB_CHECK(it != h->reqs.end(), RLB_ERR_STATE, "unknown request key " + std::to_string(keys[i]));
+    rs[i] = it->second;
+    cu[i + 1] = cu[i] + static_cast<int64_t>(rs[i]->tokens.size());
+    if (out_n_prompt) out_n_prompt[i] = rs[i]->n_prompt;
+  }
+  RLB_CHECK(cu[n] <= cap, RLB_ERR_CAPACITY, "export output capacity");
+  std::memcpy(out_cu_lens, cu.data(), sizeof(int64_t) * (n + 1));
+  // device-resident sequences: one gather kernel into a contiguous buffer
+  std::vector<int> dslots;
+  std::vector<int64_t> dcu(1, 0);
+  std::vector<int32_t> didx;
+  for (int32_t i = 0; i < n; ++i) {
+    if (rs[i]->slot >= 0) {
+      dslots.push_back(rs[i]->slot);
+      dcu.push_back(dcu.back() + static_cast<int64_t>(rs[i]->tokens.size()));
+      didx.push_back(i);
+    } else {
+      std::memcpy(out_tokens + cu[i], rs[i]->tokens.data(), sizeof(int32_t) * rs[i]->tokens.size());
+    }
+  }
+  if (!dslots.empty()) {
+    int* d_slots = nullptr;
+    int64_t* d_cu = nullptr;
+    int32_t* d_out = nullptr;
+    const int nd = static_cast<int>(dslots.size());
+    RLB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&d_slots), nd * sizeof(int), h->st));
+    RLB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&d_cu), (nd + 1) * sizeof(int64_t), h->st));
+    RLB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&d_out), std::max<int64_t>(dcu.back(), 1) * 4, h->st));
+    RLB_CUDA(cudaMemcpyAsync(d_slots, dslots.data(), nd * sizeof(int), cudaMemcpyHostToDevice, h->st));
+    RLB_CUDA(cudaMemcpyAsync(d_cu, dcu.data(), (nd + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, h->st));
+    int rc = gather_seqs_launch(d_slots, d_cu, nd, h->d_seq_tokens, h->max_seq, d_out, h->st);
+    if (rc) return rc;
+    std::vector<int32_t> buf(dcu.back());
+    RLB_CUDA(cudaMemcpyAsync(buf.data(), d_out, dcu.back() * 4, cudaMemcpyDeviceToHost, h->st));
+    RLB_CUDA(cudaFreeAsync(d_slots, h->st));
+    RLB_CUDA(cudaFreeAsync(d_cu, h->st));
+    RLB_CUDA(cudaFreeAsync(d_out, h->st));
+    RLB_CUDA(cudaStreamSynchronize(h->st));
+    for (int k = 0; k < nd; ++k) {
+      const int i = didx[k];
+      std::memcpy(out_tokens + cu[i], buf.data() + dcu[k], sizeof(int32_t) * (dcu[k + 1] - dcu[k]));
+    }
+  }
+  return RLB_OK;
+}
+
+int rlb_status(rlb_instance* h, int32_t* m_pending, int32_t* m_exec, uint64_t* weight_version) {
+  RLB_CHECK(h, RLB_ERR_ARG, "null handle");
+  if (m_pending) *m_pending = static_cast<int32_t>(h->pending.size());
+  if (m_exec) *m_exec = static_cast<int32_t>(h->reqs.size() - h->pending.size());
+  if (weight_version) *weight_version = h->version;
+  return RLB_OK;
+}
+
+int rlb_score(rlb_instance* h, const int32_t* tokens, int32_t n, float* out_logits) {
+  RLB_CHECK(h && tokens && out_logits, RLB_ERR_ARG, "null argument");
+  RLB_CHECK(h->has_weights, RLB_ERR_STATE, "no weights loaded");
+  RLB_CHECK(n >= 1 && n <= h->max_seq, RLB_ERR_CAPACITY, "score length exceeds max_seq_len");
+  RLB_CHECK(!h->free_slots.empty(), RLB_ERR_CAPACITY, "no free slot for scoring");
+  const int np = (n + PAGE - 1) / PAGE;
+  RLB_CHECK(static_cast<int>(h->free_pages.size()) >= np, RLB_ERR_CAPACITY, "no free pages for scoring");
+  RLB_CUDA(cudaSetDevice(h->device));
+  Req tmp;
+  tmp.n_prompt = n;
+  tmp.target_len = 0;
+  const int s = h->free_slots.back();
+  h->free_slots.pop_back();
+  tmp.slot = s;
+  for (int i = 0; i < np; ++i) {
+    h->h_bt[static_cast<size_t>(s) * h->pps + i] = h->free_pages.back();
+    h->free_pages.pop_back();
+  }
+  h->slots_dirty = true;
+  int rc = h->upload_slots();
+  if (rc) return rc;
+  int* tok = h->h_stage;
+  int* pos = h->h_stage + h->stage_cap;
+  int* slot = h->h_stage + 2 * h->stage_cap;
+  int* lsrc = h->h_stage + 3 * h->stage_cap;
+  for (int i = 0; i < n; ++i) {
+    tok[i] = tokens[i];
+    pos[i] = i;
+    slot[i] = s;
+  }
+  for (int beg = 0; beg < n && rc == 0; beg += h->prefill_rows) {
+    const int cnt = std::min(h->prefill_rows, n - beg);
+    RLB_CUDA(cudaMemcpyAsync(h->d_row_tok, tok + beg, cnt * 4, cudaMemcpyHostToDevice, h->st));
+    RLB_CUDA(cudaMemcpyAsync(h->d_row_pos, pos + beg, cnt * 4, cudaMemcpyHostToDevice, h->st));
+    RLB_CUDA(cudaMemcpyAsync(h->d_row_slot, slot + beg, cnt * 4, cudaMemcpyHostToDevice, h->st));
+    if ((rc = h->forward_layers(cnt))) break;
+    for (int lb = 0; lb < cnt; lb += h->max_slots) {
+      const int ln = std::min(h->max_slots, cnt - lb);
+      for (int i = 0; i < ln; ++i) lsrc[i] = lb + i;
+      RLB_CUDA(cudaMemcpyAsync(h->d_logit_src, lsrc, ln * 4, cudaMemcpyHostToDevice, h->st));
+      if ((rc = h->head(ln, false))) break;
+      RLB_CUDA(cudaMemcpyAsync(out_logits + static_cast<size_t>(beg + lb) * h->V, h->d_logits,
+                               sizeof(float) * ln * static_cast<size_t>(h->V),
+                               cudaMemcpyDeviceToHost, h->st));
+      RLB_CUDA(cudaStreamSynchronize(h->st));
+    }
+  }
+  h->release(&tmp);
+  if (rc) return rc;
+  RLB_CUDA(cudaStreamSynchronize(h->st));
+  return RLB_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,68 @@
+// Internal declarations shared by the librlb translation units.
+#pragma once
+#include "../../include/rlb.h"
+#include "common.cuh"
+
+#include <vector>
+
+namespace rlb {
+
+constexpr int PAGE = 64;      // tokens per KV page
+constexpr int SPLIT = 256;    // fixed split-K boundary of decode attention (tokens)
+
+enum Epi { EPI_BF16 = 0, EPI_RESADD = 1, EPI_SWIGLU = 2, EPI_F32 = 3 };
+
+struct GemmParams {
+  int M, N, K;
+  const bf16* bias;
+  void* out;
+  int ldo;
+};
+
+int make_kmajor_map(CUtensorMap* map, const void* ptr, int64_t rows, int64_t k, int box_rows);
+int gemm_prepare();  // set smem attributes of every GEMM variant on the current device
+int gemm_launch(const CUtensorMap& a, const CUtensorMap& b, int block_n, int epi,
+                const GemmParams& p, cudaStream_t st);
+
+// ---- elementwise / attention launchers (kernels.cu) ----
+struct AttnArgs {
+  const bf16* q;  int ldq;          // rotated q rows [R][NQ*D]
+  const bf16* kv;                   // layer base [page][NKV][2][PAGE][D]
+  const int* block_table; int bt_stride;
+  const int* row_slot; const int* row_pos;
+  int R, NQ, NKV, D, max_splits;
+  float* ws;                        // [R][NQ][max_splits][D+2]
+  bf16* out; int ldo;
+};
+int attention_launch(const AttnArgs& a, cudaStream_t st);
+
+int embed_launch(const bf16* embed, int H, const int* tok, int R, float* h, cudaStream_t st);
+int rmsnorm_launch(const float* x, int ldx, const int* src_rows, int R, const bf16* w, int H,
+                   float eps, bf16* out, int ldo, cudaStream_t st);
+int rope_append_launch(const bf16* qkv, int ldqkv, const int* row_slot, const int* row_pos, int R,
+                       const float2* rope, int NQ, int NKV, int D, bf16* qout, int ldq, bf16* kv,
+                       const int* block_table, int bt_stride, cudaStream_t st);
+int argmax_append_launch(const float* logits, int V, int L, const int* logit_slot,
+                         int32_t* seq_tokens, int32_t* seq_len, const int32_t* seq_target,
+                         int max_seq, int32_t* ring, const int32_t* ring_cur, int max_slots,
+                         cudaStream_t st);
+int decode_prepare_launch(const int* dec_slots, int R, const int32_t* seq_tokens,
+                          const int32_t* seq_len, int max_seq, int* row_tok, int* row_pos,
+                          int* row_slot, int* logit_src, int* logit_slot, int32_t* ring_ctr,
+                          int32_t* ring_cur, cudaStream_t st);
+int seed_tokens_launch(const int* row_tok, const int* row_pos, const int* row_slot, int R,
+                       int32_t* seq_tokens, int max_seq, cudaStream_t st);
+int ring_advance_launch(int32_t* ring_ctr, int32_t* ring_cur, cudaStream_t st);
+int gather_seqs_launch(const int* slots, const int64_t* cu, int n, const int32_t* seq_tokens,
+                       int max_seq, int32_t* out, cudaStream_t st);
+
+// ---- weight pull (pull.cu) ----
+struct Segment { int32_t hf; int64_t src_off, dst_off, bytes; };
+void relayout_segments(const rlb_model_cfg& m, std::vector<Segment>* out);
+int64_t arena_bytes(const rlb_model_cfg& m);
+int32_t hf_count(const rlb_model_cfg& m);
+int relayout_copy(const rlb_model_cfg& m, const void* const* hf_ptrs, int32_t n, void* dst,
+                  cudaStream_t st);
+int copy_bytes(void* dst, const void* src, int64_t nbytes, cudaStream_t st);
+
+}  // namespace rlb

@@ -1,0 +1,468 @@
+// K1 paged split-K attention, K3 small fused kernels, K5 compaction, K6
+// response-buffer append.  Every kernel works on "token rows": a row is
+// (slot, position, token).  A decode step is one row per executing slot; a
+// varlen prefill (initial prompt or migration resume) is many rows per slot.
+// Each row's arithmetic depends only on the row's own inputs and its slot's
+// KV prefix -- never on which other rows share the launch -- so a sequence
+// rebuilt by prefill on another GPU continues bit-identically (SURVEY.md §7
+// hard part 2).
+#include "internal.h"
+
+namespace rlb {
+
+// ----------------------------------------------------------- attention --
+// One CTA = (row, kv head, split of SPLIT tokens).  The GQA group of G query
+// heads sharing the kv head is processed together so K/V are read once.
+//   phase A: scores s[g][t] = (q_g . k_t) * scale * log2(e); half-warp (D=128)
+//            or quarter-warp (D=64) per token, 128-bit K loads, fixed xor-tree
+//   phase B: per-head max / exp2 / sum over the split (warp per head)
+//   phase C: o[g] = sum_t p[g][t] v_t, warp w takes tokens t = w (mod 4),
+//            lanes own D/32 dims; the 4 warp partials are summed in order.
+// Splits are fixed 256-token windows of absolute position, so the reduction
+// tree is a function of the context length alone.
+template <int D>
+__global__ void __launch_bounds__(128) attn_split_kernel(AttnArgs a) {
+  constexpr int LPT = D / 8;   // lanes per token in phase A
+  constexpr int TPW = 32 / LPT;
+  constexpr int TPI = 4 * TPW; // tokens per CTA iteration
+  constexpr int DPL = D / 32;  // dims per lane in phase C
+  constexpr int GMAX = 8;
+  __shared__ float qs[GMAX][D];
+  __shared__ float sc[GMAX][SPLIT];
+  __shared__ float red[4][GMAX][D];
+  __shared__ float ml[GMAX][2];
+
+  const int sp = blockIdx.x, kvh = blockIdx.y, r = blockIdx.z;
+  const int n = a.row_pos[r] + 1;
+  const int t0 = sp * SPLIT;
+  if (t0 >= n) return;
+  const int nt = min(SPLIT, n - t0);
+  const int G = a.NQ / a.NKV;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int* bt = a.block_table + static_cast<size_t>(a.row_slot[r]) * a.bt_stride;
+  const size_t head_stride = static_cast<size_t>(2) * PAGE * D;   // K and V of one head
+  const size_t page_stride = head_stride * a.NKV;
+  const bf16* kvh_base = a.kv + static_cast<size_t>(kvh) * head_stride;
+  const float scale = rsqrtf(static_cast<float>(D)) * 1.4426950408889634f;
+
+  const bf16* qrow = a.q + static_cast<size_t>(r) * a.ldq + static_cast<size_t>(kvh) * G * D;
+  for (int i = tid; i < G * D; i += 128) qs[i / D][i % D] = __bfloat162float(qrow[i]);
+  __syncthreads();
+
+  // ---- phase A
+  const int sub = lane % LPT, tw = lane / LPT;
+  float qreg[GMAX][8];
+#pragma unroll
+  for (int g = 0; g < GMAX; ++g)
+#pragma unroll
+    for (int e = 0; e < 8; ++e) qreg[g][e] = g < G ? qs[g][sub * 8 + e] : 0.f;
+  constexpr int U = 4;
+  for (int base = 0; base < nt; base += TPI * U) {
+    uint4 kr[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int tl = base + u * TPI + warp * TPW + tw;
+      kr[u] = make_uint4(0, 0, 0, 0);
+      if (tl < nt) {
+        const int t = t0 + tl;
+        const bf16* kp = kvh_base + static_cast<size_t>(bt[t / PAGE]) * page_stride +
+                         static_cast<size_t>(t % PAGE) * D + sub * 8;
+        kr[u] = __ldg(reinterpret_cast<const uint4*>(kp));
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int tl = base + u * TPI + warp * TPW + tw;
+      const uint32_t kw[4] = {kr[u].x, kr[u].y, kr[u].z, kr[u].w};
+      float kf[8];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        kf[2 * i] = bf_lo(kw[i]);
+        kf[2 * i + 1] = bf_hi(kw[i]);
+      }
+#pragma unroll
+      for (int g = 0; g < GMAX; ++g) {
+        if (g >= G) break;
+        float acc = 0.f;
+#pragma unroll
+        for (int e = 0; e < 8; ++e) acc = __fmaf_rn(qreg[g][e], kf[e], acc);
+#pragma unroll
+        for (int off = LPT / 2; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+        if (sub == 0 && tl < nt) sc[g][tl] = acc * scale;
+      }
+    }
+  }
+  __syncthreads();
+
+  // ---- phase B
+  for (int g = warp; g < G; g += 4) {
+    float m = -INFINITY;
+    for (int t = lane; t < nt; t += 32) m = fmaxf(m, sc[g][t]);
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, off));
+    float l = 0.f;
+    for (int t = lane; t < nt; t += 32) {
+      const float pv = exp2f(sc[g][t] - m);
+      sc[g][t] = pv;
+      l += pv;
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) l += __shfl_xor_sync(0xffffffffu, l, off);
+    if (lane == 0) {
+      ml[g][0] = m;
+      ml[g][1] = l;
+    }
+  }
+  __syncthreads();
+
+  // ---- phase C
+  float acc[GMAX][DPL];
+#pragma unroll
+  for (int g = 0; g < GMAX; ++g)
+#pragma unroll
+    for (int e = 0; e < DPL; ++e) acc[g][e] = 0.f;
+  const bf16* vbase = kvh_base + static_cast<size_t>(PAGE) * D + lane * DPL;
+  for (int tb = warp; tb < nt; tb += 4 * U) {
+    float vf[U][DPL];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int tl = tb + 4 * u;
+#pragma unroll
+      for (int e = 0; e < DPL; ++e) vf[u][e] = 0.f;
+      if (tl < nt) {
+        const int t = t0 + tl;
+        const bf16* vp = vbase + static_cast<size_t>(bt[t / PAGE]) * page_stride +
+                         static_cast<size_t>(t % PAGE) * D;
+        if constexpr (DPL == 4) {
+          const uint2 w = __ldg(reinterpret_cast<const uint2*>(vp));
+          vf[u][0] = bf_lo(w.x);
+          vf[u][1] = bf_hi(w.x);
+          vf[u][2] = bf_lo(w.y);
+          vf[u][3] = bf_hi(w.y);
+        } else {
+          const uint32_t w = __ldg(reinterpret_cast<const uint32_t*>(vp));
+          vf[u][0] = bf_lo(w);
+          vf[u][1] = bf_hi(w);
+        }
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int tl = tb + 4 * u;
+      if (tl >= nt) break;
+#pragma unroll
+      for (int g = 0; g < GMAX; ++g) {
+        if (g >= G) break;
+        const float pv = sc[g][tl];
+#pragma unroll
+        for (int e = 0; e < DPL; ++e) acc[g][e] = __fmaf_rn(pv, vf[u][e], acc[g][e]);
+      }
+    }
+  }
+#pragma unroll
+  for (int g = 0; g < GMAX; ++g) {
+    if (g >= G) break;
+#pragma unroll
+    for (int e = 0; e < DPL; ++e) red[warp][g][lane * DPL + e] = acc[g][e];
+  }
+  __syncthreads();
+  const bool single = n <= SPLIT;
+  for (int i = tid; i < G * D; i += 128) {
+    const int g = i / D, d = i % D;
+    const float o = ((red[0][g][d] + red[1][g][d]) + red[2][g][d]) + red[3][g][d];
+    const int qh = kvh * G + g;
+    if (single) {
+      a.out[static_cast<size_t>(r) * a.ldo + qh * D + d] = __float2bfloat16_rn(o / ml[g][1]);
+    } else {
+      float* w = a.ws + ((static_cast<size_t>(r) * a.NQ + qh) * a.max_splits + sp) * (D + 2);
+      w[d] = o;
+      if (d == 0) {
+        w[D] = ml[g][0];
+        w[D + 1] = ml[g][1];
+      }
+    }
+  }
+}
+
+// Merge the per-split partials of rows longer than one split, splits in
+// increasing order.
+__global__ void attn_combine_kernel(AttnArgs a) {
+  const int qh = blockIdx.x, r = blockIdx.y, d = threadIdx.x;
+  const int n = a.row_pos[r] + 1;
+  const int ns = (n + SPLIT - 1) / SPLIT;
+  if (ns <= 1) return;
+  const int D = a.D;
+  const float* w = a.ws + (static_cast<size_t>(r) * a.NQ + qh) * a.max_splits * (D + 2);
+  float M = -INFINITY;
+  for (int s = 0; s < ns; ++s) M = fmaxf(M, w[s * (D + 2) + D]);
+  float L = 0.f, O = 0.f;
+  for (int s = 0; s < ns; ++s) {
+    const float c = exp2f(w[s * (D + 2) + D] - M);
+    L = __fmaf_rn(c, w[s * (D + 2) + D + 1], L);
+    O = __fmaf_rn(c, w[s * (D + 2) + d], O);
+  }
+  a.out[static_cast<size_t>(r) * a.ldo + qh * D + d] = __float2bfloat16_rn(O / L);
+}
+
+int attention_launch(const AttnArgs& a, cudaStream_t st) {
+  if (a.R <= 0) return RLB_OK;
+  RLB_CHECK(a.NQ % a.NKV == 0 && a.NQ / a.NKV <= 8, RLB_ERR_ARG, "GQA group must be <= 8");
+  dim3 grid(a.max_splits, a.NKV, a.R);
+  if (a.D == 128)
+    attn_split_kernel<128><<<grid, 128, 0, st>>>(a);
+  else if (a.D == 64)
+    attn_split_kernel<64><<<grid, 128, 0, st>>>(a);
+  else
+    RLB_CHECK(false, RLB_ERR_ARG, "head_dim must be 64 or 128");
+  RLB_CUDA(cudaGetLastError());
+  if (a.max_splits > 1) {
+    attn_combine_kernel<<<dim3(a.NQ, a.R), a.D, 0, st>>>(a);
+    RLB_CUDA(cudaGetLastError());
+  }
+  return RLB_OK;
+}
+
+// -------------------------------------------------------------- embed ----
+__global__ void embed_kernel(const bf16* __restrict__ embed, int H, const int* __restrict__ tok,
+                             float* __restrict__ h) {
+  const int r = blockIdx.x;
+  const bf16* e = embed + static_cast<size_t>(tok[r]) * H;
+  float* o = h + static_cast<size_t>(r) * H;
+  for (int i = threadIdx.x; i < H; i += blockDim.x) o[i] = __bfloat162float(e[i]);
+}
+
+int embed_launch(const bf16* embed, int H, const int* tok, int R, float* h, cudaStream_t st) {
+  if (R <= 0) return RLB_OK;
+  embed_kernel<<<R, 256, 0, st>>>(embed, H, tok, h);
+  RLB_CUDA(cudaGetLastError());
+  return RLB_OK;
+}
+
+// ------------------------------------------------------------ rmsnorm ----
+__global__ void __launch_bounds__(256) rmsnorm_kernel(const float* __restrict__ x, int ldx,
+                                                      const int* __restrict__ src_rows,
+                                                      const bf16* __restrict__ w, int H, float eps,
+                                                      bf16* __restrict__ out, int ldo) {
+  __shared__ float part[8];
+  const int ro = blockIdx.x;
+  const int ri = src_rows ? src_rows[ro] : ro;
+  const float* xr = x + static_cast<size_t>(ri) * ldx;
+  float ss = 0.f;
+  for (int i = threadIdx.x; i < H; i += 256) ss = __fmaf_rn(xr[i], xr[i], ss);
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, off);
+  if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = ss;
+  __syncthreads();
+  float tot = 0.f;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) tot += part[k];
+  const float inv = rsqrtf(tot / static_cast<float>(H) + eps);
+  bf16* orow = out + static_cast<size_t>(ro) * ldo;
+  for (int i = threadIdx.x; i < H; i += 256)
+    orow[i] = __float2bfloat16_rn((xr[i] * inv) * __bfloat162float(w[i]));
+}
+
+int rmsnorm_launch(const float* x, int ldx, const int* src_rows, int R, const bf16* w, int H,
+                   float eps, bf16* out, int ldo, cudaStream_t st) {
+  if (R <= 0) return RLB_OK;
+  rmsnorm_kernel<<<R, 256, 0, st>>>(x, ldx, src_rows, w, H, eps, out, ldo);
+  RLB_CUDA(cudaGetLastError());
+  return RLB_OK;
+}
+
+// -------------------------------------------------- rope + KV append -----
+// q heads: rotated into qout; k heads: rotated, written to the slot's page;
+// v heads: copied to the page.  rope[pos][j] = (cos, sin) of pos * theta^(-2j/D).
+__global__ void rope_append_kernel(const bf16* __restrict__ qkv, int ldqkv,
+                                   const int* __restrict__ row_slot,
+                                   const int* __restrict__ row_pos,
+                                   const float2* __restrict__ rope, int NQ, int NKV, int D,
+                                   bf16* __restrict__ qout, int ldq, bf16* __restrict__ kv,
+                                   const int* __restrict__ block_table, int bt_stride) {
+  const int r = blockIdx.x;
+  const int half = D / 2;
+  const int pos = row_pos[r];
+  const int page = block_table[static_cast<size_t>(row_slot[r]) * bt_stride + pos / PAGE];
+  const size_t head_stride = static_cast<size_t>(2) * PAGE * D;
+  bf16* kv_page = kv + static_cast<size_t>(page) * head_stride * NKV +
+                  static_cast<size_t>(pos % PAGE) * D;
+  const bf16* in = qkv + static_cast<size_t>(r) * ldqkv;
+  const float2* cs = rope + static_cast<size_t>(pos) * half;
+  const int total = (NQ + 2 * NKV) * half;
+  for (int i = threadIdx.x; i < total; i += blockDim.x) {
+    const int head = i / half, j = i % half;
+    const float x1 = __bfloat162float(in[head * D + j]);
+    const float x2 = __bfloat162float(in[head * D + j + half]);
+    if (head < NQ + NKV) {
+      const float2 c = cs[j];
+      const float y1 = __fmaf_rn(x1, c.x, -x2 * c.y);
+      const float y2 = __fmaf_rn(x2, c.x, x1 * c.y);
+      if (head < NQ) {
+        bf16* o = qout + static_cast<size_t>(r) * ldq + head * D;
+        o[j] = __float2bfloat16_rn(y1);
+        o[j + half] = __float2bfloat16_rn(y2);
+      } else {
+        bf16* o = kv_page + static_cast<size_t>(head - NQ) * head_stride;
+        o[j] = __float2bfloat16_rn(y1);
+        o[j + half] = __float2bfloat16_rn(y2);
+      }
+    } else {
+      bf16* o = kv_page + static_cast<size_t>(head - NQ - NKV) * head_stride +
+                static_cast<size_t>(PAGE) * D;
+      o[j] = in[head * D + j];
+      o[j + half] = in[head * D + j + half];
+    }
+  }
+}
+
+int rope_append_launch(const bf16* qkv, int ldqkv, const int* row_slot, const int* row_pos, int R,
+                       const float2* rope, int NQ, int NKV, int D, bf16* qout, int ldq, bf16* kv,
+                       const int* block_table, int bt_stride, cudaStream_t st) {
+  if (R <= 0) return RLB_OK;
+  rope_append_kernel<<<R, 256, 0, st>>>(qkv, ldqkv, row_slot, row_pos, rope, NQ, NKV, D, qout, ldq,
+                                        kv, block_table, bt_stride);
+  RLB_CUDA(cudaGetLastError());
+  return RLB_OK;
+}
+
+// ---------------------------------------------- argmax + response append --
+// Greedy token (lowest index on ties) of each logits row, appended to the
+// slot's device sequence buffer (K6) and to this step's row of the token ring
+// that the host flushes with one D2H copy.
+__global__ void __launch_bounds__(512) argmax_append_kernel(
+    const float* __restrict__ logits, int V, const int* __restrict__ logit_slot,
+    int32_t* __restrict__ seq_tokens, int32_t* __restrict__ seq_len,
+    const int32_t* __restrict__ seq_target, int max_seq, int32_t* __restrict__ ring,
+    const int32_t* __restrict__ ring_cur, int max_slots) {
+  __shared__ float sv[16];
+  __shared__ int si[16];
+  const int r = blockIdx.x;
+  const float* row = logits + static_cast<size_t>(r) * V;
+  float best = -INFINITY;
+  int idx = 0x7fffffff;
+  for (int i = threadIdx.x; i < V; i += 512) {
+    const float v = row[i];
+    if (v > best) {
+      best = v;
+      idx = i;
+    }
+  }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    const float ov = __shfl_xor_sync(0xffffffffu, best, off);
+    const int oi = __shfl_xor_sync(0xffffffffu, idx, off);
+    if (ov > best || (ov == best && oi < idx)) {
+      best = ov;
+      idx = oi;
+    }
+  }
+  if ((threadIdx.x & 31) == 0) {
+    sv[threadIdx.x >> 5] = best;
+    si[threadIdx.x >> 5] = idx;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int k = 1; k < 16; ++k)
+      if (sv[k] > best || (sv[k] == best && si[k] < idx)) {
+        best = sv[k];
+        idx = si[k];
+      }
+    const int s = logit_slot[r];
+    const int len = seq_len[s];
+    if (len < seq_target[s]) {
+      seq_tokens[static_cast<size_t>(s) * max_seq + len] = idx;
+      seq_len[s] = len + 1;
+      ring[static_cast<size_t>(*ring_cur) * max_slots + s] = idx;
+    }
+  }
+}
+
+int argmax_append_launch(const float* logits, int V, int L, const int* logit_slot,
+                         int32_t* seq_tokens, int32_t* seq_len, const int32_t* seq_target,
+                         int max_seq, int32_t* ring, const int32_t* ring_cur, int max_slots,
+                         cudaStream_t st) {
+  if (L <= 0) return RLB_OK;
+  argmax_append_kernel<<<L, 512, 0, st>>>(logits, V, logit_slot, seq_tokens, seq_len, seq_target,
+                                          max_seq, ring, ring_cur, max_slots);
+  RLB_CUDA(cudaGetLastError());
+  return RLB_OK;
+}
+
+// ------------------------------------------------------ decode prepare --
+__global__ void decode_prepare_kernel(const int* __restrict__ dec_slots, int R,
+                                      const int32_t* __restrict__ seq_tokens,
+                                      const int32_t* __restrict__ seq_len, int max_seq,
+                                      int* row_tok, int* row_pos, int* row_slot, int* logit_src,
+                                      int* logit_slot, int32_t* ring_ctr, int32_t* ring_cur) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i == 0) *ring_cur = (*ring_ctr)++;
+  if (i >= R) return;
+  const int s = dec_slots[i];
+  const int len = seq_len[s];
+  row_tok[i] = seq_tokens[static_cast<size_t>(s) * max_seq + len - 1];
+  row_pos[i] = len - 1;
+  row_slot[i] = s;
+  logit_src[i] = i;
+  logit_slot[i] = s;
+}
+
+int decode_prepare_launch(const int* dec_slots, int R, const int32_t* seq_tokens,
+                          const int32_t* seq_len, int max_seq, int* row_tok, int* row_pos,
+                          int* row_slot, int* logit_src, int* logit_slot, int32_t* ring_ctr,
+                          int32_t* ring_cur, cudaStream_t st) {
+  decode_prepare_kernel<<<(R + 255) / 256, 256, 0, st>>>(dec_slots, R, seq_tokens, seq_len,
+                                                        max_seq, row_tok, row_pos, row_slot,
+                                                        logit_src, logit_slot, ring_ctr, ring_cur);
+  RLB_CUDA(cudaGetLastError());
+  return RLB_OK;
+}
+
+// Prefill rows carry the request's prompt + prefix ids: copy them into the
+// slot's device sequence buffer (the response buffer the decode reads from).
+__global__ void seed_tokens_kernel(const int* __restrict__ row_tok, const int* __restrict__ row_pos,
+                                   const int* __restrict__ row_slot, int R,
+                                   int32_t* __restrict__ seq_tokens, int max_seq) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < R) seq_tokens[static_cast<size_t>(row_slot[i]) * max_seq + row_pos[i]] = row_tok[i];
+}
+
+int seed_tokens_launch(const int* row_tok, const int* row_pos, const int* row_slot, int R,
+                       int32_t* seq_tokens, int max_seq, cudaStream_t st) {
+  if (R <= 0) return RLB_OK;
+  seed_tokens_kernel<<<(R + 255) / 256, 256, 0, st>>>(row_tok, row_pos, row_slot, R, seq_tokens,
+                                                     max_seq);
+  RLB_CUDA(cudaGetLastError());
+  return RLB_OK;
+}
+
+__global__ void ring_advance_kernel(int32_t* ring_ctr, int32_t* ring_cur) {
+  *ring_cur = (*ring_ctr)++;
+}
+
+int ring_advance_launch(int32_t* ring_ctr, int32_t* ring_cur, cudaStream_t st) {
+  ring_advance_kernel<<<1, 1, 0, st>>>(ring_ctr, ring_cur);
+  RLB_CUDA(cudaGetLastError());
+  return RLB_OK;
+}
+
+// ---------------------------------------------------- K5 compaction ------
+// Gather each slot's prompt+generated ids into one contiguous varlen buffer
+// at the exclusive-scan offsets cu[i].
+__global__ void gather_seqs_kernel(const int* __restrict__ slots, const int64_t* __restrict__ cu,
+                                   const int32_t* __restrict__ seq_tokens, int max_seq,
+                                   int32_t* __restrict__ out) {
+  const int i = blockIdx.x;
+  const int64_t beg = cu[i], len = cu[i + 1] - cu[i];
+  const int32_t* src = seq_tokens + static_cast<size_t>(slots[i]) * max_seq;
+  for (int64_t k = threadIdx.x; k < len; k += blockDim.x) out[beg + k] = src[k];
+}
+
+int gather_seqs_launch(const int* slots, const int64_t* cu, int n, const int32_t* seq_tokens,
+                       int max_seq, int32_t* out, cudaStream_t st) {
+  if (n <= 0) return RLB_OK;
+  gather_seqs_kernel<<<n, 256, 0, st>>>(slots, cu, seq_tokens, max_seq, out);
+  RLB_CUDA(cudaGetLastError());
+  return RLB_OK;
+}
+
+}  // namespace rlb

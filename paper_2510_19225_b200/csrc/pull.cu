@@ -1,0 +1,244 @@
+// K7: pull-based weight transfer with the HF -> engine re-layout fused into
+// the copy.
+//
+// Reference: the pull is a modelled byte count shared over agent egress /
+// instance ingress (pkg/src/spotrl/transfer.py:87-170) and, in live mode, a
+// framed byte stream whose payload is the concatenated weights
+// (pkg/src/spotrl/protocol.py:92-157).  Here the bytes are real: a receiver
+// reads the trainer's bf16 tensors (local, or a peer GPU's memory mapped via
+// CUDA IPC so the loads travel over NVLink) and writes its engine arena.
+// Every re-layout piece is a contiguous byte range (fused QKV rows, 64-row
+// gate/up interleave blocks), so the whole pull is one chunked copy kernel:
+// 16-byte vector loads, 4 in flight per thread, L1 no-allocate.
+#include "internal.h"
+
+namespace rlb {
+
+static int64_t align256(int64_t x) { return (x + 255) / 256 * 256; }
+
+int32_t hf_count(const rlb_model_cfg& m) { return 1 + 12 * m.layers + 1 + (m.tied ? 0 : 1); }
+
+// Mirrors paper_2510_19225_b200/shapes.py engine_layout(): arena offsets of
+// each engine tensor in carve order.
+struct ArenaCursor {
+  int64_t off = 0;
+  int64_t put(int64_t elems) {
+    const int64_t at = off;
+    off = align256(off + 2 * elems);
+    return at;
+  }
+};
+
+int64_t arena_bytes(const rlb_model_cfg& m) {
+  ArenaCursor c;
+  const int64_t H = m.hidden, QD = static_cast<int64_t>(m.n_q_heads) * m.head_dim,
+                KD = static_cast<int64_t>(m.n_kv_heads) * m.head_dim, F = m.ffn;
+  c.put(static_cast<int64_t>(m.vocab) * H);
+  for (int i = 0; i < m.layers; ++i) {
+    c.put(H);
+    c.put((QD + 2 * KD) * H);
+    c.put(QD + 2 * KD);
+    c.put(H * QD);
+    c.put(H);
+    c.put(2 * F * H);
+    c.put(H * F);
+  }
+  c.put(H);
+  if (!m.tied) c.put(static_cast<int64_t>(m.vocab) * H);
+  return c.off;
+}
+
+void relayout_segments(const rlb_model_cfg& m, std::vector<Segment>* out) {
+  out->clear();
+  const int64_t H = m.hidden, QD = static_cast<int64_t>(m.n_q_heads) * m.head_dim,
+                KD = static_cast<int64_t>(m.n_kv_heads) * m.head_dim, F = m.ffn;
+  constexpr int64_t GU = 64;
+  ArenaCursor c;
+  int32_t hf = 0;
+  auto seg = [&](int32_t h, int64_t so, int64_t d, int64_t b) { out->push_back({h, so, d, b}); };
+  int64_t e = c.put(static_cast<int64_t>(m.vocab) * H);
+  seg(hf++, 0, e, 2 * m.vocab * H);
+  for (int i = 0; i < m.layers; ++i) {
+    const int64_t ln1 = c.put(H), wqkv = c.put((QD + 2 * KD) * H), bqkv = c.put(QD + 2 * KD),
+                  wo = c.put(H * QD), ln2 = c.put(H), wgu = c.put(2 * F * H), wd = c.put(H * F);
+    const int32_t base = hf;  // ln1 q qb k kb v vb o ln2 gate up down
+    seg(base + 0, 0, ln1, 2 * H);
+    seg(base + 1, 0, wqkv, 2 * QD * H);
+    seg(base + 2, 0, bqkv, 2 * QD);
+    seg(base + 3, 0, wqkv + 2 * QD * H, 2 * KD * H);
+    seg(base + 4, 0, bqkv + 2 * QD, 2 * KD);
+    seg(base + 5, 0, wqkv + 2 * (QD + KD) * H, 2 * KD * H);
+    seg(base + 6, 0, bqkv + 2 * (QD + KD), 2 * KD);
+    seg(base + 7, 0, wo, 2 * H * QD);
+    seg(base + 8, 0, ln2, 2 * H);
+    const int64_t blk = 2 * GU * H;
+    for (int64_t b = 0; b < F / GU; ++b) {
+      seg(base + 9, b * blk, wgu + (2 * b) * blk, blk);
+      seg(base + 10, b * blk, wgu + (2 * b + 1) * blk, blk);
+    }
+    seg(base + 11, 0, wd, 2 * H * F);
+    hf += 12;
+  }
+  seg(hf++, 0, c.put(H), 2 * H);
+  if (!m.tied) seg(hf++, 0, c.put(static_cast<int64_t>(m.vocab) * H), 2 * m.vocab * H);
+}
+
+struct CopyChunk {
+  const uint8_t* src;
+  uint8_t* dst;
+  int64_t bytes;
+};
+
+__device__ __forceinline__ uint4 ld_stream(const uint4* p) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+
+constexpr int COPY_THREADS = 512;
+constexpr int COPY_UNROLL = 4;
+constexpr int64_t CHUNK_BYTES = 1 << 20;
+
+__global__ void __launch_bounds__(COPY_THREADS) chunk_copy_kernel(const CopyChunk* __restrict__ ch,
+                                                                 int n) {
+  for (int c = blockIdx.x; c < n; c += gridDim.x) {
+    const CopyChunk k = ch[c];
+    const int64_t nv = k.bytes >> 4;
+    const uint4* s = reinterpret_cast<const uint4*>(k.src);
+    uint4* d = reinterpret_cast<uint4*>(k.dst);
+    int64_t i = threadIdx.x;
+    for (; i + (COPY_UNROLL - 1) * COPY_THREADS < nv; i += COPY_UNROLL * COPY_THREADS) {
+      uint4 v[COPY_UNROLL];
+#pragma unroll
+      for (int u = 0; u < COPY_UNROLL; ++u) v[u] = ld_stream(s + i + u * COPY_THREADS);
+#pragma unroll
+      for (int u = 0; u < COPY_UNROLL; ++u) d[i + u * COPY_THREADS] = v[u];
+    }
+    for (; i < nv; i += COPY_THREADS) d[i] = ld_stream(s + i);
+    // byte tail (never hit for bf16 tensors of the supported shapes)
+    for (int64_t b = (nv << 4) + threadIdx.x; b < k.bytes; b += COPY_THREADS) k.dst[b] = k.src[b];
+  }
+}
+
+static int run_chunks(const std::vector<CopyChunk>& chunks, cudaStream_t st) {
+  if (chunks.empty()) return RLB_OK;
+  CopyChunk* d = nullptr;
+  const size_t bytes = chunks.size() * sizeof(CopyChunk);
+  RLB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&d), bytes, st));
+  RLB_CUDA(cudaMemcpyAsync(d, chunks.data(), bytes, cudaMemcpyHostToDevice, st));
+  int sms = 148, dev = 0;
+  RLB_CUDA(cudaGetDevice(&dev));
+  RLB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  const int grid = static_cast<int>(std::min<size_t>(chunks.size(), static_cast<size_t>(sms) * 4));
+  chunk_copy_kernel<<<grid, COPY_THREADS, 0, st>>>(d, static_cast<int>(chunks.size()));
+  RLB_CUDA(cudaGetLastError());
+  RLB_CUDA(cudaFreeAsync(d, st));
+  return RLB_OK;
+}
+
+static void split_into(std::vector<CopyChunk>* v, const uint8_t* s, uint8_t* d, int64_t bytes) {
+  for (int64_t o = 0; o < bytes; o += CHUNK_BYTES)
+    v->push_back({s + o, d + o, std::min<int64_t>(CHUNK_BYTES, bytes - o)});
+}
+
+int relayout_copy(const rlb_model_cfg& m, const void* const* hf_ptrs, int32_t n, void* dst,
+                  cudaStream_t st) {
+  RLB_CHECK(n == hf_count(m), RLB_ERR_ARG,
+            "expected " + std::to_string(hf_count(m)) + " HF tensors, got " + std::to_string(n));
+  std::vector<Segment> segs;
+  relayout_segments(m, &segs);
+  std::vector<CopyChunk> chunks;
+  chunks.reserve(segs.size() + 16384);
+  for (const Segment& s : segs) {
+    const uint8_t* src = static_cast<const uint8_t*>(hf_ptrs[s.hf]) + s.src_off;
+    uint8_t* d = static_cast<uint8_t*>(dst) + s.dst_off;
+    RLB_CHECK(((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(d)) & 15) == 0,
+              RLB_ERR_ARG, "weight tensors must be 16-byte aligned");
+    split_into(&chunks, src, d, s.bytes);
+  }
+  return run_chunks(chunks, st);
+}
+
+int copy_bytes(void* dst, const void* src, int64_t nbytes, cudaStream_t st) {
+  RLB_CHECK(((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & 15) == 0,
+            RLB_ERR_ARG, "copy buffers must be 16-byte aligned");
+  std::vector<CopyChunk> chunks;
+  split_into(&chunks, static_cast<const uint8_t*>(src), static_cast<uint8_t*>(dst), nbytes);
+  return run_chunks(chunks, st);
+}
+
+}  // namespace rlb
+
+extern "C" {
+
+int64_t rlb_arena_bytes(const rlb_model_cfg* m) { return m ? rlb::arena_bytes(*m) : -1; }
+
+int32_t rlb_hf_tensor_count(const rlb_model_cfg* m) { return m ? rlb::hf_count(*m) : -1; }
+
+int64_t rlb_relayout_table(const rlb_model_cfg* m, int64_t* out, int64_t cap) {
+  if (!m) return RLB_ERR_ARG;
+  std::vector<rlb::Segment> segs;
+  rlb::relayout_segments(*m, &segs);
+  for (int64_t i = 0; i < static_cast<int64_t>(segs.size()) && i < cap; ++i) {
+    out[4 * i] = segs[i].hf;
+    out[4 * i + 1] = segs[i].src_off;
+    out[4 * i + 2] = segs[i].dst_off;
+    out[4 * i + 3] = segs[i].bytes;
+  }
+  return static_cast<int64_t>(segs.size());
+}
+
+int rlb_relayout_copy(int device, const rlb_model_cfg* m, const void* const* hf_ptrs,
+                      int32_t n_tensors, void* dst_arena, void* stream) {
+  RLB_CHECK(m && hf_ptrs && dst_arena, RLB_ERR_ARG, "null argument");
+  RLB_CUDA(cudaSetDevice(device));
+  return rlb::relayout_copy(*m, hf_ptrs, n_tensors, dst_arena, static_cast<cudaStream_t>(stream));
+}
+
+int rlb_copy_bytes(int device, void* dst, const void* src, int64_t nbytes, void* stream) {
+  RLB_CHECK(dst && src && nbytes >= 0, RLB_ERR_ARG, "bad copy arguments");
+  RLB_CUDA(cudaSetDevice(device));
+  return rlb::copy_bytes(dst, src, nbytes, static_cast<cudaStream_t>(stream));
+}
+
+int rlb_ipc_handle(const void* dev_ptr, uint8_t out_handle[64], int64_t* out_offset) {
+  // The handle names the whole allocation; report where dev_ptr sits in it
+  // (allocations from a caching allocator are sub-ranges of a segment).
+  typedef CUresult (*PFN_range)(CUdeviceptr*, size_t*, CUdeviceptr);
+  static PFN_range range_fn = nullptr;
+  if (range_fn == nullptr) {
+    void* fp = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &fp, cudaEnableDefault, &q) ==
+            cudaSuccess && q == cudaDriverEntryPointSuccess)
+      range_fn = reinterpret_cast<PFN_range>(fp);
+  }
+  RLB_CHECK(range_fn != nullptr, RLB_ERR_CUDA, "cuMemGetAddressRange unavailable");
+  CUdeviceptr base = 0;
+  size_t size = 0;
+  RLB_CHECK(range_fn(&base, &size, reinterpret_cast<CUdeviceptr>(dev_ptr)) == CUDA_SUCCESS,
+            RLB_ERR_CUDA, "cuMemGetAddressRange failed");
+  cudaIpcMemHandle_t h;
+  RLB_CUDA(cudaIpcGetMemHandle(&h, reinterpret_cast<void*>(base)));
+  memcpy(out_handle, &h, 64);
+  if (out_offset) *out_offset = static_cast<int64_t>(reinterpret_cast<CUdeviceptr>(dev_ptr) - base);
+  return RLB_OK;
+}
+
+int rlb_ipc_open(int device, const uint8_t handle[64], void** dev_ptr) {
+  RLB_CUDA(cudaSetDevice(device));
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle, 64);
+  RLB_CUDA(cudaIpcOpenMemHandle(dev_ptr, h, cudaIpcMemLazyEnablePeerAccess));
+  return RLB_OK;
+}
+
+int rlb_ipc_close(int device, void* dev_ptr) {
+  RLB_CUDA(cudaSetDevice(device));
+  RLB_CUDA(cudaIpcCloseMemHandle(dev_ptr));
+  return RLB_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,247 @@
+"""RolloutInstance: one B200 rollout instance behind the rlb_* C ABI.
+
+This is the object the reference's rollout-instance surfaces plug into:
+
+  reference                                           here
+  -------------------------------------------------   ------------------------------
+  protocol `generate{request_id, prompt_tokens,        generate(request_id, prompt_tokens,
+    prefix_tokens}` (pkg/src/spotrl/protocol.py:75-81)   prefix_tokens, target_len)
+  protocol `cancel{request_id}` (protocol.py:84-85)    cancel(request_id) -> generated ids
+  protocol `status{m_pending, m_exec, weight_version}` status() -> same dict
+    (protocol.py:26-31)
+  protocol `pull_weights{version, agent_endpoint}`     pull_weights(version, source)
+    (protocol.py:88-89)
+  GenUnit decode advance _sync_unit                    step(n_steps) -> [(request_id,
+    (pkg/src/spotrl/sim/engine.py:745-784)               new_token_ids, done)]
+  migrate_out keeping `generated`                      export_partials(request_ids)
+    (pkg/src/spotrl/manager.py:336-357)
+
+Unlike the reference, token ids are real (greedy decode of a Qwen2-shape
+decoder on the GPU) and the prefix in `generate` is honoured: the instance
+rebuilds the KV cache of prompt + prefix with one varlen prefill and the
+continuation is bit-identical to an uninterrupted run.
+"""
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from ._lib import check, i32, ptr
+from .shapes import ModelShape, hf_manifest
+
+
+@dataclass
+class PullResult:
+    version: int
+    bytes: int
+    seconds: float
+
+    @property
+    def gbps(self) -> float:
+        return self.bytes / self.seconds / 1e9 if self.seconds > 0 else float("inf")
+
+
+class RolloutInstance:
+    def __init__(self, shape: ModelShape, device: int = 0, *, max_slots: int = 512,
+                 max_seq_len: int = 1536, max_prefill_rows: int = 16384, graph_steps: int = 8,
+                 num_pages: int = 0):
+        self.shape = shape
+        self.device = device
+        self.max_slots = max_slots
+        self.max_seq_len = max_seq_len
+        self._cfg = _lib.ModelCfg.from_shape(shape)
+        ecfg = _lib.EngineCfg(max_slots, max_seq_len, num_pages, max_prefill_rows, graph_steps)
+        h = ctypes.c_void_p()
+        check(_lib.lib().rlb_instance_create(device, ctypes.byref(self._cfg), ctypes.byref(ecfg),
+                                             ctypes.byref(h)))
+        self._h = h
+        self._key_of: dict[str, int] = {}
+        self._rid_of: dict[int, str] = {}
+        self._next_key = 1
+        cap = max_slots
+        self._keys = np.zeros(cap, np.uint64)
+        self._counts = np.zeros(cap, np.int32)
+        self._done = np.zeros(cap, np.int32)
+        self._tok_cap = max_slots * 520
+        self._tokens = np.zeros(self._tok_cap, np.int32)
+        self.last_steps = 0
+        self.last_prefill_rows = 0
+
+    # -- lifecycle ---------------------------------------------------------
+
+    def close(self) -> None:
+        if self._h:
+            _lib.lib().rlb_instance_destroy(self._h)
+            self._h = None
+
+    def __del__(self):  # pragma: no cover - best effort
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # -- weights (pull) ----------------------------------------------------
+
+    def load_weights(self, hf_weights, version: int) -> PullResult:
+        """Pull an HF-layout weight set (dict name -> CUDA tensor, or a list of
+        device pointers in `hf_manifest` order) with the fused re-layout."""
+        if isinstance(hf_weights, dict):
+            ptrs = [int(hf_weights[name].data_ptr()) for name, _ in hf_manifest(self.shape)]
+        else:
+            ptrs = [int(p) for p in hf_weights]
+        arr = (ctypes.c_void_p * len(ptrs))(*ptrs)
+        stats = _lib.PullStats()
+        check(_lib.lib().rlb_load_weights(self._h, arr, len(ptrs), version, ctypes.byref(stats)))
+        return PullResult(version, stats.bytes, stats.seconds)
+
+    pull_weights = load_weights
+
+    def arena(self) -> tuple[int, int]:
+        p, n = ctypes.c_void_p(), ctypes.c_int64()
+        check(_lib.lib().rlb_weights_arena(self._h, ctypes.byref(p), ctypes.byref(n)))
+        return int(p.value or 0), int(n.value)
+
+    # -- requests ----------------------------------------------------------
+
+    def _key(self, request_id: str, create: bool) -> int:
+        key = self._key_of.get(request_id)
+        if key is None:
+            if not create:
+                raise KeyError(f"unknown request {request_id!r}")
+            key = self._next_key
+            self._next_key += 1
+            self._key_of[request_id] = key
+            self._rid_of[key] = request_id
+        return key
+
+    def _forget(self, request_id: str) -> None:
+        key = self._key_of.pop(request_id, None)
+        if key is not None:
+            self._rid_of.pop(key, None)
+
+    def generate(self, request_id: str, prompt_tokens, prefix_tokens=(), *, target_len: int) -> None:
+        """protocol `generate`: serve prompt + prefix, stop at target_len generated ids."""
+        if request_id in self._key_of:
+            raise ValueError(f"duplicate request {request_id!r}")
+        p, x = i32(prompt_tokens), i32(prefix_tokens)
+        key = self._key(request_id, create=True)
+        try:
+            check(_lib.lib().rlb_submit(self._h, key, ptr(p), len(p), ptr(x) if len(x) else None,
+                                        len(x), target_len))
+        except Exception:
+            self._forget(request_id)
+            raise
+
+    submit = generate
+
+    def generate_varlen(self, request_ids, tokens, cu_lens, n_prompt, target_len) -> None:
+        """Batched resume: sequence i = tokens[cu_lens[i]:cu_lens[i+1]], first n_prompt[i] prompt."""
+        n = len(request_ids)
+        keys = np.array([self._key(r, create=True) for r in request_ids], np.uint64)
+        t, cu = i32(tokens), np.ascontiguousarray(np.asarray(cu_lens, np.int64))
+        npr, tl = i32(n_prompt), i32(target_len)
+        check(_lib.lib().rlb_submit_varlen(self._h, n, ptr(keys), ptr(t), ptr(cu), ptr(npr), ptr(tl)))
+
+    def step(self, n_steps: int = 16) -> list[tuple[str, np.ndarray, bool]]:
+        """Admit + prefill pending requests, decode up to n_steps; returns the
+        new ids per request and whether it reached target_len (the request is
+        then retired from the instance)."""
+        b = _lib.TokenBatch(len(self._keys), self._tok_cap,
+                            self._keys.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64)),
+                            self._counts.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)),
+                            self._done.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)),
+                            self._tokens.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)), 0, 0, 0, 0)
+        self._ensure_token_cap(n_steps)
+        b.cap_tokens = self._tok_cap
+        b.tokens = self._tokens.ctypes.data_as(ctypes.POINTER(ctypes.c_int32))
+        check(_lib.lib().rlb_step(self._h, n_steps, ctypes.byref(b)))
+        self.last_steps, self.last_prefill_rows = b.steps_run, b.prefill_rows
+        out = []
+        off = 0
+        for i in range(b.n_entries):
+            key, cnt, done = int(self._keys[i]), int(self._counts[i]), bool(self._done[i])
+            rid = self._rid_of[key]
+            out.append((rid, self._tokens[off:off + cnt].copy(), done))
+            off += cnt
+            if done:
+                self._forget(rid)
+        return out
+
+    def _ensure_token_cap(self, n_steps: int) -> None:
+        need = self.max_slots * (n_steps + 2)
+        if need > self._tok_cap:
+            self._tok_cap = need
+            self._tokens = np.zeros(need, np.int32)
+
+    def cancel(self, request_id: str) -> list[int]:
+        """protocol `cancel`: drop the request, return its generated ids."""
+        key = self._key(request_id, create=False)
+        buf = np.zeros(self.max_seq_len, np.int32)
+        n = ctypes.c_int32()
+        check(_lib.lib().rlb_cancel(self._h, key, ptr(buf), len(buf), ctypes.byref(n)))
+        self._forget(request_id)
+        return buf[:n.value].tolist()
+
+    def export_partials(self, request_ids) -> list[tuple[list[int], list[int]]]:
+        """K5 compaction: (prompt ids, generated ids) of each request, gathered
+        on the device into one contiguous varlen buffer."""
+        n = len(request_ids)
+        if n == 0:
+            return []
+        keys = np.array([self._key(r, create=False) for r in request_ids], np.uint64)
+        cap = n * self.max_seq_len
+        toks = np.zeros(cap, np.int32)
+        cu = np.zeros(n + 1, np.int64)
+        npr = np.zeros(n, np.int32)
+        check(_lib.lib().rlb_export_partials(self._h, n, ptr(keys), ptr(toks), cap, ptr(cu), ptr(npr)))
+        out = []
+        for i in range(n):
+            seq = toks[cu[i]:cu[i + 1]]
+            out.append((seq[:npr[i]].tolist(), seq[npr[i]:].tolist()))
+        return out
+
+    def status(self) -> dict:
+        """protocol `status` payload."""
+        mp, me, wv = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_uint64()
+        check(_lib.lib().rlb_status(self._h, ctypes.byref(mp), ctypes.byref(me), ctypes.byref(wv)))
+        return {"m_pending": mp.value, "m_exec": me.value, "weight_version": int(wv.value)}
+
+    def score(self, tokens) -> np.ndarray:
+        """Teacher-forced fp32 logits [len(tokens), vocab] of one sequence."""
+        t = i32(tokens)
+        out = np.zeros((len(t), self.shape.vocab), np.float32)
+        check(_lib.lib().rlb_score(self._h, ptr(t), len(t), ptr(out)))
+        return out
+
+    # -- convenience -------------------------------------------------------
+
+    def run_to_completion(self, n_steps: int = 64) -> dict[str, list[int]]:
+        """Step until nothing is pending or executing; returns all ids generated."""
+        got: dict[str, list[int]] = {}
+        while True:
+            st = self.status()
+            if st["m_pending"] == 0 and st["m_exec"] == 0:
+                return got
+            for rid, toks, _ in self.step(n_steps):
+                got.setdefault(rid, []).extend(toks.tolist())
+
+
+def gemm(device: int, A, B, bias=None, out=None, epilogue: int = 0, block_n: int = 128):
+    """Kernel-level entry point rlb_gemm on torch CUDA tensors (parity tests)."""
+    import torch
+    M, K = A.shape
+    N = B.shape[0]
+    if out is None:
+        if epilogue == 0:
+            out = torch.empty(M, N, dtype=torch.bfloat16, device=A.device)
+        elif epilogue == 2:
+            out = torch.empty(M, N // 2, dtype=torch.bfloat16, device=A.device)
+        else:
+            out = torch.zeros(M, N, dtype=torch.float32, device=A.device)
+    check(_lib.lib().rlb_gemm(device, M, N, K, A.data_ptr(), B.data_ptr(),
+                              bias.data_ptr() if bias is not None else None, out.data_ptr(),
+                              epilogue, block_n))
+    return out

@@ -1,0 +1,144 @@
+"""End-to-end parity of the B200 rollout instance against the CPU fp32 oracle.
+
+* greedy rollouts, teacher-forced comparison (north_star rule, tolerance 2e-2
+  on logits for bf16 serving, exemption rate reported);
+* teacher-forced GPU logits vs oracle logits;
+* migrate/resume: export partials mid-rollout, resume on a fresh instance via
+  generate(prompt, prefix) -> bit-identical to the uninterrupted run;
+* weight pull: the engine arena equals the reference re-layout bytewise.
+"""
+import numpy as np
+import pytest
+import torch
+
+from paper_2510_19225_b200.shapes import TINY, small_shape, engine_layout, relayout_segments, hf_manifest
+from paper_2510_19225_b200.synth import synth_hf_weights, synth_prompts
+from oracle.qwen2_fp32 import Qwen2Fp32, teacher_forced_compare
+
+pytestmark = pytest.mark.gpu
+TOL_BF16 = 2e-2
+
+
+@pytest.fixture(scope="module")
+def cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    return 0
+
+
+def _instance(shape, w, **kw):
+    from paper_2510_19225_b200.instance import RolloutInstance
+    inst = RolloutInstance(shape, 0, **kw)
+    inst.load_weights(w, version=1)
+    return inst
+
+
+def _rollout(inst, prompts, target, n_steps=16, prefix=None):
+    for i, p in enumerate(prompts):
+        inst.generate(f"r{i}", p, prefix[i] if prefix else (), target_len=target)
+    got = inst.run_to_completion(n_steps)
+    return [(list(prefix[i]) if prefix else []) + got.get(f"r{i}", []) for i in range(len(prompts))]
+
+
+@pytest.fixture(scope="module")
+def tiny(cuda):
+    w = synth_hf_weights(TINY, seed=0, device="cuda")
+    oracle = Qwen2Fp32(TINY, w)
+    return w, oracle
+
+
+def test_tiny_rollout_teacher_forced(tiny):
+    """Config 1: 64 prompts (lengths U[16,64]) x 128 greedy tokens."""
+    w, oracle = tiny
+    prompts = synth_prompts(64, TINY.vocab, 16, 64, seed=1)
+    inst = _instance(TINY, w, max_slots=64, max_seq_len=256)
+    gen = _rollout(inst, prompts, 128)
+    assert all(len(g) == 128 for g in gen)
+    rep = teacher_forced_compare(oracle, prompts, gen, TOL_BF16)
+    print(f"tiny: {rep.steps} steps, exemption rate {rep.exemption_rate:.4f}")
+    assert rep.ok, rep.failures[:5]
+    assert rep.exemption_rate < 0.05
+
+
+def test_tiny_score_logits(tiny):
+    w, oracle = tiny
+    prompt = synth_prompts(1, TINY.vocab, 200, 200, seed=3)[0]
+    inst = _instance(TINY, w, max_slots=8, max_seq_len=512)
+    got = inst.score(prompt)
+    ref, _ = oracle.forward(prompt)
+    err = float(np.abs(got - ref.numpy()).max())
+    print("tiny score max |dlogit|", err)
+    assert err < 1e-2
+
+
+def test_tiny_migration_bit_exact(tiny):
+    """Kill mid-rollout, resume prompt+prefix on a fresh instance: identical ids."""
+    w, _ = tiny
+    prompts = synth_prompts(24, TINY.vocab, 16, 300, seed=5)
+    ref = _rollout(_instance(TINY, w, max_slots=32, max_seq_len=512), prompts, 160)
+    src = _instance(TINY, w, max_slots=32, max_seq_len=512)
+    for i, p in enumerate(prompts):
+        src.generate(f"r{i}", p, target_len=160)
+    partial = {}
+    for _ in range(5):   # 1 prefill + up to 5*13 decode steps
+        for rid, toks, _ in src.step(13):
+            partial.setdefault(rid, []).extend(toks.tolist())
+    ids = [f"r{i}" for i in range(len(prompts))]
+    exported = src.export_partials(ids)
+    for i, (pr, gen) in enumerate(exported):
+        assert pr == prompts[i]
+        assert gen == partial.get(f"r{i}", [])
+        assert 0 < len(gen) < 160
+    dst = _instance(TINY, w, max_slots=16, max_seq_len=512)   # smaller batch than the source
+    resumed = _rollout(dst, prompts, 160, prefix=[g for _, g in exported])
+    assert resumed == ref
+
+
+@pytest.fixture(scope="module")
+def mid(cuda):
+    shape = small_shape(layers=2, vocab=8192)
+    w = synth_hf_weights(shape, seed=0, device="cuda")
+    return shape, w, Qwen2Fp32(shape, w)
+
+
+def test_qwen_width_rollout_teacher_forced(mid):
+    shape, w, oracle = mid
+    prompts = synth_prompts(8, shape.vocab, 128, 384, seed=1)
+    inst = _instance(shape, w, max_slots=16, max_seq_len=1024)
+    gen = _rollout(inst, prompts, 64)
+    rep = teacher_forced_compare(oracle, prompts, gen, TOL_BF16)
+    print(f"1.5B-width 2L: {rep.steps} steps, exemption rate {rep.exemption_rate:.4f}")
+    assert rep.ok, rep.failures[:5]
+
+
+def test_qwen_width_migration_bit_exact(mid):
+    shape, w, _ = mid
+    prompts = synth_prompts(12, shape.vocab, 128, 384, seed=7)
+    ref = _rollout(_instance(shape, w, max_slots=16, max_seq_len=1024), prompts, 300)
+    src = _instance(shape, w, max_slots=16, max_seq_len=1024)
+    for i, p in enumerate(prompts):
+        src.generate(f"r{i}", p, target_len=300)
+    for _ in range(3):
+        src.step(37)
+    exported = src.export_partials([f"r{i}" for i in range(len(prompts))])
+    dst = _instance(shape, w, max_slots=5, max_seq_len=1024, max_prefill_rows=700)
+    resumed = _rollout(dst, prompts, 300, prefix=[g for _, g in exported])
+    assert resumed == ref
+
+
+def test_pull_bytewise(mid):
+    """The engine arena equals the host-side reference re-layout byte for byte."""
+    shape, w, _ = mid
+    inst = _instance(shape, w, max_slots=4, max_seq_len=256)
+    ptr_, nbytes = inst.arena()
+    arena = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
+    torch.cuda.synchronize()
+    from paper_2510_19225_b200 import _lib
+    _lib.check(_lib.lib().rlb_copy_bytes(0, arena.data_ptr(), ptr_, nbytes, None))
+    torch.cuda.synchronize()
+    names = [n for n, _ in hf_manifest(shape)]
+    expect = torch.zeros(nbytes, dtype=torch.uint8, device="cuda")
+    for hf, so, do, nb in relayout_segments(shape):
+        src = w[names[hf]].contiguous().view(torch.uint8).flatten()
+        expect[do:do + nb] = src[so:so + nb]
+    assert torch.equal(arena, expect)
