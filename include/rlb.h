@@ -138,6 +138,25 @@ int rlb_cancel(rlb_instance* h, uint64_t key, int32_t* out_tokens, int32_t cap,
 int rlb_export_partials(rlb_instance* h, int32_t n, const uint64_t* keys, int32_t* out_tokens,
                         int64_t cap, int64_t* out_cu_lens, int32_t* out_n_prompt);
 int rlb_status(rlb_instance* h, int32_t* m_pending, int32_t* m_exec, uint64_t* weight_version);
+/* Cumulative device-side accounting of an instance (CUDA events on its stream). */
+typedef struct {
+  double prefill_ms;       /* device time of admission + varlen prefill */
+  double decode_ms;        /* device time of decode steps */
+  int64_t prefill_rows;
+  int64_t decode_steps;
+  int64_t decode_rows;     /* sum over decode steps of executing sequences */
+  int64_t kernel_launches; /* librlb kernels launched (graph nodes counted) */
+  int64_t h2d_bytes;
+  int64_t d2h_bytes;
+} rlb_stats;
+int rlb_get_stats(rlb_instance* h, rlb_stats* out, int32_t reset);
+/* Re-launch one kernel of the last decode step `iters` times on the instance
+ * stream (rows, KV and weights as that step left them) and time it with CUDA
+ * events.  which: 0 attention (layer 0), 1 gate_up GEMM, 2 down GEMM, 3 QKV
+ * GEMM, 4 O GEMM, 5 lm_head GEMM.  Returns the average launch time and the
+ * algorithmic bytes (attention) or FLOPs (GEMMs) of one launch. */
+int rlb_profile_kernel(rlb_instance* h, int32_t which, int32_t iters, double* avg_ms,
+                       double* work_per_launch);
 /* Teacher-forced scoring: fp32 logits of every row of `tokens` (one sequence,
  * scratch slot), written to host out_logits[n][vocab]. */
 int rlb_score(rlb_instance* h, const int32_t* tokens, int32_t n, float* out_logits);

@@ -56,8 +56,22 @@ class PullStats(ctypes.Structure):
     _fields_ = [("bytes", ctypes.c_int64), ("seconds", ctypes.c_double)]
 
 
+class Stats(ctypes.Structure):
+    _fields_ = [("prefill_ms", ctypes.c_double), ("decode_ms", ctypes.c_double),
+                ("prefill_rows", ctypes.c_int64), ("decode_steps", ctypes.c_int64),
+                ("decode_rows", ctypes.c_int64), ("kernel_launches", ctypes.c_int64),
+                ("h2d_bytes", ctypes.c_int64), ("d2h_bytes", ctypes.c_int64)]
+
+    def as_dict(self) -> dict:
+        return {name: getattr(self, name) for name, _ in self._fields_}
+
+
 _P = ctypes.c_void_p
 _SIGS = {
+    "rlb_get_stats": (ctypes.c_int, [_P, ctypes.POINTER(Stats), ctypes.c_int32]),
+    "rlb_profile_kernel": (ctypes.c_int, [_P, ctypes.c_int32, ctypes.c_int32,
+                                          ctypes.POINTER(ctypes.c_double),
+                                          ctypes.POINTER(ctypes.c_double)]),
     "rlb_instance_create": (ctypes.c_int, [ctypes.c_int, ctypes.POINTER(ModelCfg),
                                            ctypes.POINTER(EngineCfg), ctypes.POINTER(_P)]),
     "rlb_instance_destroy": (ctypes.c_int, [_P]),

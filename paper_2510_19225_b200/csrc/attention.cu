@@ -1,0 +1,299 @@
+// K1: split-K paged decode attention on the tensor cores (mma.sync m16n8k16).
+//
+// One CTA = (token row, kv head, split of SPLIT=256 absolute positions); the
+// GQA group (G <= 8 query heads sharing the kv head) forms the M rows of the
+// MMA, so K and V of the split are read from HBM exactly once.  Warp w owns
+// the 64 positions [t0 + 64w, t0 + 64w + 64) -- one KV page -- and streams them
+// in 16-token chunks through a 3-stage cp.async ring (XOR-swizzled rows,
+// ldmatrix / ldmatrix.trans fragments, zero-fill past the context end):
+//     S = Q K^T (fp32) -> scale, mask -> online softmax in fixed chunk order
+//     -> P (bf16, reusing the S accumulator layout as the A operand) -> O += P V
+// The four warp partials are merged in warp order, then either normalised
+// (context <= one split) or written as (O, m, l) for the split combine.
+//
+// Determinism: every reduction order (quad shuffles, chunk order, warp order,
+// split order) is a function of the row's context length only, so a row gets
+// the same bits whether it is a decode row or one of the rows of a varlen
+// prefill -- the property migration resume relies on (SURVEY.md §7 part 2).
+#include "internal.h"
+
+namespace rlb {
+
+namespace {
+
+constexpr int WARPS = 4;
+constexpr int CHUNK = 16;          // tokens per pipeline stage
+constexpr int STAGES = 3;
+constexpr int WARP_TOKENS = SPLIT / WARPS;   // 64 = one page
+
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, bool valid) {
+  const int n = valid ? 16 : 0;   // zero-fill past the context end
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(n)
+               : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t (&r)[4]) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(addr));
+}
+__device__ __forceinline__ void ldsm_x4_t(uint32_t addr, uint32_t (&r)[4]) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(addr));
+}
+// D = A(16x16, rows 8..15 zero) * B(16x8) + D
+__device__ __forceinline__ void mma_bf16(float (&d)[4], uint32_t a0, uint32_t a2, uint32_t b0,
+                                         uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%0,%1,%2,%3};"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a0), "r"(0u), "r"(a2), "r"(0u), "r"(b0), "r"(b1));
+}
+
+}  // namespace
+
+template <int D>
+__global__ void __launch_bounds__(WARPS * 32, 2) attn_mma_kernel(AttnArgs a) {
+  constexpr int ROWB = D * 2;            // bytes per token row
+  constexpr int CPR = ROWB / 16;         // 16-byte chunks per row
+  constexpr int KSTEPS = D / 16;
+  constexpr int NT = D / 8;              // output n-tiles
+  constexpr int STAGE_BYTES = 2 * CHUNK * ROWB;      // K and V
+  constexpr int WARP_SMEM = STAGES * STAGE_BYTES;
+  extern __shared__ __align__(128) uint8_t smem[];
+
+  const int sp = blockIdx.x, kvh = blockIdx.y, r = blockIdx.z;
+  const int n = a.row_pos[r] + 1;
+  const int t0 = sp * SPLIT;
+  if (t0 >= n) return;
+  const int G = a.NQ / a.NKV;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int wt0 = t0 + warp * WARP_TOKENS;                 // first position of this warp
+  const int ntok = max(0, min(WARP_TOKENS, n - wt0));      // valid positions of this warp
+  const int nchunks = (ntok + CHUNK - 1) / CHUNK;
+  const float scale = rsqrtf(static_cast<float>(D)) * 1.4426950408889634f;
+
+  // Q fragments (A operand): row = lane/4 = head in the group (rows >= G are zero).
+  uint32_t qa[KSTEPS][2];
+  {
+    const int h = lane >> 2;
+    const bf16* qrow = a.q + static_cast<size_t>(r) * a.ldq + static_cast<size_t>(kvh * G + h) * D;
+#pragma unroll
+    for (int kk = 0; kk < KSTEPS; ++kk) {
+      const int c = kk * 16 + 2 * (lane & 3);
+      qa[kk][0] = h < G ? *reinterpret_cast<const uint32_t*>(qrow + c) : 0u;
+      qa[kk][1] = h < G ? *reinterpret_cast<const uint32_t*>(qrow + c + 8) : 0u;
+    }
+  }
+
+  uint8_t* wsm = smem + warp * WARP_SMEM;
+  const uint32_t wsm_u32 = smem_u32(wsm);
+  const bf16* kpage = nullptr;
+  if (ntok > 0) {
+    const int page = a.block_table[static_cast<size_t>(a.row_slot[r]) * a.bt_stride + wt0 / PAGE];
+    kpage = a.kv + (static_cast<size_t>(page) * a.NKV + kvh) * (2 * PAGE * D) +
+            static_cast<size_t>(wt0 % PAGE) * D;
+  }
+
+  auto issue = [&](int c) {
+    const uint32_t st = wsm_u32 + (c % STAGES) * STAGE_BYTES;
+#pragma unroll
+    for (int i = 0; i < (CHUNK * CPR) / 32; ++i) {
+      const int idx = i * 32 + lane;
+      const int row = idx / CPR, ch = idx % CPR;
+      const int tok = c * CHUNK + row;
+      const bool ok = tok < ntok;
+      const bf16* src = kpage + static_cast<size_t>(ok ? tok : 0) * D + ch * 8;
+      const uint32_t off = row * ROWB + ((ch ^ (row & 7)) << 4);
+      cp_async16(st + off, src, ok);
+      cp_async16(st + CHUNK * ROWB + off, src + PAGE * D, ok);
+    }
+  };
+
+  float o[NT][4];
+#pragma unroll
+  for (int t = 0; t < NT; ++t) o[t][0] = o[t][1] = o[t][2] = o[t][3] = 0.f;
+  float m_run = -INFINITY, l_run = 0.f;
+
+#pragma unroll
+  for (int c = 0; c < STAGES - 1; ++c) {
+    if (c < nchunks) issue(c);
+    cp_commit();
+  }
+  for (int c = 0; c < nchunks; ++c) {
+    if (c + STAGES - 1 < nchunks) issue(c + STAGES - 1);
+    cp_commit();
+    cp_wait<STAGES - 1>();
+    __syncwarp();
+    const uint32_t ks = wsm_u32 + (c % STAGES) * STAGE_BYTES;
+    const uint32_t vs = ks + CHUNK * ROWB;
+    // ---- S = Q K^T over 16 tokens (two n-tiles of 8)
+    float s[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
+    {
+      const int mi = lane >> 3, ri = lane & 7;
+      const int row = (mi >> 1) * 8 + ri;         // token within the chunk
+#pragma unroll
+      for (int kk = 0; kk < KSTEPS; ++kk) {
+        const int ch = 2 * kk + (mi & 1);
+        uint32_t b[4];
+        ldsm_x4(ks + row * ROWB + ((ch ^ (row & 7)) << 4), b);
+        mma_bf16(s[0], qa[kk][0], qa[kk][1], b[0], b[1]);
+        mma_bf16(s[1], qa[kk][0], qa[kk][1], b[2], b[3]);
+      }
+    }
+    // ---- online softmax (row = lane/4, columns 2*(lane%4)+{0,1} of each n-tile)
+    float mx = -INFINITY;
+#pragma unroll
+    for (int j = 0; j < 2; ++j)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int tok = c * CHUNK + 8 * j + 2 * (lane & 3) + e;
+        s[j][e] = tok < ntok ? s[j][e] * scale : -INFINITY;
+        mx = fmaxf(mx, s[j][e]);
+      }
+    mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
+    mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
+    const float m_new = fmaxf(m_run, mx);
+    const float corr = exp2f(m_run - m_new);
+    float p[2][2], rs = 0.f;
+#pragma unroll
+    for (int j = 0; j < 2; ++j)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        p[j][e] = exp2f(s[j][e] - m_new);
+        rs += p[j][e];
+      }
+    rs += __shfl_xor_sync(0xffffffffu, rs, 1);
+    rs += __shfl_xor_sync(0xffffffffu, rs, 2);
+    l_run = __fmaf_rn(l_run, corr, rs);
+    m_run = m_new;
+#pragma unroll
+    for (int t = 0; t < NT; ++t) {
+      o[t][0] *= corr;
+      o[t][1] *= corr;
+    }
+    const uint32_t pa0 = pack_bf2(p[0][0], p[0][1]);
+    const uint32_t pa2 = pack_bf2(p[1][0], p[1][1]);
+    // ---- O += P V   (V^T fragments via ldmatrix.trans)
+    {
+      const int mi = lane >> 3, ri = lane & 7;
+      const int row = (mi & 1) * 8 + ri;          // token within the chunk
+#pragma unroll
+      for (int dt = 0; dt < NT / 2; ++dt) {
+        const int ch = 2 * dt + (mi >> 1);
+        uint32_t b[4];
+        ldsm_x4_t(vs + row * ROWB + ((ch ^ (row & 7)) << 4), b);
+        mma_bf16(o[2 * dt], pa0, pa2, b[0], b[1]);
+        mma_bf16(o[2 * dt + 1], pa0, pa2, b[2], b[3]);
+      }
+    }
+    __syncwarp();
+  }
+  cp_wait<0>();
+  __syncthreads();
+
+  // ---- merge the 4 warp partials in warp order
+  float* red = reinterpret_cast<float*>(smem);            // [WARPS][8][D]
+  float* mls = red + WARPS * 8 * D;                        // [WARPS][8][2]
+  {
+    const int h = lane >> 2;
+#pragma unroll
+    for (int t = 0; t < NT; ++t) {
+      const int col = t * 8 + 2 * (lane & 3);
+      red[(warp * 8 + h) * D + col] = o[t][0];
+      red[(warp * 8 + h) * D + col + 1] = o[t][1];
+    }
+    if ((lane & 3) == 0) {
+      mls[(warp * 8 + h) * 2] = m_run;
+      mls[(warp * 8 + h) * 2 + 1] = l_run;
+    }
+  }
+  __syncthreads();
+  const bool single = n <= SPLIT;
+  for (int i = threadIdx.x; i < G * D; i += WARPS * 32) {
+    const int g = i / D, d = i % D;
+    float M = -INFINITY;
+#pragma unroll
+    for (int w = 0; w < WARPS; ++w) M = fmaxf(M, mls[(w * 8 + g) * 2]);
+    float L = 0.f, O = 0.f;
+#pragma unroll
+    for (int w = 0; w < WARPS; ++w) {
+      const float cw = exp2f(mls[(w * 8 + g) * 2] - M);
+      L = __fmaf_rn(cw, mls[(w * 8 + g) * 2 + 1], L);
+      O = __fmaf_rn(cw, red[(w * 8 + g) * D + d], O);
+    }
+    const int qh = kvh * G + g;
+    if (single) {
+      a.out[static_cast<size_t>(r) * a.ldo + qh * D + d] = __float2bfloat16_rn(O / L);
+    } else {
+      float* wsp = a.ws + ((static_cast<size_t>(r) * a.NQ + qh) * a.max_splits + sp) * (D + 2);
+      wsp[d] = O;
+      if (d == 0) {
+        wsp[D] = M;
+        wsp[D + 1] = L;
+      }
+    }
+  }
+}
+
+// Merge the per-split partials of rows longer than one split, in split order.
+__global__ void attn_combine_kernel(AttnArgs a) {
+  const int qh = blockIdx.x, r = blockIdx.y, d = threadIdx.x;
+  const int n = a.row_pos[r] + 1;
+  const int ns = (n + SPLIT - 1) / SPLIT;
+  if (ns <= 1) return;
+  const int D = a.D;
+  const float* w = a.ws + (static_cast<size_t>(r) * a.NQ + qh) * a.max_splits * (D + 2);
+  float M = -INFINITY;
+  for (int s = 0; s < ns; ++s) M = fmaxf(M, w[s * (D + 2) + D]);
+  float L = 0.f, O = 0.f;
+  for (int s = 0; s < ns; ++s) {
+    const float c = exp2f(w[s * (D + 2) + D] - M);
+    L = __fmaf_rn(c, w[s * (D + 2) + D + 1], L);
+    O = __fmaf_rn(c, w[s * (D + 2) + d], O);
+  }
+  a.out[static_cast<size_t>(r) * a.ldo + qh * D + d] = __float2bfloat16_rn(O / L);
+}
+
+template <int D>
+static int launch_attn(const AttnArgs& a, cudaStream_t st) {
+  constexpr int smem_pipe = WARPS * STAGES * 2 * CHUNK * D * 2;
+  constexpr int smem_red = WARPS * 8 * D * 4 + WARPS * 8 * 2 * 4;
+  constexpr int smem = smem_pipe > smem_red ? smem_pipe : smem_red;
+  static bool attr[64] = {false};
+  int dev = 0;
+  RLB_CUDA(cudaGetDevice(&dev));
+  if (!attr[dev & 63]) {
+    RLB_CUDA(cudaFuncSetAttribute(attn_mma_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    attr[dev & 63] = true;
+  }
+  attn_mma_kernel<D><<<dim3(a.max_splits, a.NKV, a.R), WARPS * 32, smem, st>>>(a);
+  RLB_CUDA(cudaGetLastError());
+  return RLB_OK;
+}
+
+int attention_launch(const AttnArgs& a, cudaStream_t st) {
+  if (a.R <= 0) return RLB_OK;
+  RLB_CHECK(a.NQ % a.NKV == 0 && a.NQ / a.NKV <= 8, RLB_ERR_ARG, "GQA group must be <= 8");
+  int rc;
+  if (a.D == 128)
+    rc = launch_attn<128>(a, st);
+  else if (a.D == 64)
+    rc = launch_attn<64>(a, st);
+  else
+    RLB_CHECK(false, RLB_ERR_ARG, "head_dim must be 64 or 128");
+  if (rc) return rc;
+  if (a.max_splits > 1) {
+    attn_combine_kernel<<<dim3(a.NQ, a.R), a.D, 0, st>>>(a);
+    RLB_CUDA(cudaGetLastError());
+  }
+  return RLB_OK;
+}
+
+}  // namespace rlb

@@ -111,7 +111,14 @@ struct rlb_instance {
   std::vector<int> dec_list;
   std::map<int, cudaGraphExec_t> graphs;
   int graph_built_for_version = -1;
-  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr, evA = nullptr, evB = nullptr;
+  rlb_stats stats{};
+  int last_R = 0;  // rows of the last decode step (for rlb_profile_kernel)
+  int64_t launches_per_forward(int R_logits) const {
+    // embed + per layer (2 norms, 4 GEMMs, rope, attention [+combine]) + head
+    return 1 + static_cast<int64_t>(m.layers) * (8 + (max_splits > 1 ? 1 : 0)) +
+           (R_logits > 0 ? 3 : 0);
+  }
 
   ~rlb_instance();
   int init();
@@ -139,6 +146,8 @@ rlb_instance::~rlb_instance() {
   if (h_ring) cudaFreeHost(h_ring);
   if (ev0) cudaEventDestroy(ev0);
   if (ev1) cudaEventDestroy(ev1);
+  if (evA) cudaEventDestroy(evA);
+  if (evB) cudaEventDestroy(evB);
   if (st) cudaStreamDestroy(st);
   for (auto& kv_ : reqs) delete kv_.second;
 }
@@ -173,6 +182,8 @@ int rlb_instance::init() {
   RLB_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
   RLB_CUDA(cudaEventCreate(&ev0));
   RLB_CUDA(cudaEventCreate(&ev1));
+  RLB_CUDA(cudaEventCreate(&evA));
+  RLB_CUDA(cudaEventCreate(&evB));
 
   arena_bytes = rlb::arena_bytes(m);
   int rc;
@@ -326,6 +337,7 @@ int rlb_instance::upload_slots() {
                            cudaMemcpyHostToDevice, st));
   RLB_CUDA(cudaMemcpyAsync(d_bt, h_bt.data(), sizeof(int) * h_bt.size(), cudaMemcpyHostToDevice, st));
   RLB_CUDA(cudaStreamSynchronize(st));  // host vectors are pageable; keep them stable
+  stats.h2d_bytes += static_cast<int64_t>(sizeof(int32_t)) * (2 * max_slots + h_bt.size());
   slots_dirty = false;
   return RLB_OK;
 }
@@ -424,8 +436,11 @@ int rlb_instance::admit_and_prefill(int* rows_run) {
     if ((rc = ring_advance_launch(d_ring_ctr, d_ring_cur, st))) return rc;
     if ((rc = forward_layers(static_cast<int>(n)))) return rc;
     if ((rc = head(nl, true))) return rc;
+    stats.h2d_bytes += static_cast<int64_t>(n) * 12 + static_cast<int64_t>(nl) * 8;
+    stats.kernel_launches += 2 + launches_per_forward(nl);
     beg += n;
   }
+  stats.prefill_rows += static_cast<int64_t>(total_rows);
   for (Req* r : admitted) r->prefilled = true;
   *rows_run = static_cast<int>(total_rows);
   return RLB_OK;
@@ -447,9 +462,16 @@ int rlb_instance::run_decode(int steps, int* steps_run) {
     const int R = static_cast<int>(dec_list.size());
     if (R == 0) break;
     RLB_CUDA(cudaMemcpyAsync(d_dec_slots, dec_list.data(), R * sizeof(int), cudaMemcpyHostToDevice, st));
+    stats.h2d_bytes += static_cast<int64_t>(R) * 4;
+    last_R = R;
     int burst = std::min(steps - *steps_run, min_left);
     const int gs = e.graph_steps;
+    const int64_t per_step = 1 + launches_per_forward(R);
     while (burst > 0) {
+      const int k = (gs > 0 && burst >= gs) ? gs : 1;
+      stats.decode_steps += k;
+      stats.decode_rows += static_cast<int64_t>(k) * R;
+      stats.kernel_launches += k * per_step;
       if (gs > 0 && burst >= gs) {
         auto it = graphs.find(R);
         if (it == graphs.end()) {
@@ -493,6 +515,7 @@ int rlb_instance::flush(rlb_token_batch* out) {
     RLB_CUDA(cudaMemsetAsync(d_ring, 0xff, sizeof(int32_t) * rows * static_cast<size_t>(max_slots), st));
     RLB_CUDA(cudaMemsetAsync(d_ring_ctr, 0, sizeof(int32_t), st));
     RLB_CUDA(cudaStreamSynchronize(st));
+    stats.d2h_bytes += 4 + static_cast<int64_t>(rows) * max_slots * 4;
     for (int row = 0; row < rows; ++row) {
       const int32_t* rr = h_ring + static_cast<size_t>(row) * max_slots;
       for (int s = 0; s < max_slots; ++s)
@@ -646,10 +669,18 @@ int rlb_step(rlb_instance* h, int32_t n_steps, rlb_token_batch* out) {
   RLB_CHECK(h->has_weights, RLB_ERR_STATE, "no weights loaded");
   RLB_CUDA(cudaSetDevice(h->device));
   int rows = 0, steps = 0, rc;
+  RLB_CUDA(cudaEventRecord(h->evA, h->st));
   if ((rc = h->admit_and_prefill(&rows))) return rc;
+  RLB_CUDA(cudaEventRecord(h->evB, h->st));
   const int max_steps = RING_ROWS - 1 - (rows + h->prefill_rows - 1) / h->prefill_rows;
   if ((rc = h->run_decode(std::min<int>(std::max(n_steps, 0), max_steps), &steps))) return rc;
+  RLB_CUDA(cudaEventRecord(h->ev1, h->st));
   if ((rc = h->flush(out))) return rc;
+  float ms_pre = 0.f, ms_dec = 0.f;
+  RLB_CUDA(cudaEventElapsedTime(&ms_pre, h->evA, h->evB));
+  RLB_CUDA(cudaEventElapsedTime(&ms_dec, h->evB, h->ev1));
+  if (rows > 0) h->stats.prefill_ms += ms_pre;
+  if (steps > 0) h->stats.decode_ms += ms_dec;
   if (out) {
     out->steps_run = steps;
     out->prefill_rows = rows;
@@ -740,6 +771,73 @@ int rlb_status(rlb_instance* h, int32_t* m_pending, int32_t* m_exec, uint64_t* w
   if (m_pending) *m_pending = static_cast<int32_t>(h->pending.size());
   if (m_exec) *m_exec = static_cast<int32_t>(h->reqs.size() - h->pending.size());
   if (weight_version) *weight_version = h->version;
+  return RLB_OK;
+}
+
+int rlb_get_stats(rlb_instance* h, rlb_stats* out, int32_t reset) {
+  RLB_CHECK(h && out, RLB_ERR_ARG, "null argument");
+  *out = h->stats;
+  if (reset) h->stats = rlb_stats{};
+  return RLB_OK;
+}
+
+int rlb_profile_kernel(rlb_instance* h, int32_t which, int32_t iters, double* avg_ms,
+                       double* work_per_launch) {
+  RLB_CHECK(h && avg_ms && work_per_launch && iters > 0, RLB_ERR_ARG, "bad argument");
+  RLB_CHECK(h->last_R > 0, RLB_ERR_STATE, "no decode step has run yet");
+  RLB_CUDA(cudaSetDevice(h->device));
+  const int R = h->last_R;
+  const LayerW& w = h->L[0];
+  const int NQ = h->NQ, D = h->D, H = h->H, F = h->F;
+  double work = 0.0;
+  auto launch = [&]() -> int {
+    switch (which) {
+      case 0: {
+        AttnArgs a{h->d_q, NQ * D, h->kv, h->d_bt, h->pps, h->d_row_slot, h->d_row_pos, R, NQ,
+                   h->NKV, D, h->max_splits, h->d_ws, h->d_attn, NQ * D};
+        return attention_launch(a, h->st);
+      }
+      case 1: return gemm_launch(h->m_xn, w.m_gu, BN_GU, EPI_SWIGLU,
+                                 GemmParams{R, 2 * F, H, nullptr, h->d_act, F}, h->st);
+      case 2: return gemm_launch(h->m_act, w.m_down, BN_DOWN, EPI_F32,
+                                 GemmParams{R, H, F, nullptr, h->d_logits, H}, h->st);
+      case 3: return gemm_launch(h->m_xn, w.m_qkv, BN_QKV, EPI_BF16,
+                                 GemmParams{R, h->QKV, H, w.bqkv, h->d_qkv, h->QKV}, h->st);
+      case 4: return gemm_launch(h->m_attn, w.m_o, BN_O, EPI_F32,
+                                 GemmParams{R, H, NQ * D, nullptr, h->d_logits, H}, h->st);
+      case 5: return gemm_launch(h->m_xn, h->m_lm, BN_LM, EPI_F32,
+                                 GemmParams{R, h->V, H, nullptr, h->d_logits, h->V}, h->st);
+    }
+    set_error("unknown kernel id");
+    return RLB_ERR_ARG;
+  };
+  switch (which) {
+    case 0: {  // K and V of every row's context, q in, attention out (bf16)
+      std::vector<int> rows(R);
+      RLB_CUDA(cudaMemcpy(rows.data(), h->d_row_pos, 4 * R, cudaMemcpyDeviceToHost));
+      double ctx = 0;
+      for (int i = 0; i < R; ++i) ctx += rows[i] + 1;
+      work = ctx * h->NKV * 2.0 * D * 2.0 + 2.0 * R * NQ * D * 2.0;
+      break;
+    }
+    case 1: work = 2.0 * R * 2.0 * F * H; break;
+    case 2: work = 2.0 * R * H * F; break;
+    case 3: work = 2.0 * R * h->QKV * H; break;
+    case 4: work = 2.0 * R * H * NQ * D; break;
+    case 5: work = 2.0 * R * h->V * static_cast<double>(H); break;
+    default: RLB_CHECK(false, RLB_ERR_ARG, "unknown kernel id");
+  }
+  int rc = launch();  // warm
+  if (rc) return rc;
+  RLB_CUDA(cudaEventRecord(h->ev0, h->st));
+  for (int i = 0; i < iters; ++i)
+    if ((rc = launch())) return rc;
+  RLB_CUDA(cudaEventRecord(h->ev1, h->st));
+  RLB_CUDA(cudaEventSynchronize(h->ev1));
+  float ms = 0.f;
+  RLB_CUDA(cudaEventElapsedTime(&ms, h->ev0, h->ev1));
+  *avg_ms = ms / iters;
+  *work_per_launch = work;
   return RLB_OK;
 }
 

@@ -1,4 +1,4 @@
-// K1 paged split-K attention, K3 small fused kernels, K5 compaction, K6
+// K3 small fused kernels, K5 compaction, K6
 // response-buffer append.  Every kernel works on "token rows": a row is
 // (slot, position, token).  A decode step is one row per executing slot; a
 // varlen prefill (initial prompt or migration resume) is many rows per slot.
@@ -9,218 +9,6 @@
 #include "internal.h"
 
 namespace rlb {
-
-// ----------------------------------------------------------- attention --
-// One CTA = (row, kv head, split of SPLIT tokens).  The GQA group of G query
-// heads sharing the kv head is processed together so K/V are read once.
-//   phase A: scores s[g][t] = (q_g . k_t) * scale * log2(e); half-warp (D=128)
-//            or quarter-warp (D=64) per token, 128-bit K loads, fixed xor-tree
-//   phase B: per-head max / exp2 / sum over the split (warp per head)
-//   phase C: o[g] = sum_t p[g][t] v_t, warp w takes tokens t = w (mod 4),
-//            lanes own D/32 dims; the 4 warp partials are summed in order.
-// Splits are fixed 256-token windows of absolute position, so the reduction
-// tree is a function of the context length alone.
-template <int D>
-__global__ void __launch_bounds__(128) attn_split_kernel(AttnArgs a) {
-  constexpr int LPT = D / 8;   // lanes per token in phase A
-  constexpr int TPW = 32 / LPT;
-  constexpr int TPI = 4 * TPW; // tokens per CTA iteration
-  constexpr int DPL = D / 32;  // dims per lane in phase C
-  constexpr int GMAX = 8;
-  __shared__ float qs[GMAX][D];
-  __shared__ float sc[GMAX][SPLIT];
-  __shared__ float red[4][GMAX][D];
-  __shared__ float ml[GMAX][2];
-
-  const int sp = blockIdx.x, kvh = blockIdx.y, r = blockIdx.z;
-  const int n = a.row_pos[r] + 1;
-  const int t0 = sp * SPLIT;
-  if (t0 >= n) return;
-  const int nt = min(SPLIT, n - t0);
-  const int G = a.NQ / a.NKV;
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int* bt = a.block_table + static_cast<size_t>(a.row_slot[r]) * a.bt_stride;
-  const size_t head_stride = static_cast<size_t>(2) * PAGE * D;   // K and V of one head
-  const size_t page_stride = head_stride * a.NKV;
-  const bf16* kvh_base = a.kv + static_cast<size_t>(kvh) * head_stride;
-  const float scale = rsqrtf(static_cast<float>(D)) * 1.4426950408889634f;
-
-  const bf16* qrow = a.q + static_cast<size_t>(r) * a.ldq + static_cast<size_t>(kvh) * G * D;
-  for (int i = tid; i < G * D; i += 128) qs[i / D][i % D] = __bfloat162float(qrow[i]);
-  __syncthreads();
-
-  // ---- phase A
-  const int sub = lane % LPT, tw = lane / LPT;
-  float qreg[GMAX][8];
-#pragma unroll
-  for (int g = 0; g < GMAX; ++g)
-#pragma unroll
-    for (int e = 0; e < 8; ++e) qreg[g][e] = g < G ? qs[g][sub * 8 + e] : 0.f;
-  constexpr int U = 4;
-  for (int base = 0; base < nt; base += TPI * U) {
-    uint4 kr[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int tl = base + u * TPI + warp * TPW + tw;
-      kr[u] = make_uint4(0, 0, 0, 0);
-      if (tl < nt) {
-        const int t = t0 + tl;
-        const bf16* kp = kvh_base + static_cast<size_t>(bt[t / PAGE]) * page_stride +
-                         static_cast<size_t>(t % PAGE) * D + sub * 8;
-        kr[u] = __ldg(reinterpret_cast<const uint4*>(kp));
-      }
-    }
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int tl = base + u * TPI + warp * TPW + tw;
-      const uint32_t kw[4] = {kr[u].x, kr[u].y, kr[u].z, kr[u].w};
-      float kf[8];
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        kf[2 * i] = bf_lo(kw[i]);
-        kf[2 * i + 1] = bf_hi(kw[i]);
-      }
-#pragma unroll
-      for (int g = 0; g < GMAX; ++g) {
-        if (g >= G) break;
-        float acc = 0.f;
-#pragma unroll
-        for (int e = 0; e < 8; ++e) acc = __fmaf_rn(qreg[g][e], kf[e], acc);
-#pragma unroll
-        for (int off = LPT / 2; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
-        if (sub == 0 && tl < nt) sc[g][tl] = acc * scale;
-      }
-    }
-  }
-  __syncthreads();
-
-  // ---- phase B
-  for (int g = warp; g < G; g += 4) {
-    float m = -INFINITY;
-    for (int t = lane; t < nt; t += 32) m = fmaxf(m, sc[g][t]);
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, off));
-    float l = 0.f;
-    for (int t = lane; t < nt; t += 32) {
-      const float pv = exp2f(sc[g][t] - m);
-      sc[g][t] = pv;
-      l += pv;
-    }
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) l += __shfl_xor_sync(0xffffffffu, l, off);
-    if (lane == 0) {
-      ml[g][0] = m;
-      ml[g][1] = l;
-    }
-  }
-  __syncthreads();
-
-  // ---- phase C
-  float acc[GMAX][DPL];
-#pragma unroll
-  for (int g = 0; g < GMAX; ++g)
-#pragma unroll
-    for (int e = 0; e < DPL; ++e) acc[g][e] = 0.f;
-  const bf16* vbase = kvh_base + static_cast<size_t>(PAGE) * D + lane * DPL;
-  for (int tb = warp; tb < nt; tb += 4 * U) {
-    float vf[U][DPL];
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int tl = tb + 4 * u;
-#pragma unroll
-      for (int e = 0; e < DPL; ++e) vf[u][e] = 0.f;
-      if (tl < nt) {
-        const int t = t0 + tl;
-        const bf16* vp = vbase + static_cast<size_t>(bt[t / PAGE]) * page_stride +
-                         static_cast<size_t>(t % PAGE) * D;
-        if constexpr (DPL == 4) {
-          const uint2 w = __ldg(reinterpret_cast<const uint2*>(vp));
-          vf[u][0] = bf_lo(w.x);
-          vf[u][1] = bf_hi(w.x);
-          vf[u][2] = bf_lo(w.y);
-          vf[u][3] = bf_hi(w.y);
-        } else {
-          const uint32_t w = __ldg(reinterpret_cast<const uint32_t*>(vp));
-          vf[u][0] = bf_lo(w);
-          vf[u][1] = bf_hi(w);
-        }
-      }
-    }
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int tl = tb + 4 * u;
-      if (tl >= nt) break;
-#pragma unroll
-      for (int g = 0; g < GMAX; ++g) {
-        if (g >= G) break;
-        const float pv = sc[g][tl];
-#pragma unroll
-        for (int e = 0; e < DPL; ++e) acc[g][e] = __fmaf_rn(pv, vf[u][e], acc[g][e]);
-      }
-    }
-  }
-#pragma unroll
-  for (int g = 0; g < GMAX; ++g) {
-    if (g >= G) break;
-#pragma unroll
-    for (int e = 0; e < DPL; ++e) red[warp][g][lane * DPL + e] = acc[g][e];
-  }
-  __syncthreads();
-  const bool single = n <= SPLIT;
-  for (int i = tid; i < G * D; i += 128) {
-    const int g = i / D, d = i % D;
-    const float o = ((red[0][g][d] + red[1][g][d]) + red[2][g][d]) + red[3][g][d];
-    const int qh = kvh * G + g;
-    if (single) {
-      a.out[static_cast<size_t>(r) * a.ldo + qh * D + d] = __float2bfloat16_rn(o / ml[g][1]);
-    } else {
-      float* w = a.ws + ((static_cast<size_t>(r) * a.NQ + qh) * a.max_splits + sp) * (D + 2);
-      w[d] = o;
-      if (d == 0) {
-        w[D] = ml[g][0];
-        w[D + 1] = ml[g][1];
-      }
-    }
-  }
-}
-
-// Merge the per-split partials of rows longer than one split, splits in
-// increasing order.
-__global__ void attn_combine_kernel(AttnArgs a) {
-  const int qh = blockIdx.x, r = blockIdx.y, d = threadIdx.x;
-  const int n = a.row_pos[r] + 1;
-  const int ns = (n + SPLIT - 1) / SPLIT;
-  if (ns <= 1) return;
-  const int D = a.D;
-  const float* w = a.ws + (static_cast<size_t>(r) * a.NQ + qh) * a.max_splits * (D + 2);
-  float M = -INFINITY;
-  for (int s = 0; s < ns; ++s) M = fmaxf(M, w[s * (D + 2) + D]);
-  float L = 0.f, O = 0.f;
-  for (int s = 0; s < ns; ++s) {
-    const float c = exp2f(w[s * (D + 2) + D] - M);
-    L = __fmaf_rn(c, w[s * (D + 2) + D + 1], L);
-    O = __fmaf_rn(c, w[s * (D + 2) + d], O);
-  }
-  a.out[static_cast<size_t>(r) * a.ldo + qh * D + d] = __float2bfloat16_rn(O / L);
-}
-
-int attention_launch(const AttnArgs& a, cudaStream_t st) {
-  if (a.R <= 0) return RLB_OK;
-  RLB_CHECK(a.NQ % a.NKV == 0 && a.NQ / a.NKV <= 8, RLB_ERR_ARG, "GQA group must be <= 8");
-  dim3 grid(a.max_splits, a.NKV, a.R);
-  if (a.D == 128)
-    attn_split_kernel<128><<<grid, 128, 0, st>>>(a);
-  else if (a.D == 64)
-    attn_split_kernel<64><<<grid, 128, 0, st>>>(a);
-  else
-    RLB_CHECK(false, RLB_ERR_ARG, "head_dim must be 64 or 128");
-  RLB_CUDA(cudaGetLastError());
-  if (a.max_splits > 1) {
-    attn_combine_kernel<<<dim3(a.NQ, a.R), a.D, 0, st>>>(a);
-    RLB_CUDA(cudaGetLastError());
-  }
-  return RLB_OK;
-}
 
 // -------------------------------------------------------------- embed ----
 __global__ void embed_kernel(const bf16* __restrict__ embed, int H, const int* __restrict__ tok,

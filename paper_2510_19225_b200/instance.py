@@ -216,6 +216,22 @@ class RolloutInstance:
         check(_lib.lib().rlb_score(self._h, ptr(t), len(t), ptr(out)))
         return out
 
+    KERNELS = {"attention": 0, "gate_up": 1, "down": 2, "qkv": 3, "o_proj": 4, "lm_head": 5}
+
+    def stats(self, reset: bool = False) -> dict:
+        """Cumulative device-time accounting (CUDA events on the instance stream)."""
+        s = _lib.Stats()
+        check(_lib.lib().rlb_get_stats(self._h, ctypes.byref(s), int(reset)))
+        return s.as_dict()
+
+    def profile_kernel(self, name: str, iters: int = 20) -> tuple[float, float]:
+        """(avg launch ms, algorithmic bytes or FLOPs per launch) of one kernel of
+        the last decode step, re-launched `iters` times and timed with CUDA events."""
+        ms, work = ctypes.c_double(), ctypes.c_double()
+        check(_lib.lib().rlb_profile_kernel(self._h, self.KERNELS[name], iters, ctypes.byref(ms),
+                                            ctypes.byref(work)))
+        return ms.value, work.value
+
     # -- convenience -------------------------------------------------------
 
     def run_to_completion(self, n_steps: int = 64) -> dict[str, list[int]]:
