@@ -312,11 +312,16 @@ int rlb_instance::head(int Lrows, bool append) {
   if (Lrows <= 0) return RLB_OK;
   int rc;
   if ((rc = rmsnorm_launch(d_h, H, d_logit_src, Lrows, norm, H, m.rms_eps, d_xn, H, st))) return rc;
-  GemmParams p{Lrows, V, H, nullptr, d_logits, V};
-  if ((rc = gemm_launch(m_xn, m_lm, BN_LM, EPI_F32, p, st))) return rc;
-  if (!append) return RLB_OK;
-  return argmax_append_launch(d_logits, V, Lrows, d_logit_slot, d_seq_tokens, d_seq_len,
-                              d_seq_target, max_seq, d_ring, d_ring_cur, max_slots, st);
+  if (!append) {
+    GemmParams p{Lrows, V, H, nullptr, d_logits, V};
+    return gemm_launch(m_xn, m_lm, BN_LM, EPI_F32, p, st);
+  }
+  const int ntiles = (V + BN_LM - 1) / BN_LM;
+  GemmParams p{Lrows, V, H, nullptr, d_logits, ntiles};
+  if ((rc = gemm_launch(m_xn, m_lm, BN_LM, EPI_ARGMAX, p, st))) return rc;
+  return argmax_append_launch(reinterpret_cast<const float2*>(d_logits), ntiles, Lrows,
+                              d_logit_slot, d_seq_tokens, d_seq_len, d_seq_target, max_seq, d_ring,
+                              d_ring_cur, max_slots, st);
 }
 
 int rlb_instance::decode_step_launch(int R) {
@@ -805,8 +810,9 @@ int rlb_profile_kernel(rlb_instance* h, int32_t which, int32_t iters, double* av
                                  GemmParams{R, h->QKV, H, w.bqkv, h->d_qkv, h->QKV}, h->st);
       case 4: return gemm_launch(h->m_attn, w.m_o, BN_O, EPI_F32,
                                  GemmParams{R, H, NQ * D, nullptr, h->d_logits, H}, h->st);
-      case 5: return gemm_launch(h->m_xn, h->m_lm, BN_LM, EPI_F32,
-                                 GemmParams{R, h->V, H, nullptr, h->d_logits, h->V}, h->st);
+      case 5: return gemm_launch(h->m_xn, h->m_lm, BN_LM, EPI_ARGMAX,
+                                 GemmParams{R, h->V, H, nullptr, h->d_logits,
+                                            (h->V + BN_LM - 1) / BN_LM}, h->st);
     }
     set_error("unknown kernel id");
     return RLB_ERR_ARG;

@@ -137,6 +137,30 @@ __global__ void __launch_bounds__(256, 1)
           }
         }
       }
+    } else if constexpr (EPI == EPI_ARGMAX) {
+      // greedy head: per (row, N-tile) max and its lowest column index; the
+      // full-vocab fp32 logits never reach HBM.
+      float best = -INFINITY;
+      int bidx = 0x7fffffff;
+#pragma unroll 1
+      for (int c = 0; c < BN; c += 16) {
+        uint32_t r[16];
+        tmem_ld16(tbase + c, r);
+        tmem_ld_wait();
+        const int n = n_blk * BN + c;
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          const float v = __uint_as_float(r[i]);
+          if (n + i < p.N && v > best) {
+            best = v;
+            bidx = n + i;
+          }
+        }
+      }
+      if (live) {
+        float2* part = reinterpret_cast<float2*>(p.out) + static_cast<size_t>(m) * p.ldo + n_blk;
+        *part = make_float2(best, __int_as_float(bidx));
+      }
     } else {
 #pragma unroll 1
       for (int c = 0; c < BN; c += 16) {
@@ -244,7 +268,7 @@ template <int BN>
 static int set_attr_bn() {
   int rc;
   if ((rc = set_attr<BN, EPI_BF16>()) || (rc = set_attr<BN, EPI_RESADD>()) ||
-      (rc = set_attr<BN, EPI_F32>()))
+      (rc = set_attr<BN, EPI_F32>()) || (rc = set_attr<BN, EPI_ARGMAX>()))
     return rc;
   if constexpr (BN >= 128) return set_attr<BN, EPI_SWIGLU>();
   return RLB_OK;
@@ -281,6 +305,7 @@ static int launch_bn(const CUtensorMap& a, const CUtensorMap& b, int epi, const 
       if constexpr (BN >= 128) return launch_one<BN, EPI_SWIGLU>(a, b, p, st);
       break;
     case EPI_F32: return launch_one<BN, EPI_F32>(a, b, p, st);
+    case EPI_ARGMAX: return launch_one<BN, EPI_ARGMAX>(a, b, p, st);
   }
   set_error("bad epilogue");
   return RLB_ERR_ARG;

@@ -10,7 +10,7 @@ namespace rlb {
 constexpr int PAGE = 64;      // tokens per KV page
 constexpr int SPLIT = 256;    // fixed split-K boundary of decode attention (tokens)
 
-enum Epi { EPI_BF16 = 0, EPI_RESADD = 1, EPI_SWIGLU = 2, EPI_F32 = 3 };
+enum Epi { EPI_BF16 = 0, EPI_RESADD = 1, EPI_SWIGLU = 2, EPI_F32 = 3, EPI_ARGMAX = 4 };
 
 struct GemmParams {
   int M, N, K;
@@ -42,7 +42,7 @@ int rmsnorm_launch(const float* x, int ldx, const int* src_rows, int R, const bf
 int rope_append_launch(const bf16* qkv, int ldqkv, const int* row_slot, const int* row_pos, int R,
                        const float2* rope, int NQ, int NKV, int D, bf16* qout, int ldq, bf16* kv,
                        const int* block_table, int bt_stride, cudaStream_t st);
-int argmax_append_launch(const float* logits, int V, int L, const int* logit_slot,
+int argmax_append_launch(const float2* part, int ntiles, int L, const int* logit_slot,
                          int32_t* seq_tokens, int32_t* seq_len, const int32_t* seq_target,
                          int max_seq, int32_t* ring, const int32_t* ring_cur, int max_slots,
                          cudaStream_t st);

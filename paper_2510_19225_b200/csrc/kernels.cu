@@ -117,22 +117,25 @@ int rope_append_launch(const bf16* qkv, int ldqkv, const int* row_slot, const in
 // Greedy token (lowest index on ties) of each logits row, appended to the
 // slot's device sequence buffer (K6) and to this step's row of the token ring
 // that the host flushes with one D2H copy.
+// Input: per (row, lm_head N-tile) (max, lowest argmax index) partials written
+// by the EPI_ARGMAX GEMM epilogue.
 __global__ void __launch_bounds__(512) argmax_append_kernel(
-    const float* __restrict__ logits, int V, const int* __restrict__ logit_slot,
+    const float2* __restrict__ part, int ntiles, const int* __restrict__ logit_slot,
     int32_t* __restrict__ seq_tokens, int32_t* __restrict__ seq_len,
     const int32_t* __restrict__ seq_target, int max_seq, int32_t* __restrict__ ring,
     const int32_t* __restrict__ ring_cur, int max_slots) {
   __shared__ float sv[16];
   __shared__ int si[16];
   const int r = blockIdx.x;
-  const float* row = logits + static_cast<size_t>(r) * V;
+  const float2* row = part + static_cast<size_t>(r) * ntiles;
   float best = -INFINITY;
   int idx = 0x7fffffff;
-  for (int i = threadIdx.x; i < V; i += 512) {
-    const float v = row[i];
-    if (v > best) {
-      best = v;
-      idx = i;
+  for (int i = threadIdx.x; i < ntiles; i += 512) {
+    const float2 v = row[i];
+    const int vi = __float_as_int(v.y);
+    if (v.x > best || (v.x == best && vi < idx)) {
+      best = v.x;
+      idx = vi;
     }
   }
 #pragma unroll
@@ -165,13 +168,13 @@ __global__ void __launch_bounds__(512) argmax_append_kernel(
   }
 }
 
-int argmax_append_launch(const float* logits, int V, int L, const int* logit_slot,
+int argmax_append_launch(const float2* part, int ntiles, int L, const int* logit_slot,
                          int32_t* seq_tokens, int32_t* seq_len, const int32_t* seq_target,
                          int max_seq, int32_t* ring, const int32_t* ring_cur, int max_slots,
                          cudaStream_t st) {
   if (L <= 0) return RLB_OK;
-  argmax_append_kernel<<<L, 512, 0, st>>>(logits, V, logit_slot, seq_tokens, seq_len, seq_target,
-                                          max_seq, ring, ring_cur, max_slots);
+  argmax_append_kernel<<<L, 512, 0, st>>>(part, ntiles, logit_slot, seq_tokens, seq_len,
+                                          seq_target, max_seq, ring, ring_cur, max_slots);
   RLB_CUDA(cudaGetLastError());
   return RLB_OK;
 }
