@@ -1,0 +1,88 @@
+"""Event-log audits of the rollout path (control-plane oracle).
+
+TEST INFRASTRUCTURE ONLY -- imported by tests/ and never by the product path.
+
+Restates the reference's log re-derivations (`pkg/tests/oracles.py:146-236`):
+replaying `request_created` / `route` / `tokens` / `migrate_out` / `complete`
+records enforces single ownership and append-only token growth
+(`audit_requests`, oracles.py:146-196), exact token conservation per request
+and over route legs (`assert_token_conservation`, oracles.py:199-209), and
+version gating of remote token events (`assert_version_gating`,
+oracles.py:212-236).  The restatement runs on logs written by the B200 path
+(manager.py mirror + real instances) and is pinned against the reference's
+own logs and counts in tests/golden/ref_sim_*.jsonl.gz
+(tests/test_audit.py).
+"""
+from __future__ import annotations
+
+
+def audit_requests(records: list[dict]) -> dict[str, dict]:
+    """Per-request facts; asserts ownership / growth invariants on the way
+    (oracles.py:146-196)."""
+    reqs: dict[str, dict] = {}
+    owner: dict[str, str] = {}
+    for rec in records:
+        kind = rec["type"]
+        rid = rec.get("request_id")
+        if kind == "request_created":
+            assert rid not in reqs, f"duplicate request {rid}"
+            reqs[rid] = {"target": rec["target_len"], "tokens": 0, "complete": False, "legs": []}
+        elif kind == "route":
+            assert rid not in owner, f"{rid} routed while owned by {owner.get(rid)}"
+            assert not reqs[rid]["complete"], f"{rid} routed after completion"
+            owner[rid] = rec["instance_id"]
+            reqs[rid]["legs"].append([rec["instance_id"], 0])
+        elif kind == "tokens":
+            assert owner.get(rid) == rec["instance_id"], f"tokens for {rid} from a non-owner"
+            r = reqs[rid]
+            r["tokens"] += rec["count"]
+            assert r["tokens"] == rec["total"], f"token count drift for {rid}"
+            assert r["tokens"] <= r["target"], f"{rid} overshot"
+            r["legs"][-1][1] += rec["count"]
+        elif kind == "migrate_out":
+            assert owner.pop(rid) == rec["instance_id"]
+            r = reqs[rid]
+            if rec["kept_tokens"] != r["tokens"]:
+                # recompute policy discards the prefix on preemption
+                assert rec["reason"] == "preempt" and rec["kept_tokens"] == 0, rec
+                r["tokens"], r["legs"] = 0, []
+        elif kind == "complete":
+            assert owner.pop(rid) == rec["instance_id"]
+            r = reqs[rid]
+            assert not r["complete"], f"{rid} completed twice"
+            r["complete"] = True
+            assert rec["length"] == r["target"], f"{rid} completed at {rec['length']}"
+    return reqs
+
+
+def assert_token_conservation(records: list[dict]) -> int:
+    """Every request completes with exactly target_len tokens, consistent over
+    its legs (oracles.py:199-209).  Returns the request count."""
+    reqs = audit_requests(records)
+    for rid, r in reqs.items():
+        assert r["complete"], f"{rid} never completed"
+        assert r["tokens"] == r["target"], f"{rid}: {r['tokens']} != {r['target']}"
+        assert sum(n for _, n in r["legs"]) == r["target"], rid
+    return len(reqs)
+
+
+def assert_version_gating(records: list[dict]) -> int:
+    """No remote token event without a completed pull of the step's version
+    (oracles.py:212-236).  Returns the number of remote token events checked."""
+    step_version = 0
+    pulled: dict[str, int] = {}
+    checked = 0
+    for rec in records:
+        kind = rec["type"]
+        if kind == "step_start":
+            step_version = rec["version"]
+        elif kind == "pull_done":
+            pulled[rec["instance_id"]] = rec["version"]
+        elif kind == "preempt":
+            pulled.pop(rec["instance_id"], None)
+        elif kind == "tokens" and not rec["instance_id"].startswith("local"):
+            checked += 1
+            assert rec["version"] == step_version, f"stale token event on {rec['instance_id']}"
+            assert pulled.get(rec["instance_id"]) == step_version, (
+                f"{rec['instance_id']} emitted tokens without pulling version {step_version}")
+    return checked

@@ -1,0 +1,119 @@
+#!/usr/bin/env python
+"""Generate the committed golden fixtures under tests/golden/ (run in the
+builder container; /root/reference and transformers must be importable).
+
+1. tiny_hf.npz -- the arithmetic oracle's independent cross-check: the tiny
+   config-1 decoder with the seeded synthetic weights, run through
+   transformers' Qwen2ForCausalLM (fp32, eager attention): greedy tokens and
+   last-position logits for 4 prompts.  Pins oracle/qwen2_fp32.py.
+2. ref_sim_{migrate,recompute}.jsonl.gz -- event logs of the UNMODIFIED
+   reference simulator (pkg/src/spotrl/sim/engine.py) on the first config +
+   trace of the reference's fuzzed preemption corpus
+   (pkg/tests/test_acceptance.py:191-227), 8 steps,
+   plus the counts the reference oracles (pkg/tests/oracles.py) derive from
+   them.  Pins oracle/audit.py.
+3. ref_manager_script.jsonl -- the event log of the reference RolloutManager
+   driven by a fixed call script (scripts/manager_script.py) with preemption,
+   migration and gating.  Pins paper_2510_19225_b200/manager.py.
+"""
+from __future__ import annotations
+
+import dataclasses
+import gzip
+import json
+import os
+import sys
+
+import numpy as np
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "scripts"))
+GOLD = os.path.join(ROOT, "tests", "golden")
+REF = "/root/reference/pkg"
+
+
+def tiny_hf():
+    from transformers import Qwen2Config, Qwen2ForCausalLM
+    from paper_2510_19225_b200.shapes import TINY as m
+    from paper_2510_19225_b200.synth import synth_hf_weights, synth_prompts
+    w = synth_hf_weights(m, seed=0)
+    cfg = Qwen2Config(vocab_size=m.vocab, hidden_size=m.hidden, intermediate_size=m.ffn,
+                      num_hidden_layers=m.layers, num_attention_heads=m.n_q_heads,
+                      num_key_value_heads=m.n_kv_heads, head_dim=m.head_dim,
+                      rope_theta=m.rope_theta, rms_norm_eps=m.rms_eps,
+                      tie_word_embeddings=m.tied, max_position_embeddings=4096,
+                      attn_implementation="eager", torch_dtype=torch.float32)
+    hf = Qwen2ForCausalLM(cfg).eval()
+    hf.load_state_dict({k: v.float() for k, v in w.items()}, strict=True)
+    prompts = synth_prompts(4, m.vocab, 16, 64, seed=1)
+    new = 24
+    toks, last = [], []
+    with torch.no_grad():
+        for p in prompts:
+            out = hf.generate(torch.tensor([p]), max_new_tokens=new, do_sample=False,
+                              min_new_tokens=new)
+            g = out[0, len(p):].tolist()
+            toks.append(g)
+            logits = hf(torch.tensor([p + g[:-1]])).logits[0]
+            last.append(logits[len(p) - 1:].numpy()[:: 6])  # every 6th position
+    wsum = np.array([float(w[k].float().sum()) for k in sorted(w)], np.float64)
+    np.savez_compressed(os.path.join(GOLD, "tiny_hf.npz"),
+                        prompt_lens=np.array([len(p) for p in prompts]),
+                        prompts=np.concatenate([np.array(p) for p in prompts]),
+                        tokens=np.array(toks), logits=np.stack(last).astype(np.float32),
+                        weight_sums=wsum)
+    print("tiny_hf.npz", np.array(toks)[:, :8])
+
+
+def ref_sim():
+    sys.path[:0] = [f"{REF}/src", f"{REF}/tests"]
+    from spotrl.sim.config import SimConfig
+    from spotrl.sim.engine import run_experiment
+    from spotrl.traces import SynthesisParams, synthesize
+    import oracles
+    import random
+    from test_acceptance import fuzz_config, fuzz_trace   # the reference's fuzz corpus, run 0
+    rng = random.Random(1234)
+    base, trace = fuzz_config(rng), fuzz_trace(rng)
+    for policy in ("migrate", "recompute"):
+        cfg = dataclasses.replace(base, migration=policy, steps=8)
+        res = run_experiment(cfg, trace)
+        recs = res.log.records
+        facts = {
+            "requests": oracles.assert_token_conservation(recs),
+            "gated_token_events": oracles.assert_version_gating(recs),
+            "preemptions": len(res.log.of_type("preempt")),
+            "migrate_out": len(res.log.of_type("migrate_out")),
+            "kept_tokens": sum(r["kept_tokens"] for r in res.log.of_type("migrate_out")),
+        }
+        oracles.assert_stats_closure(recs)
+        path = os.path.join(GOLD, f"ref_sim_{policy}.jsonl.gz")
+        with gzip.open(path, "wt") as f:
+            f.write(json.dumps({"facts": facts}) + "\n")
+            f.write(res.log.to_jsonl())
+        print(path, facts, len(recs))
+
+
+def ref_manager():
+    sys.path[:0] = [f"{REF}/src"]
+    from spotrl.events import EventLog
+    from spotrl.manager import RolloutManager
+    import manager_script
+    for policy in ("migrate", "recompute"):
+        log = EventLog()
+        mgr = RolloutManager(theta=3, m_b=4, log=log, migration=policy)
+        errors = manager_script.run(mgr)
+        path = os.path.join(GOLD, f"ref_manager_script_{policy}.jsonl")
+        with open(path, "w") as f:
+            f.write(json.dumps({"errors": errors}) + "\n")
+            f.write(log.to_jsonl())
+        print(path, len(log.records), errors)
+
+
+if __name__ == "__main__":
+    os.makedirs(GOLD, exist_ok=True)
+    tiny_hf()
+    ref_sim()
+    ref_manager()
