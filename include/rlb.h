@@ -105,10 +105,19 @@ int rlb_load_weights(rlb_instance* h, const void* const* hf_ptrs, int32_t n_tens
                      uint64_t version, rlb_pull_stats* stats);
 /* Engine arena device pointer + bytes (for bytewise checks / chained hops). */
 int rlb_weights_arena(rlb_instance* h, void** arena, int64_t* bytes);
+/* Declare the arena filled with `version` by an external copy (the fan-out
+ * writes it with rlb_relayout_copy_range / rlb_copy_bytes). */
+int rlb_mark_weights(rlb_instance* h, uint64_t version);
 /* Stand-alone fused re-layout copy on `device` (stream 0 if stream==NULL). */
 int rlb_relayout_copy(int device, const rlb_model_cfg* model, const void* const* hf_ptrs,
                       int32_t n_tensors, void* dst_arena, void* stream);
-/* Plain chunked device copy (peer or local) used for chained fan-out hops. */
+/* The slice of the fused re-layout that writes arena bytes [lo, hi) (16-byte
+ * aligned): the scatter phase of the 1->N fan-out. */
+int rlb_relayout_copy_range(int device, const rlb_model_cfg* model, const void* const* hf_ptrs,
+                            int32_t n_tensors, void* dst_arena, int64_t lo, int64_t hi,
+                            void* stream);
+/* Plain chunked device copy (peer or local): the all-gather phase of the
+ * fan-out copies engine-layout slices between rollout GPUs. */
 int rlb_copy_bytes(int device, void* dst, const void* src, int64_t nbytes, void* stream);
 
 /* ---- CUDA IPC (pull sessions between processes) ------------------------ */

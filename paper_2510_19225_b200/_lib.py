@@ -82,9 +82,12 @@ _SIGS = {
     "rlb_load_weights": (ctypes.c_int, [_P, _P, ctypes.c_int32, ctypes.c_uint64,
                                         ctypes.POINTER(PullStats)]),
     "rlb_weights_arena": (ctypes.c_int, [_P, ctypes.POINTER(_P), ctypes.POINTER(ctypes.c_int64)]),
+    "rlb_mark_weights": (ctypes.c_int, [_P, ctypes.c_uint64]),
     "rlb_relayout_copy": (ctypes.c_int, [ctypes.c_int, ctypes.POINTER(ModelCfg), _P,
                                          ctypes.c_int32, _P, _P]),
     "rlb_copy_bytes": (ctypes.c_int, [ctypes.c_int, _P, _P, ctypes.c_int64, _P]),
+    "rlb_relayout_copy_range": (ctypes.c_int, [ctypes.c_int, ctypes.POINTER(ModelCfg), _P,
+                                               ctypes.c_int32, _P, ctypes.c_int64, ctypes.c_int64, _P]),
     "rlb_ipc_handle": (ctypes.c_int, [_P, _P, ctypes.POINTER(ctypes.c_int64)]),
     "rlb_ipc_open": (ctypes.c_int, [ctypes.c_int, _P, ctypes.POINTER(_P)]),
     "rlb_ipc_close": (ctypes.c_int, [ctypes.c_int, _P]),

@@ -628,6 +628,15 @@ int rlb_weights_arena(rlb_instance* h, void** arena, int64_t* bytes) {
   return RLB_OK;
 }
 
+int rlb_mark_weights(rlb_instance* h, uint64_t version) {
+  RLB_CHECK(h, RLB_ERR_ARG, "null handle");
+  RLB_CHECK(!h->has_weights || version >= h->version, RLB_ERR_ARG,
+            "weight version " + std::to_string(version) + " < " + std::to_string(h->version));
+  h->version = version;
+  h->has_weights = true;
+  return RLB_OK;
+}
+
 static int submit_one(rlb_instance* h, uint64_t key, const int32_t* toks, int32_t n_prompt,
                       int32_t n_total, int32_t target_len) {
   RLB_CHECK(n_prompt >= 1, RLB_ERR_ARG, "empty prompt");

@@ -12,6 +12,9 @@
 // 16-byte vector loads, 4 in flight per thread, L1 no-allocate.
 #include "internal.h"
 
+#include <algorithm>
+#include <cstring>
+
 namespace rlb {
 
 static int64_t align256(int64_t x) { return (x + 255) / 256 * 256; }
@@ -161,6 +164,27 @@ int relayout_copy(const rlb_model_cfg& m, const void* const* hf_ptrs, int32_t n,
   return run_chunks(chunks, st);
 }
 
+// The part of the fused re-layout that lands in arena bytes [lo, hi): used by
+// the scatter phase of the 1->N fan-out (each receiver pulls one slice).
+int relayout_copy_range(const rlb_model_cfg& m, const void* const* hf_ptrs, int32_t n, void* dst,
+                        int64_t lo, int64_t hi, cudaStream_t st) {
+  RLB_CHECK(n == hf_count(m), RLB_ERR_ARG, "wrong HF tensor count");
+  RLB_CHECK(lo % 16 == 0 && hi % 16 == 0 && lo <= hi, RLB_ERR_ARG, "range must be 16B aligned");
+  std::vector<Segment> segs;
+  relayout_segments(m, &segs);
+  std::vector<CopyChunk> chunks;
+  for (const Segment& s : segs) {
+    const int64_t a = std::max(lo, s.dst_off), b = std::min(hi, s.dst_off + s.bytes);
+    if (a >= b) continue;
+    const uint8_t* src = static_cast<const uint8_t*>(hf_ptrs[s.hf]) + s.src_off + (a - s.dst_off);
+    uint8_t* d = static_cast<uint8_t*>(dst) + a;
+    RLB_CHECK(((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(d)) & 15) == 0,
+              RLB_ERR_ARG, "weight tensors must be 16-byte aligned");
+    split_into(&chunks, src, d, b - a);
+  }
+  return run_chunks(chunks, st);
+}
+
 int copy_bytes(void* dst, const void* src, int64_t nbytes, cudaStream_t st) {
   RLB_CHECK(((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & 15) == 0,
             RLB_ERR_ARG, "copy buffers must be 16-byte aligned");
@@ -195,6 +219,15 @@ int rlb_relayout_copy(int device, const rlb_model_cfg* m, const void* const* hf_
   RLB_CHECK(m && hf_ptrs && dst_arena, RLB_ERR_ARG, "null argument");
   RLB_CUDA(cudaSetDevice(device));
   return rlb::relayout_copy(*m, hf_ptrs, n_tensors, dst_arena, static_cast<cudaStream_t>(stream));
+}
+
+int rlb_relayout_copy_range(int device, const rlb_model_cfg* m, const void* const* hf_ptrs,
+                            int32_t n_tensors, void* dst_arena, int64_t lo, int64_t hi,
+                            void* stream) {
+  RLB_CHECK(m && hf_ptrs && dst_arena, RLB_ERR_ARG, "null argument");
+  RLB_CUDA(cudaSetDevice(device));
+  return rlb::relayout_copy_range(*m, hf_ptrs, n_tensors, dst_arena, lo, hi,
+                                  static_cast<cudaStream_t>(stream));
 }
 
 int rlb_copy_bytes(int device, void* dst, const void* src, int64_t nbytes, void* stream) {

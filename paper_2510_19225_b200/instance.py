@@ -99,6 +99,10 @@ class RolloutInstance:
 
     pull_weights = load_weights
 
+    def mark_weights(self, version: int) -> None:
+        """The arena was filled externally (fan-out pull) with `version`."""
+        check(_lib.lib().rlb_mark_weights(self._h, version))
+
     def arena(self) -> tuple[int, int]:
         p, n = ctypes.c_void_p(), ctypes.c_int64()
         check(_lib.lib().rlb_weights_arena(self._h, ctypes.byref(p), ctypes.byref(n)))
