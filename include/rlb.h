@@ -173,9 +173,11 @@ int rlb_score(rlb_instance* h, const int32_t* tokens, int32_t n, float* out_logi
 /* ---- kernel-level entry points (parity tests) -------------------------- */
 /* C = A[M,K] . B[N,K]^T with epilogue: 0 bf16 out (+bias if bias!=NULL),
  * 1 fp32 residual add (C fp32 in/out), 2 SwiGLU over 64-row interleaved
- * gate/up blocks (bf16 out [M, N/2]), 3 fp32 out.  All device pointers. */
+ * gate/up blocks (bf16 out [M, N/2]), 3 fp32 out.  block_n 128 or 256;
+ * splits > 1 runs split-K (fp32 partials + ordered reduce; epilogues 0,1,3).
+ * All device pointers. */
 int rlb_gemm(int device, int32_t M, int32_t N, int32_t K, const void* A, const void* B,
-             const void* bias, void* C, int32_t epilogue, int32_t block_n);
+             const void* bias, void* C, int32_t epilogue, int32_t block_n, int32_t splits);
 
 #ifdef __cplusplus
 }

@@ -102,7 +102,7 @@ _SIGS = {
                                   ctypes.POINTER(ctypes.c_uint64)]),
     "rlb_score": (ctypes.c_int, [_P, _P, ctypes.c_int32, _P]),
     "rlb_gemm": (ctypes.c_int, [ctypes.c_int, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, _P, _P,
-                                _P, _P, ctypes.c_int32, ctypes.c_int32]),
+                                _P, _P, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32]),
 }
 EXPORTED = tuple(_SIGS)
 

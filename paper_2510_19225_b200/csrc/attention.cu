@@ -1,20 +1,22 @@
-// K1: split-K paged decode attention on the tensor cores (mma.sync m16n8k16).
+// K1: paged decode attention on the tensor cores (mma.sync m16n8k16).
 //
-// One CTA = (token row, kv head, split of SPLIT=256 absolute positions); the
-// GQA group (G <= 8 query heads sharing the kv head) forms the M rows of the
-// MMA, so K and V of the split are read from HBM exactly once.  Warp w owns
-// the 64 positions [t0 + 64w, t0 + 64w + 64) -- one KV page -- and streams them
-// in 16-token chunks through a 3-stage cp.async ring (XOR-swizzled rows,
-// ldmatrix / ldmatrix.trans fragments, zero-fill past the context end):
-//     S = Q K^T (fp32) -> scale, mask -> online softmax in fixed chunk order
-//     -> P (bf16, reusing the S accumulator layout as the A operand) -> O += P V
-// The four warp partials are merged in warp order, then either normalised
-// (context <= one split) or written as (O, m, l) for the split combine.
+// One CTA = (token row, kv head, window of SUPER=2048 positions); for every
+// context the configs use (<= 1408 + prefix) that is one CTA per (row, kv head)
+// and no combine pass.  The GQA group (G <= 8 query heads sharing the kv head)
+// forms the M rows of the MMA, so K and V are read from HBM exactly once.
+// Positions are cut into 64-token pages; warp w owns pages w, w+4, w+8, ...
+// of the window and streams them in 16-token chunks through a STAGES-deep
+// cp.async ring (XOR-swizzled rows, ldmatrix / ldmatrix.trans fragments,
+// zero-fill past the context end):
+//     S = Q K^T (fp32) -> scale, mask -> online softmax in chunk order
+//     -> P (bf16, the S accumulator layout reused as the A operand) -> O += P V
+// The four warp partials are merged in warp order, then normalised (or, for
+// windows beyond the first, written as (O, m, l) and merged in window order).
 //
 // Determinism: every reduction order (quad shuffles, chunk order, warp order,
-// split order) is a function of the row's context length only, so a row gets
-// the same bits whether it is a decode row or one of the rows of a varlen
-// prefill -- the property migration resume relies on (SURVEY.md §7 part 2).
+// window order) is a function of the row's context length only, so a row gets
+// the same bits as a decode row or as one of the rows of a varlen prefill --
+// the property migration resume relies on (SURVEY.md §7 part 2).
 #include "internal.h"
 
 namespace rlb {
@@ -22,9 +24,10 @@ namespace rlb {
 namespace {
 
 constexpr int WARPS = 4;
-constexpr int CHUNK = 16;          // tokens per pipeline stage
+constexpr int CHUNK = 16;              // tokens per pipeline stage
 constexpr int STAGES = 3;
-constexpr int WARP_TOKENS = SPLIT / WARPS;   // 64 = one page
+constexpr int SUPER = 2048;            // positions per CTA window (8 pages per warp)
+static_assert(SUPER / PAGE / WARPS <= 32, "page ids of a warp are held one per lane");
 
 __device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, bool valid) {
   const int n = valid ? 16 : 0;   // zero-fill past the context end
@@ -68,18 +71,11 @@ __global__ void __launch_bounds__(WARPS * 32, 2) attn_mma_kernel(AttnArgs a) {
   constexpr int WARP_SMEM = STAGES * STAGE_BYTES;
   extern __shared__ __align__(128) uint8_t smem[];
 
-  const int sp = blockIdx.x, kvh = blockIdx.y, r = blockIdx.z;
-  const int n = a.row_pos[r] + 1;
-  const int t0 = sp * SPLIT;
-  if (t0 >= n) return;
-  const int G = a.NQ / a.NKV;
+  const int ws_idx = blockIdx.x, kvh = blockIdx.y, r = blockIdx.z;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int wt0 = t0 + warp * WARP_TOKENS;                 // first position of this warp
-  const int ntok = max(0, min(WARP_TOKENS, n - wt0));      // valid positions of this warp
-  const int nchunks = (ntok + CHUNK - 1) / CHUNK;
-  const float scale = rsqrtf(static_cast<float>(D)) * 1.4426950408889634f;
+  const int G = a.NQ / a.NKV;
 
-  // Q fragments (A operand): row = lane/4 = head in the group (rows >= G are zero).
+  // Q fragments first: independent of the row metadata loads below.
   uint32_t qa[KSTEPS][2];
   {
     const int h = lane >> 2;
@@ -91,25 +87,42 @@ __global__ void __launch_bounds__(WARPS * 32, 2) attn_mma_kernel(AttnArgs a) {
       qa[kk][1] = h < G ? *reinterpret_cast<const uint32_t*>(qrow + c + 8) : 0u;
     }
   }
+  const int n = a.row_pos[r] + 1;
+  const int w0 = ws_idx * SUPER;
+  if (w0 >= n) return;
+  const int wn = min(SUPER, n - w0);                     // positions in this window
+  const float scale = rsqrtf(static_cast<float>(D)) * 1.4426950408889634f;
+
+  // pages of this warp: window pages p = warp, warp+4, ...; prefetch their ids
+  const int npages = (wn + PAGE - 1) / PAGE;
+  const int nseg = npages > warp ? (npages - warp + WARPS - 1) / WARPS : 0;
+  int my_page = 0;
+  if (lane < nseg) {
+    const int p = w0 / PAGE + warp + lane * WARPS;
+    my_page = a.block_table[static_cast<size_t>(a.row_slot[r]) * a.bt_stride + p];
+  }
+  // chunk c of this warp: segment c/4 (window page warp + 4*(c/4)), rows 16*(c%4)..
+  const int last_seg_tokens = nseg > 0 ? min(PAGE, wn - (warp + (nseg - 1) * WARPS) * PAGE) : 0;
+  const int nchunks = nseg > 0 ? (nseg - 1) * (PAGE / CHUNK) + (last_seg_tokens + CHUNK - 1) / CHUNK : 0;
 
   uint8_t* wsm = smem + warp * WARP_SMEM;
   const uint32_t wsm_u32 = smem_u32(wsm);
-  const bf16* kpage = nullptr;
-  if (ntok > 0) {
-    const int page = a.block_table[static_cast<size_t>(a.row_slot[r]) * a.bt_stride + wt0 / PAGE];
-    kpage = a.kv + (static_cast<size_t>(page) * a.NKV + kvh) * (2 * PAGE * D) +
-            static_cast<size_t>(wt0 % PAGE) * D;
-  }
+  const size_t head_off = static_cast<size_t>(kvh) * (2 * PAGE * D);
+  const size_t page_stride = static_cast<size_t>(a.NKV) * (2 * PAGE * D);
 
   auto issue = [&](int c) {
+    const int seg = c >> 2;
+    const int page = __shfl_sync(0xffffffffu, my_page, seg);
+    const int seg_tok = min(PAGE, wn - (warp + seg * WARPS) * PAGE);   // valid tokens in the page
+    const bf16* kp = a.kv + static_cast<size_t>(page) * page_stride + head_off;
     const uint32_t st = wsm_u32 + (c % STAGES) * STAGE_BYTES;
 #pragma unroll
     for (int i = 0; i < (CHUNK * CPR) / 32; ++i) {
       const int idx = i * 32 + lane;
       const int row = idx / CPR, ch = idx % CPR;
-      const int tok = c * CHUNK + row;
-      const bool ok = tok < ntok;
-      const bf16* src = kpage + static_cast<size_t>(ok ? tok : 0) * D + ch * 8;
+      const int tok = (c & 3) * CHUNK + row;          // token within the page
+      const bool ok = tok < seg_tok;
+      const bf16* src = kp + static_cast<size_t>(ok ? tok : 0) * D + ch * 8;
       const uint32_t off = row * ROWB + ((ch ^ (row & 7)) << 4);
       cp_async16(st + off, src, ok);
       cp_async16(st + CHUNK * ROWB + off, src + PAGE * D, ok);
@@ -133,6 +146,8 @@ __global__ void __launch_bounds__(WARPS * 32, 2) attn_mma_kernel(AttnArgs a) {
     __syncwarp();
     const uint32_t ks = wsm_u32 + (c % STAGES) * STAGE_BYTES;
     const uint32_t vs = ks + CHUNK * ROWB;
+    const int seg_tok = min(PAGE, wn - (warp + (c >> 2) * WARPS) * PAGE);
+    const int tok0 = (c & 3) * CHUNK;
     // ---- S = Q K^T over 16 tokens (two n-tiles of 8)
     float s[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
     {
@@ -153,8 +168,8 @@ __global__ void __launch_bounds__(WARPS * 32, 2) attn_mma_kernel(AttnArgs a) {
     for (int j = 0; j < 2; ++j)
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
-        const int tok = c * CHUNK + 8 * j + 2 * (lane & 3) + e;
-        s[j][e] = tok < ntok ? s[j][e] * scale : -INFINITY;
+        const int tok = tok0 + 8 * j + 2 * (lane & 3) + e;
+        s[j][e] = tok < seg_tok ? s[j][e] * scale : -INFINITY;
         mx = fmaxf(mx, s[j][e]);
       }
     mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
@@ -206,8 +221,7 @@ __global__ void __launch_bounds__(WARPS * 32, 2) attn_mma_kernel(AttnArgs a) {
 #pragma unroll
     for (int t = 0; t < NT; ++t) {
       const int col = t * 8 + 2 * (lane & 3);
-      red[(warp * 8 + h) * D + col] = o[t][0];
-      red[(warp * 8 + h) * D + col + 1] = o[t][1];
+      *reinterpret_cast<float2*>(&red[(warp * 8 + h) * D + col]) = make_float2(o[t][0], o[t][1]);
     }
     if ((lane & 3) == 0) {
       mls[(warp * 8 + h) * 2] = m_run;
@@ -215,7 +229,7 @@ __global__ void __launch_bounds__(WARPS * 32, 2) attn_mma_kernel(AttnArgs a) {
     }
   }
   __syncthreads();
-  const bool single = n <= SPLIT;
+  const bool single = n <= SUPER;
   for (int i = threadIdx.x; i < G * D; i += WARPS * 32) {
     const int g = i / D, d = i % D;
     float M = -INFINITY;
@@ -232,7 +246,7 @@ __global__ void __launch_bounds__(WARPS * 32, 2) attn_mma_kernel(AttnArgs a) {
     if (single) {
       a.out[static_cast<size_t>(r) * a.ldo + qh * D + d] = __float2bfloat16_rn(O / L);
     } else {
-      float* wsp = a.ws + ((static_cast<size_t>(r) * a.NQ + qh) * a.max_splits + sp) * (D + 2);
+      float* wsp = a.ws + ((static_cast<size_t>(r) * a.NQ + qh) * a.max_splits + ws_idx) * (D + 2);
       wsp[d] = O;
       if (d == 0) {
         wsp[D] = M;
@@ -242,11 +256,11 @@ __global__ void __launch_bounds__(WARPS * 32, 2) attn_mma_kernel(AttnArgs a) {
   }
 }
 
-// Merge the per-split partials of rows longer than one split, in split order.
+// Merge the per-window partials of rows longer than one window, in order.
 __global__ void attn_combine_kernel(AttnArgs a) {
   const int qh = blockIdx.x, r = blockIdx.y, d = threadIdx.x;
   const int n = a.row_pos[r] + 1;
-  const int ns = (n + SPLIT - 1) / SPLIT;
+  const int ns = (n + SUPER - 1) / SUPER;
   if (ns <= 1) return;
   const int D = a.D;
   const float* w = a.ws + (static_cast<size_t>(r) * a.NQ + qh) * a.max_splits * (D + 2);
@@ -260,6 +274,8 @@ __global__ void attn_combine_kernel(AttnArgs a) {
   }
   a.out[static_cast<size_t>(r) * a.ldo + qh * D + d] = __float2bfloat16_rn(O / L);
 }
+
+int attention_windows(int max_seq) { return (max_seq + SUPER - 1) / SUPER; }
 
 template <int D>
 static int launch_attn(const AttnArgs& a, cudaStream_t st) {

@@ -52,8 +52,20 @@ struct LayerW {
 };
 
 // GEMM tile widths per projection (N-tile of the 128 x BN UMMA tile).
-constexpr int BN_QKV = 128, BN_O = 64, BN_GU = 256, BN_DOWN = 64, BN_LM = 256;
+constexpr int BN_QKV = 128, BN_O = 128, BN_GU = 256, BN_DOWN = 128, BN_LM = 256;
 constexpr int RING_ROWS = 512;
+
+// Split-K factor of an [N, K] projection: the largest divisor d of the K
+// blocks with (N-tiles x 2 row tiles of a 512-row decode step) x d <= 148 SMs
+// and >= 4 K blocks per split.  Depends on the weight shape only.
+static int pick_splits(int N, int K, int bn) {
+  const int nk = K / 64;
+  const int tiles = ((N + bn - 1) / bn) * 2;
+  int best = 1;
+  for (int d = 1; d <= nk; ++d)
+    if (nk % d == 0 && nk / d >= 4 && tiles * d <= 148 && d <= 8) best = d;
+  return best;
+}
 
 template <typename T>
 static int dalloc(T** p, size_t n) {
@@ -114,11 +126,21 @@ struct rlb_instance {
   cudaEvent_t ev0 = nullptr, ev1 = nullptr, evA = nullptr, evB = nullptr;
   rlb_stats stats{};
   int last_R = 0;  // rows of the last decode step (for rlb_profile_kernel)
+  // split-K factors of the small-N projections: a property of the model
+  // shape only (never of M or of the engine config), so every instance of
+  // the same model reduces every row identically.
+  int sp_qkv = 1, sp_o = 1, sp_down = 1;
+  float* d_part = nullptr;  // split-K partials [splits][max_rows][N]
+  int pending_rows = 0;     // rows of the forward whose last down partials await the head
   int64_t launches_per_forward(int R_logits) const {
-    // embed + per layer (2 norms, 4 GEMMs, rope, attention [+combine]) + head
-    return 1 + static_cast<int64_t>(m.layers) * (8 + (max_splits > 1 ? 1 : 0)) +
-           (R_logits > 0 ? 3 : 0);
+    // embed + first norm + per layer (4 GEMMs, qkv_rope, attention [+window
+    // combine], 2 residual norms; the last layer's second one is the head's)
+    // + head (norm, lm_head, argmax)
+    const int per_layer = 8 + (max_splits > 1 ? 1 : 0);
+    return 2 + static_cast<int64_t>(m.layers) * per_layer - 1 + (R_logits > 0 ? 3 : 0);
   }
+  int proj(const CUtensorMap& a, const CUtensorMap& b, int bn, int splits, int epi, int R, int N,
+           int K, const bf16* bias, void* out, int ldo);
 
   ~rlb_instance();
   int init();
@@ -139,7 +161,8 @@ rlb_instance::~rlb_instance() {
   for (auto& g : graphs) cudaGraphExecDestroy(g.second);
   void* bufs[] = {arena, kv, d_bt, d_seq_tokens, d_seq_len, d_seq_target, d_row_tok, d_row_pos,
                   d_row_slot, d_logit_src, d_logit_slot, d_dec_slots, d_h, d_xn, d_qkv, d_q,
-                  d_attn, d_act, d_logits, d_ws, d_ring, d_ring_ctr, d_ring_cur, d_rope};
+                  d_attn, d_act, d_logits, d_ws, d_ring, d_ring_ctr, d_ring_cur, d_rope,
+                  d_part};
   for (void* b : bufs)
     if (b) cudaFree(b);
   if (h_stage) cudaFreeHost(h_stage);
@@ -169,14 +192,18 @@ int rlb_instance::init() {
   RLB_CHECK(max_slots > 0 && max_seq > 0, RLB_ERR_ARG, "max_slots/max_seq_len must be positive");
   pps = (max_seq + PAGE - 1) / PAGE;
   num_pages = e.num_pages > 0 ? e.num_pages : max_slots * pps;
-  max_splits = (max_seq + SPLIT - 1) / SPLIT;
+  max_splits = attention_windows(max_seq);
   const size_t ws_row = static_cast<size_t>(NQ) * max_splits * (D + 2) * sizeof(float);
   const size_t ws_budget = static_cast<size_t>(1) << 30;
-  prefill_rows = e.max_prefill_rows > 0 ? e.max_prefill_rows : 16384;
+  // Prefill chunks of ~1k rows keep the split-K partials of a chunk L2-resident.
+  prefill_rows = e.max_prefill_rows > 0 ? e.max_prefill_rows : 1024;
   prefill_rows = static_cast<int>(std::min<size_t>(prefill_rows, ws_budget / ws_row));
   prefill_rows = std::max(prefill_rows, 128);
   max_rows = std::max(prefill_rows, max_slots);
-  max_rows = (max_rows + 127) / 128 * 128;
+  max_rows = (max_rows + 255) / 256 * 256;
+  sp_qkv = pick_splits(QKV, H, BN_QKV);
+  sp_o = pick_splits(H, NQ * D, BN_O);
+  sp_down = pick_splits(H, F, BN_DOWN);
 
   RLB_CUDA(cudaSetDevice(device));
   RLB_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
@@ -220,6 +247,9 @@ int rlb_instance::init() {
   const int logit_rows = (max_slots + 127) / 128 * 128;
   if ((rc = dalloc(&d_logits, static_cast<size_t>(logit_rows) * V))) return rc;
   if ((rc = dalloc(&d_ws, R * ws_row / sizeof(float)))) return rc;
+  const size_t part = std::max({static_cast<size_t>(sp_qkv) * QKV, static_cast<size_t>(sp_o) * H,
+                                static_cast<size_t>(sp_down) * H});
+  if ((rc = dalloc(&d_part, part * R))) return rc;
   if ((rc = dalloc(&d_ring, static_cast<size_t>(RING_ROWS) * max_slots))) return rc;
   if ((rc = dalloc(&d_ring_ctr, 1)) || (rc = dalloc(&d_ring_cur, 1))) return rc;
   RLB_CUDA(cudaMemset(d_ring, 0xff, sizeof(int32_t) * RING_ROWS * max_slots));
@@ -281,44 +311,65 @@ int rlb_instance::bind_arena() {
 }
 
 int rlb_instance::forward_layers(int R) {
+  // Per layer: QKV / O / down GEMMs write split-K fp32 partials that their
+  // row-wise consumers reduce in split order, fused with what they do anyway:
+  //   qkv partials -> [sum + bias + RoPE + KV append]        (qkv_rope)
+  //   o partials   -> [h += sum; xn = RMSNorm(h) * ln2]       (resid_norm)
+  //   down partials-> [h += sum; xn = RMSNorm(h) * ln1(l+1)]  (resid_norm; the
+  //                    last layer's is folded into the head's final norm)
   int rc;
   if ((rc = embed_launch(embed, H, d_row_tok, R, d_h, st))) return rc;
+  if ((rc = resid_norm_launch(d_h, nullptr, 0, R, nullptr, R, L[0].ln1, H, m.rms_eps, d_xn, false,
+                              st)))
+    return rc;
   for (int l = 0; l < m.layers; ++l) {
     const LayerW& w = L[l];
     bf16* kv_l = kv + layer_stride * l;
-    if ((rc = rmsnorm_launch(d_h, H, nullptr, R, w.ln1, H, m.rms_eps, d_xn, H, st))) return rc;
-    GemmParams p{R, QKV, H, w.bqkv, d_qkv, QKV};
-    if ((rc = gemm_launch(m_xn, w.m_qkv, BN_QKV, EPI_BF16, p, st))) return rc;
-    if ((rc = rope_append_launch(d_qkv, QKV, d_row_slot, d_row_pos, R, d_rope, NQ, NKV, D, d_q,
-                                 NQ * D, kv_l, d_bt, pps, st)))
+    if ((rc = proj(m_xn, w.m_qkv, BN_QKV, sp_qkv, EPI_PARTIAL, R, QKV, H, nullptr, nullptr, 0)))
+      return rc;
+    if ((rc = qkv_rope_launch(d_part, sp_qkv, R, w.bqkv, d_row_slot, d_row_pos, R, d_rope, NQ, NKV,
+                              D, d_q, NQ * D, kv_l, d_bt, pps, st)))
       return rc;
     AttnArgs a{d_q, NQ * D, kv_l, d_bt, pps, d_row_slot, d_row_pos, R, NQ, NKV, D, max_splits,
                d_ws, d_attn, NQ * D};
     if ((rc = attention_launch(a, st))) return rc;
-    GemmParams po{R, H, NQ * D, nullptr, d_h, H};
-    if ((rc = gemm_launch(m_attn, w.m_o, BN_O, EPI_RESADD, po, st))) return rc;
-    if ((rc = rmsnorm_launch(d_h, H, nullptr, R, w.ln2, H, m.rms_eps, d_xn, H, st))) return rc;
-    GemmParams pg{R, 2 * F, H, nullptr, d_act, F};
-    if ((rc = gemm_launch(m_xn, w.m_gu, BN_GU, EPI_SWIGLU, pg, st))) return rc;
-    GemmParams pd{R, H, F, nullptr, d_h, H};
-    if ((rc = gemm_launch(m_act, w.m_down, BN_DOWN, EPI_RESADD, pd, st))) return rc;
+    if ((rc = proj(m_attn, w.m_o, BN_O, sp_o, EPI_PARTIAL, R, H, NQ * D, nullptr, nullptr, 0)))
+      return rc;
+    if ((rc = resid_norm_launch(d_h, d_part, sp_o, R, nullptr, R, w.ln2, H, m.rms_eps, d_xn, true,
+                                st)))
+      return rc;
+    if ((rc = proj(m_xn, w.m_gu, BN_GU, 1, EPI_SWIGLU, R, 2 * F, H, nullptr, d_act, F))) return rc;
+    if ((rc = proj(m_act, w.m_down, BN_DOWN, sp_down, EPI_PARTIAL, R, H, F, nullptr, nullptr, 0)))
+      return rc;
+    if (l + 1 < m.layers &&
+        (rc = resid_norm_launch(d_h, d_part, sp_down, R, nullptr, R, L[l + 1].ln1, H, m.rms_eps,
+                                d_xn, true, st)))
+      return rc;
   }
+  pending_rows = R;   // the last down projection's partials wait for the head
   return RLB_OK;
 }
 
-// Final norm over the rows listed in d_logit_src, lm_head, and (optionally)
-// argmax + append into the slots listed in d_logit_slot.
+int rlb_instance::proj(const CUtensorMap& a, const CUtensorMap& b, int bn, int splits, int epi,
+                       int R, int N, int K, const bf16* bias, void* out, int ldo) {
+  GemmParams p{R, N, K, bias, out, ldo, splits < 1 ? 1 : splits, d_part};
+  return gemm_launch(a, b, bn, epi, p, st);
+}
+
+// Final residual (last down projection's partials) + RMSNorm over the rows
+// listed in d_logit_src, lm_head, and (optionally) argmax + append into the
+// slots listed in d_logit_slot.  h is not written, so the head can run over
+// several row blocks of one forward.
 int rlb_instance::head(int Lrows, bool append) {
   if (Lrows <= 0) return RLB_OK;
   int rc;
-  if ((rc = rmsnorm_launch(d_h, H, d_logit_src, Lrows, norm, H, m.rms_eps, d_xn, H, st))) return rc;
-  if (!append) {
-    GemmParams p{Lrows, V, H, nullptr, d_logits, V};
-    return gemm_launch(m_xn, m_lm, BN_LM, EPI_F32, p, st);
-  }
+  if ((rc = resid_norm_launch(d_h, d_part, sp_down, pending_rows, d_logit_src, Lrows, norm, H,
+                              m.rms_eps, d_xn, false, st)))
+    return rc;
+  if (!append) return proj(m_xn, m_lm, BN_LM, 1, EPI_F32, Lrows, V, H, nullptr, d_logits, V);
   const int ntiles = (V + BN_LM - 1) / BN_LM;
-  GemmParams p{Lrows, V, H, nullptr, d_logits, ntiles};
-  if ((rc = gemm_launch(m_xn, m_lm, BN_LM, EPI_ARGMAX, p, st))) return rc;
+  if ((rc = proj(m_xn, m_lm, BN_LM, 1, EPI_ARGMAX, Lrows, V, H, nullptr, d_logits, ntiles)))
+    return rc;
   return argmax_append_launch(reinterpret_cast<const float2*>(d_logits), ntiles, Lrows,
                               d_logit_slot, d_seq_tokens, d_seq_len, d_seq_target, max_seq, d_ring,
                               d_ring_cur, max_slots, st);
@@ -409,6 +460,10 @@ int rlb_instance::admit_and_prefill(int* rows_run) {
   size_t beg = 0;
   size_t ri = 0;          // request whose rows are being placed
   size_t rrow = 0;        // rows of admitted[ri] already placed
+  // every slot gets exactly one first token during the prefill, so all chunks
+  // share one ring row
+  if ((rc = ring_advance_launch(d_ring_ctr, d_ring_cur, st))) return rc;
+  stats.kernel_launches += 1;
   while (beg < total_rows) {
     const size_t n = std::min<size_t>(prefill_rows, total_rows - beg);
     // logits rows: sequences whose last row falls inside [beg, beg+n)
@@ -438,11 +493,10 @@ int rlb_instance::admit_and_prefill(int* rows_run) {
     if ((rc = seed_tokens_launch(d_row_tok, d_row_pos, d_row_slot, static_cast<int>(n), d_seq_tokens,
                                  max_seq, st)))
       return rc;
-    if ((rc = ring_advance_launch(d_ring_ctr, d_ring_cur, st))) return rc;
     if ((rc = forward_layers(static_cast<int>(n)))) return rc;
     if ((rc = head(nl, true))) return rc;
     stats.h2d_bytes += static_cast<int64_t>(n) * 12 + static_cast<int64_t>(nl) * 8;
-    stats.kernel_launches += 2 + launches_per_forward(nl);
+    stats.kernel_launches += 1 + launches_per_forward(nl);
     beg += n;
   }
   stats.prefill_rows += static_cast<int64_t>(total_rows);
@@ -811,17 +865,18 @@ int rlb_profile_kernel(rlb_instance* h, int32_t which, int32_t iters, double* av
                    h->NKV, D, h->max_splits, h->d_ws, h->d_attn, NQ * D};
         return attention_launch(a, h->st);
       }
-      case 1: return gemm_launch(h->m_xn, w.m_gu, BN_GU, EPI_SWIGLU,
-                                 GemmParams{R, 2 * F, H, nullptr, h->d_act, F}, h->st);
-      case 2: return gemm_launch(h->m_act, w.m_down, BN_DOWN, EPI_F32,
-                                 GemmParams{R, H, F, nullptr, h->d_logits, H}, h->st);
-      case 3: return gemm_launch(h->m_xn, w.m_qkv, BN_QKV, EPI_BF16,
-                                 GemmParams{R, h->QKV, H, w.bqkv, h->d_qkv, h->QKV}, h->st);
-      case 4: return gemm_launch(h->m_attn, w.m_o, BN_O, EPI_F32,
-                                 GemmParams{R, H, NQ * D, nullptr, h->d_logits, H}, h->st);
-      case 5: return gemm_launch(h->m_xn, h->m_lm, BN_LM, EPI_ARGMAX,
-                                 GemmParams{R, h->V, H, nullptr, h->d_logits,
-                                            (h->V + BN_LM - 1) / BN_LM}, h->st);
+      // split projections: the GEMM writing its split-K partials (the reduce
+      // is fused into the consumer kernel and not counted here)
+      case 1: return h->proj(h->m_xn, w.m_gu, BN_GU, 1, EPI_SWIGLU, R, 2 * F, H, nullptr,
+                             h->d_act, F);
+      case 2: return h->proj(h->m_act, w.m_down, BN_DOWN, h->sp_down, EPI_PARTIAL, R, H, F,
+                             nullptr, nullptr, 0);
+      case 3: return h->proj(h->m_xn, w.m_qkv, BN_QKV, h->sp_qkv, EPI_PARTIAL, R, h->QKV, H,
+                             nullptr, nullptr, 0);
+      case 4: return h->proj(h->m_attn, w.m_o, BN_O, h->sp_o, EPI_PARTIAL, R, H, NQ * D, nullptr,
+                             nullptr, 0);
+      case 5: return h->proj(h->m_xn, h->m_lm, BN_LM, 1, EPI_ARGMAX, R, h->V, H, nullptr,
+                             h->d_logits, (h->V + BN_LM - 1) / BN_LM);
     }
     set_error("unknown kernel id");
     return RLB_ERR_ARG;

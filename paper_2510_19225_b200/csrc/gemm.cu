@@ -1,50 +1,101 @@
-// K2: tcgen05 + TMA GEMMs for the dense projections of the decode step.
+// K2: tcgen05 + TMA GEMMs for the dense projections.
 //
 //   C[M, N] = A[M, K] . B[N, K]^T      (A = activations, B = weights; both K-major bf16)
 //
-// One CTA computes one 128 x BN tile.  Warp roles (256 threads):
-//   warp 0     one elected lane issues TMA loads (A 128x64, B BNx64, 128B swizzle)
-//              into a STAGES-deep smem ring guarded by full/empty mbarriers;
-//   warp 1     one elected lane issues tcgen05.mma (M=128, N=BN, K=16) into a
-//              TMEM fp32 accumulator and frees smem stages with tcgen05.commit;
-//   warp 2     allocates / frees the TMEM columns;
-//   warps 4-7  epilogue: tcgen05.ld 32 lanes x 16 columns -> registers -> fused
-//              op (bias / fp32 residual add / SwiGLU / fp32 store) -> global.
-//
-// Batch invariance (SURVEY.md §7 hard part 2): an output row depends only on
-// its A row and on B; the K loop order is fixed and there is no split-K, so a
-// token row gets bit-identical results whether it runs in a 512-row decode
-// batch or inside a 16k-row varlen prefill chunk.  Migration resume relies on
-// this.
+// One CTA computes a 256 x BN tile as two 128 x BN UMMA accumulators in TMEM
+// that share every B stage (the B tile is read from L2 once per 256 rows, so
+// a decode step at M=512 reads each weight tile twice, not four times).
+// Warp roles (384 threads):
+//   warp 0      one elected lane issues TMA loads: A rows [m, m+128), A rows
+//               [m+128, m+256) and B rows [n, n+BN), 64-element (128 B) K
+//               slices with the 128B swizzle, into a STAGES-deep smem ring
+//               guarded by full/empty mbarriers;
+//   warp 1      one elected lane issues tcgen05.mma (M=128, N=BN, K=16) for
+//               both halves and releases stages with tcgen05.commit;
+//   warp 2      allocates / frees 2*BN TMEM columns;
+//   warps 4-11  epilogue: warps 4-7 drain accumulator 0, warps 8-11
+//               accumulator 1 (tcgen05.ld 32 lanes x 16 columns) and apply the
+//               fused op: bias+bf16 / fp32 residual add / SwiGLU / fp32 /
+//               greedy argmax partials.
+// Split-K (grid.z = splits) covers the small-N projections of a decode step:
+// each split stores an fp32 partial and the last CTA of the tile to arrive
+// (atomic tile counter) sums the partials in split order and applies the
+// epilogue -- no extra launch.  The split count is a property of the weight
+// matrix (never of M), so a token row's result is bit-identical in a 512-row
+// decode batch and in a varlen prefill chunk -- migration resume relies on
+// this (SURVEY.md §7 hard part 2).
 #include "internal.h"
 
 namespace rlb {
 
-constexpr int BM = 128;
-constexpr int BK = 64;
+constexpr int BM = 256;      // rows per CTA (two UMMA_M=128 accumulators)
+constexpr int HM = 128;      // rows per accumulator
+constexpr int BK = 64;       // K elements per stage (one 128 B swizzle atom)
+constexpr int GEMM_THREADS = 384;
 
 template <int BN>
 struct GemmCfg {
-  static constexpr int A_BYTES = BM * BK * 2;
+  static constexpr int A_BYTES = HM * BK * 2;          // one half
   static constexpr int B_BYTES = BN * BK * 2;
-  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int STAGES = BN == 256 ? 4 : (BN == 128 ? 6 : 8);
+  static constexpr int STAGE_BYTES = 2 * A_BYTES + B_BYTES;
+  static constexpr int STAGES = BN == 256 ? 3 : 4;
   static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 256;
-  static constexpr uint32_t TMEM_COLS = BN < 32 ? 32 : BN;
+  static constexpr uint32_t TMEM_COLS = 2 * BN;
 };
 
 __device__ __forceinline__ float silu_f(float g) { return g / (1.0f + expf(-g)); }
 
+// Generic split-K reduce (kernel-level test entry rlb_gemm only; the engine
+// fuses the reduction into its row-wise consumer kernels): sum the fp32
+// partials of each row in split order and apply the epilogue.
+template <int EPI>
+__global__ void __launch_bounds__(256) splitk_reduce_kernel(GemmParams p) {
+  const int m = blockIdx.x;
+  const size_t slab = static_cast<size_t>(p.M) * p.N;
+#pragma unroll 1
+  for (int n = threadIdx.x * 4; n < p.N; n += 1024) {
+    const float* src = p.ws + static_cast<size_t>(m) * p.N + n;
+    float4 acc = __ldcg(reinterpret_cast<const float4*>(src));
+    for (int z = 1; z < p.splits; ++z) {
+      const float4 v = __ldcg(reinterpret_cast<const float4*>(src + z * slab));
+      acc.x += v.x;
+      acc.y += v.y;
+      acc.z += v.z;
+      acc.w += v.w;
+    }
+    if constexpr (EPI == EPI_BF16) {
+      if (p.bias) {
+        acc.x += __bfloat162float(p.bias[n]);
+        acc.y += __bfloat162float(p.bias[n + 1]);
+        acc.z += __bfloat162float(p.bias[n + 2]);
+        acc.w += __bfloat162float(p.bias[n + 3]);
+      }
+      *reinterpret_cast<uint2*>(reinterpret_cast<bf16*>(p.out) + static_cast<size_t>(m) * p.ldo + n) =
+          make_uint2(pack_bf2(acc.x, acc.y), pack_bf2(acc.z, acc.w));
+    } else if constexpr (EPI == EPI_RESADD) {
+      float4* h = reinterpret_cast<float4*>(reinterpret_cast<float*>(p.out) +
+                                            static_cast<size_t>(m) * p.ldo + n);
+      float4 x = *h;
+      x.x += acc.x;
+      x.y += acc.y;
+      x.z += acc.z;
+      x.w += acc.w;
+      *h = x;
+    } else if constexpr (EPI == EPI_F32) {
+      *reinterpret_cast<float4*>(reinterpret_cast<float*>(p.out) + static_cast<size_t>(m) * p.ldo + n) =
+          acc;
+    }
+  }
+}
+
 template <int BN, int EPI>
-__global__ void __launch_bounds__(256, 1)
+__global__ void __launch_bounds__(GEMM_THREADS, 1)
     gemm_bf16_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                  GemmParams p) {
   using C = GemmCfg<BN>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~static_cast<uintptr_t>(1023));
-  uint8_t* sA = smem;
-  uint8_t* sB = smem + C::STAGES * C::A_BYTES;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE_BYTES);
   uint64_t* full = bars;
   uint64_t* empty = bars + C::STAGES;
@@ -53,9 +104,11 @@ __global__ void __launch_bounds__(256, 1)
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  const int m_blk = blockIdx.y;
   const int n_blk = blockIdx.x;
-  const int nk = p.K / BK;
+  const int m_blk = blockIdx.y;
+  const int nk_total = p.K / BK;
+  const int nk = nk_total / p.splits;          // k-blocks of this split
+  const int kb0 = blockIdx.z * nk;
 
   if (warp == 0 && lane == 0) {
     tma_prefetch(&tmA);
@@ -78,39 +131,45 @@ __global__ void __launch_bounds__(256, 1)
       for (int kb = 0; kb < nk; ++kb) {
         const int s = kb % C::STAGES;
         const uint32_t ph = (kb / C::STAGES) & 1;
+        uint8_t* st = smem + s * C::STAGE_BYTES;
         mbar_wait(smem_u32(&empty[s]), ph ^ 1);
         mbar_expect_tx(smem_u32(&full[s]), C::STAGE_BYTES);
-        tma_load_2d(smem_u32(sA + s * C::A_BYTES), &tmA, smem_u32(&full[s]), kb * BK, m_blk * BM);
-        tma_load_2d(smem_u32(sB + s * C::B_BYTES), &tmB, smem_u32(&full[s]), kb * BK, n_blk * BN);
+        const int kx = (kb0 + kb) * BK;
+        tma_load_2d(smem_u32(st), &tmA, smem_u32(&full[s]), kx, m_blk * BM);
+        tma_load_2d(smem_u32(st + C::A_BYTES), &tmA, smem_u32(&full[s]), kx, m_blk * BM + HM);
+        tma_load_2d(smem_u32(st + 2 * C::A_BYTES), &tmB, smem_u32(&full[s]), kx, n_blk * BN);
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {
-      constexpr uint32_t idesc = umma_idesc_bf16(BM, BN);
+      constexpr uint32_t idesc = umma_idesc_bf16(HM, BN);
       for (int kb = 0; kb < nk; ++kb) {
         const int s = kb % C::STAGES;
         const uint32_t ph = (kb / C::STAGES) & 1;
+        const uint32_t st = smem_u32(smem + s * C::STAGE_BYTES);
         mbar_wait(smem_u32(&full[s]), ph);
         tc_fence_after();
-        const uint64_t ad = umma_desc_sw128(smem_u32(sA + s * C::A_BYTES));
-        const uint64_t bd = umma_desc_sw128(smem_u32(sB + s * C::B_BYTES));
+        const uint64_t a0 = umma_desc_sw128(st);
+        const uint64_t a1 = umma_desc_sw128(st + C::A_BYTES);
+        const uint64_t bd = umma_desc_sw128(st + 2 * C::A_BYTES);
 #pragma unroll
         for (int k = 0; k < BK / 16; ++k) {
           // +32 bytes per K=16 step inside the 128 B swizzle atom (encoded >> 4)
-          umma_bf16(tmem, ad + 2 * k, bd + 2 * k, idesc, (kb | k) != 0);
+          umma_bf16(tmem, a0 + 2 * k, bd + 2 * k, idesc, (kb | k) != 0);
+          umma_bf16(tmem + BN, a1 + 2 * k, bd + 2 * k, idesc, (kb | k) != 0);
         }
         umma_commit(smem_u32(&empty[s]));
       }
       umma_commit(smem_u32(tfull));
     }
   } else if (warp >= 4) {
-    const int q = warp & 3;
-    const int row = q * 32 + lane;
-    const int m = m_blk * BM + row;
+    const int half = (warp - 4) >> 2;          // accumulator 0 or 1
+    const int q = warp & 3;                    // TMEM lane quadrant
+    const int m = m_blk * BM + half * HM + q * 32 + lane;
     const bool live = m < p.M;
     mbar_wait(smem_u32(tfull), 0);
     tc_fence_after();
-    const uint32_t tbase = tmem + (static_cast<uint32_t>(q * 32) << 16);
+    const uint32_t tbase = tmem + half * BN + (static_cast<uint32_t>(q * 32) << 16);
     if constexpr (EPI == EPI_SWIGLU) {
       bf16* out = reinterpret_cast<bf16*>(p.out);
 #pragma unroll 1
@@ -139,7 +198,7 @@ __global__ void __launch_bounds__(256, 1)
       }
     } else if constexpr (EPI == EPI_ARGMAX) {
       // greedy head: per (row, N-tile) max and its lowest column index; the
-      // full-vocab fp32 logits never reach HBM.
+      // full-vocab logits never reach HBM.
       float best = -INFINITY;
       int bidx = 0x7fffffff;
 #pragma unroll 1
@@ -160,6 +219,23 @@ __global__ void __launch_bounds__(256, 1)
       if (live) {
         float2* part = reinterpret_cast<float2*>(p.out) + static_cast<size_t>(m) * p.ldo + n_blk;
         *part = make_float2(best, __int_as_float(bidx));
+      }
+    } else if constexpr (EPI == EPI_PARTIAL) {
+      // split-K: store this K range's fp32 partial [z][M][N]; the row-wise
+      // consumer kernel sums the splits in order and applies the epilogue.
+      float* part = p.ws + static_cast<size_t>(blockIdx.z) * p.M * p.N;
+#pragma unroll 1
+      for (int c = 0; c < BN; c += 16) {
+        uint32_t r[16];
+        tmem_ld16(tbase + c, r);
+        tmem_ld_wait();
+        const int n = n_blk * BN + c;
+        if (!live || n >= p.N) continue;
+        float4* o = reinterpret_cast<float4*>(part + static_cast<size_t>(m) * p.N + n);
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+          o[i] = make_float4(__uint_as_float(r[4 * i]), __uint_as_float(r[4 * i + 1]),
+                             __uint_as_float(r[4 * i + 2]), __uint_as_float(r[4 * i + 3]));
       }
     } else {
 #pragma unroll 1
@@ -203,8 +279,8 @@ __global__ void __launch_bounds__(256, 1)
             h[i] = x;
           }
         } else {  // EPI_F32
-          float4* o = reinterpret_cast<float4*>(reinterpret_cast<float*>(p.out) +
-                                                static_cast<size_t>(m) * p.ldo + n);
+          float* base = reinterpret_cast<float*>(p.out);
+          float4* o = reinterpret_cast<float4*>(base + static_cast<size_t>(m) * p.ldo + n);
 #pragma unroll
           for (int i = 0; i < 4; ++i)
             o[i] = make_float4(__uint_as_float(r[4 * i]), __uint_as_float(r[4 * i + 1]),
@@ -268,9 +344,9 @@ template <int BN>
 static int set_attr_bn() {
   int rc;
   if ((rc = set_attr<BN, EPI_BF16>()) || (rc = set_attr<BN, EPI_RESADD>()) ||
-      (rc = set_attr<BN, EPI_F32>()) || (rc = set_attr<BN, EPI_ARGMAX>()))
+      (rc = set_attr<BN, EPI_F32>()) || (rc = set_attr<BN, EPI_ARGMAX>()) ||
+      (rc = set_attr<BN, EPI_SWIGLU>()) || (rc = set_attr<BN, EPI_PARTIAL>()))
     return rc;
-  if constexpr (BN >= 128) return set_attr<BN, EPI_SWIGLU>();
   return RLB_OK;
 }
 
@@ -280,7 +356,7 @@ int gemm_prepare() {
   RLB_CUDA(cudaGetDevice(&dev));
   if (done[dev & 63]) return RLB_OK;
   int rc;
-  if ((rc = set_attr_bn<64>()) || (rc = set_attr_bn<128>()) || (rc = set_attr_bn<256>())) return rc;
+  if ((rc = set_attr_bn<128>()) || (rc = set_attr_bn<256>())) return rc;
   done[dev & 63] = true;
   return RLB_OK;
 }
@@ -289,8 +365,8 @@ template <int BN, int EPI>
 static int launch_one(const CUtensorMap& a, const CUtensorMap& b, const GemmParams& p,
                       cudaStream_t st) {
   using C = GemmCfg<BN>;
-  dim3 grid((p.N + BN - 1) / BN, (p.M + BM - 1) / BM);
-  gemm_bf16_tc<BN, EPI><<<grid, 256, C::SMEM, st>>>(a, b, p);
+  dim3 grid((p.N + BN - 1) / BN, (p.M + BM - 1) / BM, p.splits);
+  gemm_bf16_tc<BN, EPI><<<grid, GEMM_THREADS, C::SMEM, st>>>(a, b, p);
   RLB_CUDA(cudaGetLastError());
   return RLB_OK;
 }
@@ -301,11 +377,10 @@ static int launch_bn(const CUtensorMap& a, const CUtensorMap& b, int epi, const 
   switch (epi) {
     case EPI_BF16: return launch_one<BN, EPI_BF16>(a, b, p, st);
     case EPI_RESADD: return launch_one<BN, EPI_RESADD>(a, b, p, st);
-    case EPI_SWIGLU:
-      if constexpr (BN >= 128) return launch_one<BN, EPI_SWIGLU>(a, b, p, st);
-      break;
+    case EPI_SWIGLU: return launch_one<BN, EPI_SWIGLU>(a, b, p, st);
     case EPI_F32: return launch_one<BN, EPI_F32>(a, b, p, st);
     case EPI_ARGMAX: return launch_one<BN, EPI_ARGMAX>(a, b, p, st);
+    case EPI_PARTIAL: return launch_one<BN, EPI_PARTIAL>(a, b, p, st);
   }
   set_error("bad epilogue");
   return RLB_ERR_ARG;
@@ -315,38 +390,58 @@ int gemm_launch(const CUtensorMap& a, const CUtensorMap& b, int block_n, int epi
                 const GemmParams& p, cudaStream_t st) {
   if (p.M <= 0) return RLB_OK;
   RLB_CHECK(p.K % BK == 0 && p.N % 16 == 0, RLB_ERR_ARG, "GEMM shape not tileable");
+  RLB_CHECK(p.splits >= 1 && (p.K / BK) % p.splits == 0, RLB_ERR_ARG,
+            "split-K must divide the K blocks");
+  RLB_CHECK((p.splits == 1 && epi != EPI_PARTIAL) || (epi == EPI_PARTIAL && p.ws != nullptr),
+            RLB_ERR_ARG, "split-K GEMMs write fp32 partials to a workspace (EPI_PARTIAL)");
   RLB_CHECK(epi != EPI_SWIGLU || (block_n % 128 == 0 && p.N % 128 == 0), RLB_ERR_ARG,
             "SwiGLU GEMM needs 128-column gate/up tiles");
   switch (block_n) {
-    case 64: return launch_bn<64>(a, b, epi, p, st);
     case 128: return launch_bn<128>(a, b, epi, p, st);
     case 256: return launch_bn<256>(a, b, epi, p, st);
   }
-  set_error("block_n must be 64, 128 or 256");
+  set_error("block_n must be 128 or 256");
   return RLB_ERR_ARG;
 }
 
 }  // namespace rlb
 
 extern "C" int rlb_gemm(int device, int32_t M, int32_t N, int32_t K, const void* A, const void* B,
-                        const void* bias, void* Cout, int32_t epilogue, int32_t block_n) {
+                        const void* bias, void* Cout, int32_t epilogue, int32_t block_n,
+                        int32_t splits) {
   using namespace rlb;
   RLB_CUDA(cudaSetDevice(device));
   int rc = gemm_prepare();
   if (rc) return rc;
   CUtensorMap ma, mb;
-  rc = make_kmajor_map(&ma, A, M, K, BM);
+  rc = make_kmajor_map(&ma, A, M, K, HM);
   if (rc) return rc;
   rc = make_kmajor_map(&mb, B, N, K, block_n);
   if (rc) return rc;
-  GemmParams p;
+  GemmParams p{};
   p.M = M;
   p.N = N;
   p.K = K;
   p.bias = static_cast<const bf16*>(bias);
   p.out = Cout;
   p.ldo = epilogue == EPI_SWIGLU ? N / 2 : N;
-  rc = gemm_launch(ma, mb, block_n, epilogue, p, 0);
+  p.splits = splits < 1 ? 1 : splits;
+  if (p.splits == 1) {
+    rc = gemm_launch(ma, mb, block_n, epilogue, p, 0);
+  } else {
+    RLB_CUDA(cudaMalloc(&p.ws, sizeof(float) * static_cast<size_t>(p.splits) * M * N));
+    rc = gemm_launch(ma, mb, block_n, EPI_PARTIAL, p, 0);
+    if (!rc) {
+      switch (epilogue) {
+        case EPI_BF16: splitk_reduce_kernel<EPI_BF16><<<M, 256>>>(p); break;
+        case EPI_RESADD: splitk_reduce_kernel<EPI_RESADD><<<M, 256>>>(p); break;
+        case EPI_F32: splitk_reduce_kernel<EPI_F32><<<M, 256>>>(p); break;
+        default: set_error("split-K supports epilogues 0, 1, 3"); rc = RLB_ERR_ARG;
+      }
+    }
+    cudaDeviceSynchronize();
+    cudaFree(p.ws);
+  }
   if (rc) return rc;
   RLB_CUDA(cudaDeviceSynchronize());
   return RLB_OK;

@@ -8,15 +8,17 @@
 namespace rlb {
 
 constexpr int PAGE = 64;      // tokens per KV page
-constexpr int SPLIT = 256;    // fixed split-K boundary of decode attention (tokens)
 
-enum Epi { EPI_BF16 = 0, EPI_RESADD = 1, EPI_SWIGLU = 2, EPI_F32 = 3, EPI_ARGMAX = 4 };
+enum Epi { EPI_BF16 = 0, EPI_RESADD = 1, EPI_SWIGLU = 2, EPI_F32 = 3, EPI_ARGMAX = 4,
+           EPI_PARTIAL = 5 };
 
 struct GemmParams {
   int M, N, K;
   const bf16* bias;
   void* out;
   int ldo;
+  int splits;     // split-K factor (1 = no split)
+  float* ws;      // EPI_PARTIAL: fp32 partials [splits][M][N]
 };
 
 int make_kmajor_map(CUtensorMap* map, const void* ptr, int64_t rows, int64_t k, int box_rows);
@@ -35,13 +37,15 @@ struct AttnArgs {
   bf16* out; int ldo;
 };
 int attention_launch(const AttnArgs& a, cudaStream_t st);
+int attention_windows(int max_seq);   // CTA windows per row (AttnArgs.max_splits)
 
 int embed_launch(const bf16* embed, int H, const int* tok, int R, float* h, cudaStream_t st);
-int rmsnorm_launch(const float* x, int ldx, const int* src_rows, int R, const bf16* w, int H,
-                   float eps, bf16* out, int ldo, cudaStream_t st);
-int rope_append_launch(const bf16* qkv, int ldqkv, const int* row_slot, const int* row_pos, int R,
-                       const float2* rope, int NQ, int NKV, int D, bf16* qout, int ldq, bf16* kv,
-                       const int* block_table, int bt_stride, cudaStream_t st);
+int resid_norm_launch(float* h, const float* part, int S, int Mp, const int* src_rows, int R,
+                      const bf16* w, int H, float eps, bf16* xn, bool write_h, cudaStream_t st);
+int qkv_rope_launch(const float* part, int S, int Mp, const bf16* bias, const int* row_slot,
+                    const int* row_pos, int R, const float2* rope, int NQ, int NKV, int D,
+                    bf16* qout, int ldq, bf16* kv, const int* block_table, int bt_stride,
+                    cudaStream_t st);
 int argmax_append_launch(const float2* part, int ntiles, int L, const int* logit_slot,
                          int32_t* seq_tokens, int32_t* seq_len, const int32_t* seq_target,
                          int max_seq, int32_t* ring, const int32_t* ring_cur, int max_slots,

@@ -26,92 +26,6 @@ int embed_launch(const bf16* embed, int H, const int* tok, int R, float* h, cuda
   return RLB_OK;
 }
 
-// ------------------------------------------------------------ rmsnorm ----
-__global__ void __launch_bounds__(256) rmsnorm_kernel(const float* __restrict__ x, int ldx,
-                                                      const int* __restrict__ src_rows,
-                                                      const bf16* __restrict__ w, int H, float eps,
-                                                      bf16* __restrict__ out, int ldo) {
-  __shared__ float part[8];
-  const int ro = blockIdx.x;
-  const int ri = src_rows ? src_rows[ro] : ro;
-  const float* xr = x + static_cast<size_t>(ri) * ldx;
-  float ss = 0.f;
-  for (int i = threadIdx.x; i < H; i += 256) ss = __fmaf_rn(xr[i], xr[i], ss);
-#pragma unroll
-  for (int off = 16; off > 0; off >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, off);
-  if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = ss;
-  __syncthreads();
-  float tot = 0.f;
-#pragma unroll
-  for (int k = 0; k < 8; ++k) tot += part[k];
-  const float inv = rsqrtf(tot / static_cast<float>(H) + eps);
-  bf16* orow = out + static_cast<size_t>(ro) * ldo;
-  for (int i = threadIdx.x; i < H; i += 256)
-    orow[i] = __float2bfloat16_rn((xr[i] * inv) * __bfloat162float(w[i]));
-}
-
-int rmsnorm_launch(const float* x, int ldx, const int* src_rows, int R, const bf16* w, int H,
-                   float eps, bf16* out, int ldo, cudaStream_t st) {
-  if (R <= 0) return RLB_OK;
-  rmsnorm_kernel<<<R, 256, 0, st>>>(x, ldx, src_rows, w, H, eps, out, ldo);
-  RLB_CUDA(cudaGetLastError());
-  return RLB_OK;
-}
-
-// -------------------------------------------------- rope + KV append -----
-// q heads: rotated into qout; k heads: rotated, written to the slot's page;
-// v heads: copied to the page.  rope[pos][j] = (cos, sin) of pos * theta^(-2j/D).
-__global__ void rope_append_kernel(const bf16* __restrict__ qkv, int ldqkv,
-                                   const int* __restrict__ row_slot,
-                                   const int* __restrict__ row_pos,
-                                   const float2* __restrict__ rope, int NQ, int NKV, int D,
-                                   bf16* __restrict__ qout, int ldq, bf16* __restrict__ kv,
-                                   const int* __restrict__ block_table, int bt_stride) {
-  const int r = blockIdx.x;
-  const int half = D / 2;
-  const int pos = row_pos[r];
-  const int page = block_table[static_cast<size_t>(row_slot[r]) * bt_stride + pos / PAGE];
-  const size_t head_stride = static_cast<size_t>(2) * PAGE * D;
-  bf16* kv_page = kv + static_cast<size_t>(page) * head_stride * NKV +
-                  static_cast<size_t>(pos % PAGE) * D;
-  const bf16* in = qkv + static_cast<size_t>(r) * ldqkv;
-  const float2* cs = rope + static_cast<size_t>(pos) * half;
-  const int total = (NQ + 2 * NKV) * half;
-  for (int i = threadIdx.x; i < total; i += blockDim.x) {
-    const int head = i / half, j = i % half;
-    const float x1 = __bfloat162float(in[head * D + j]);
-    const float x2 = __bfloat162float(in[head * D + j + half]);
-    if (head < NQ + NKV) {
-      const float2 c = cs[j];
-      const float y1 = __fmaf_rn(x1, c.x, -x2 * c.y);
-      const float y2 = __fmaf_rn(x2, c.x, x1 * c.y);
-      if (head < NQ) {
-        bf16* o = qout + static_cast<size_t>(r) * ldq + head * D;
-        o[j] = __float2bfloat16_rn(y1);
-        o[j + half] = __float2bfloat16_rn(y2);
-      } else {
-        bf16* o = kv_page + static_cast<size_t>(head - NQ) * head_stride;
-        o[j] = __float2bfloat16_rn(y1);
-        o[j + half] = __float2bfloat16_rn(y2);
-      }
-    } else {
-      bf16* o = kv_page + static_cast<size_t>(head - NQ - NKV) * head_stride +
-                static_cast<size_t>(PAGE) * D;
-      o[j] = in[head * D + j];
-      o[j + half] = in[head * D + j + half];
-    }
-  }
-}
-
-int rope_append_launch(const bf16* qkv, int ldqkv, const int* row_slot, const int* row_pos, int R,
-                       const float2* rope, int NQ, int NKV, int D, bf16* qout, int ldq, bf16* kv,
-                       const int* block_table, int bt_stride, cudaStream_t st) {
-  if (R <= 0) return RLB_OK;
-  rope_append_kernel<<<R, 256, 0, st>>>(qkv, ldqkv, row_slot, row_pos, rope, NQ, NKV, D, qout, ldq,
-                                        kv, block_table, bt_stride);
-  RLB_CUDA(cudaGetLastError());
-  return RLB_OK;
-}
 
 // ---------------------------------------------- argmax + response append --
 // Greedy token (lowest index on ties) of each logits row, appended to the

@@ -249,7 +249,8 @@ class RolloutInstance:
                 got.setdefault(rid, []).extend(toks.tolist())
 
 
-def gemm(device: int, A, B, bias=None, out=None, epilogue: int = 0, block_n: int = 128):
+def gemm(device: int, A, B, bias=None, out=None, epilogue: int = 0, block_n: int = 128,
+         splits: int = 1):
     """Kernel-level entry point rlb_gemm on torch CUDA tensors (parity tests)."""
     import torch
     M, K = A.shape
@@ -263,5 +264,5 @@ def gemm(device: int, A, B, bias=None, out=None, epilogue: int = 0, block_n: int
             out = torch.zeros(M, N, dtype=torch.float32, device=A.device)
     check(_lib.lib().rlb_gemm(device, M, N, K, A.data_ptr(), B.data_ptr(),
                               bias.data_ptr() if bias is not None else None, out.data_ptr(),
-                              epilogue, block_n))
+                              epilogue, block_n, splits))
     return out
