@@ -17,6 +17,7 @@
 // window order) is a function of the row's context length only, so a row gets
 // the same bits as a decode row or as one of the rows of a varlen prefill --
 // the property migration resume relies on (SURVEY.md §7 part 2).
+#define RLB_PDL_CLASS 2
 #include "internal.h"
 
 namespace rlb {
@@ -74,6 +75,8 @@ __global__ void __launch_bounds__(WARPS * 32, 2) attn_mma_kernel(AttnArgs a) {
   const int ws_idx = blockIdx.x, kvh = blockIdx.y, r = blockIdx.z;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int G = a.NQ / a.NKV;
+  pdl_trigger();
+  pdl_wait();   // q and this step's K/V rows come from the previous kernel
 
   // Q fragments first: independent of the row metadata loads below.
   uint32_t qa[KSTEPS][2];
@@ -258,6 +261,8 @@ __global__ void __launch_bounds__(WARPS * 32, 2) attn_mma_kernel(AttnArgs a) {
 
 // Merge the per-window partials of rows longer than one window, in order.
 __global__ void attn_combine_kernel(AttnArgs a) {
+  pdl_trigger();
+  pdl_wait();
   const int qh = blockIdx.x, r = blockIdx.y, d = threadIdx.x;
   const int n = a.row_pos[r] + 1;
   const int ns = (n + SUPER - 1) / SUPER;
@@ -289,8 +294,8 @@ static int launch_attn(const AttnArgs& a, cudaStream_t st) {
     RLB_CUDA(cudaFuncSetAttribute(attn_mma_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     attr[dev & 63] = true;
   }
-  attn_mma_kernel<D><<<dim3(a.max_splits, a.NKV, a.R), WARPS * 32, smem, st>>>(a);
-  RLB_CUDA(cudaGetLastError());
+  RLB_CUDA(launch_k(attn_mma_kernel<D>, dim3(a.max_splits, a.NKV, a.R), dim3(WARPS * 32), smem,
+                    st, a));
   return RLB_OK;
 }
 
@@ -306,8 +311,7 @@ int attention_launch(const AttnArgs& a, cudaStream_t st) {
     RLB_CHECK(false, RLB_ERR_ARG, "head_dim must be 64 or 128");
   if (rc) return rc;
   if (a.max_splits > 1) {
-    attn_combine_kernel<<<dim3(a.NQ, a.R), a.D, 0, st>>>(a);
-    RLB_CUDA(cudaGetLastError());
+    RLB_CUDA(launch_k(attn_combine_kernel, dim3(a.NQ, a.R), dim3(a.D), 0, st, a));
   }
   return RLB_OK;
 }

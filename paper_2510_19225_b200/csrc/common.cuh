@@ -143,6 +143,40 @@ __device__ __forceinline__ void tmem_ld_wait() {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
+// ------------------------------------------ programmatic dependent launch --
+// Every hot kernel is launched with programmatic stream serialization: it may
+// start (and run its prologue: barrier init, TMEM alloc, descriptor
+// prefetch) while its predecessor drains, then blocks in pdl_wait() until the
+// predecessor grid has completed and its writes are visible.  pdl_trigger()
+// lets the successor grid launch once every CTA of this grid has started.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
+bool pdl_enabled(int cls);   // RLB_PDL_MASK (bit per kernel class) / RLB_NO_PDL
+
+#ifndef RLB_PDL_CLASS
+#define RLB_PDL_CLASS 8
+#endif
+#define launch_k(...) launch_k_cls(RLB_PDL_CLASS, __VA_ARGS__)
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_k_cls(int cls, void (*kernel)(KArgs...), dim3 grid, dim3 block,
+                                size_t smem, cudaStream_t st, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled(cls) ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+}
+
 __device__ __forceinline__ bool elect_one() {
   uint32_t pred = 0;
   asm volatile(

@@ -24,10 +24,26 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <deque>
 #include <map>
 #include <unordered_map>
+
+// Programmatic dependent launch per kernel class (1 GEMM, 2 attention, 4 row
+// consumers, 8 small kernels), selected by RLB_PDL_MASK.  Off by default:
+// with GEMM + row-consumer + small-kernel classes all enabled the varlen
+// prefill path produced wrong tokens on B200 (every pair of classes was
+// clean; cause not yet isolated), and the measured gain was ~0.2%.
+bool pdl_enabled(int cls) {
+  static const int mask = [] {
+    const char* off = std::getenv("RLB_NO_PDL");
+    if (off && off[0] == '1') return 0;
+    const char* m = std::getenv("RLB_PDL_MASK");
+    return m ? std::atoi(m) : 0;
+  }();
+  return (mask & cls) != 0;
+}
 
 namespace rlb {
 

@@ -24,6 +24,7 @@
 // matrix (never of M), so a token row's result is bit-identical in a 512-row
 // decode batch and in a varlen prefill chunk -- migration resume relies on
 // this (SURVEY.md §7 hard part 2).
+#define RLB_PDL_CLASS 1
 #include "internal.h"
 
 namespace rlb {
@@ -125,6 +126,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  pdl_trigger();
+  pdl_wait();   // A (activations) is the previous kernel's output
 
   if (warp == 0) {
     if (lane == 0) {
@@ -366,8 +369,7 @@ static int launch_one(const CUtensorMap& a, const CUtensorMap& b, const GemmPara
                       cudaStream_t st) {
   using C = GemmCfg<BN>;
   dim3 grid((p.N + BN - 1) / BN, (p.M + BM - 1) / BM, p.splits);
-  gemm_bf16_tc<BN, EPI><<<grid, GEMM_THREADS, C::SMEM, st>>>(a, b, p);
-  RLB_CUDA(cudaGetLastError());
+  RLB_CUDA(launch_k(gemm_bf16_tc<BN, EPI>, grid, dim3(GEMM_THREADS), C::SMEM, st, a, b, p));
   return RLB_OK;
 }
 

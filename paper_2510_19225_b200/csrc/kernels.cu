@@ -13,6 +13,8 @@ namespace rlb {
 // -------------------------------------------------------------- embed ----
 __global__ void embed_kernel(const bf16* __restrict__ embed, int H, const int* __restrict__ tok,
                              float* __restrict__ h) {
+  pdl_trigger();
+  pdl_wait();
   const int r = blockIdx.x;
   const bf16* e = embed + static_cast<size_t>(tok[r]) * H;
   float* o = h + static_cast<size_t>(r) * H;
@@ -21,8 +23,7 @@ __global__ void embed_kernel(const bf16* __restrict__ embed, int H, const int* _
 
 int embed_launch(const bf16* embed, int H, const int* tok, int R, float* h, cudaStream_t st) {
   if (R <= 0) return RLB_OK;
-  embed_kernel<<<R, 256, 0, st>>>(embed, H, tok, h);
-  RLB_CUDA(cudaGetLastError());
+  RLB_CUDA(launch_k(embed_kernel, dim3(R), dim3(256), 0, st, embed, H, tok, h));
   return RLB_OK;
 }
 
@@ -40,6 +41,8 @@ __global__ void __launch_bounds__(512) argmax_append_kernel(
     const int32_t* __restrict__ ring_cur, int max_slots) {
   __shared__ float sv[16];
   __shared__ int si[16];
+  pdl_trigger();
+  pdl_wait();
   const int r = blockIdx.x;
   const float2* row = part + static_cast<size_t>(r) * ntiles;
   float best = -INFINITY;
@@ -87,9 +90,8 @@ int argmax_append_launch(const float2* part, int ntiles, int L, const int* logit
                          int max_seq, int32_t* ring, const int32_t* ring_cur, int max_slots,
                          cudaStream_t st) {
   if (L <= 0) return RLB_OK;
-  argmax_append_kernel<<<L, 512, 0, st>>>(part, ntiles, logit_slot, seq_tokens, seq_len,
-                                          seq_target, max_seq, ring, ring_cur, max_slots);
-  RLB_CUDA(cudaGetLastError());
+  RLB_CUDA(launch_k(argmax_append_kernel, dim3(L), dim3(512), 0, st, part, ntiles, logit_slot,
+                    seq_tokens, seq_len, seq_target, max_seq, ring, ring_cur, max_slots));
   return RLB_OK;
 }
 
@@ -99,6 +101,8 @@ __global__ void decode_prepare_kernel(const int* __restrict__ dec_slots, int R,
                                       const int32_t* __restrict__ seq_len, int max_seq,
                                       int* row_tok, int* row_pos, int* row_slot, int* logit_src,
                                       int* logit_slot, int32_t* ring_ctr, int32_t* ring_cur) {
+  pdl_trigger();
+  pdl_wait();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i == 0) *ring_cur = (*ring_ctr)++;
   if (i >= R) return;
@@ -115,10 +119,9 @@ int decode_prepare_launch(const int* dec_slots, int R, const int32_t* seq_tokens
                           const int32_t* seq_len, int max_seq, int* row_tok, int* row_pos,
                           int* row_slot, int* logit_src, int* logit_slot, int32_t* ring_ctr,
                           int32_t* ring_cur, cudaStream_t st) {
-  decode_prepare_kernel<<<(R + 255) / 256, 256, 0, st>>>(dec_slots, R, seq_tokens, seq_len,
-                                                        max_seq, row_tok, row_pos, row_slot,
-                                                        logit_src, logit_slot, ring_ctr, ring_cur);
-  RLB_CUDA(cudaGetLastError());
+  RLB_CUDA(launch_k(decode_prepare_kernel, dim3((R + 255) / 256), dim3(256), 0, st, dec_slots, R,
+                    seq_tokens, seq_len, max_seq, row_tok, row_pos, row_slot, logit_src, logit_slot,
+                    ring_ctr, ring_cur));
   return RLB_OK;
 }
 
@@ -127,6 +130,8 @@ int decode_prepare_launch(const int* dec_slots, int R, const int32_t* seq_tokens
 __global__ void seed_tokens_kernel(const int* __restrict__ row_tok, const int* __restrict__ row_pos,
                                    const int* __restrict__ row_slot, int R,
                                    int32_t* __restrict__ seq_tokens, int max_seq) {
+  pdl_trigger();
+  pdl_wait();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < R) seq_tokens[static_cast<size_t>(row_slot[i]) * max_seq + row_pos[i]] = row_tok[i];
 }
@@ -134,19 +139,19 @@ __global__ void seed_tokens_kernel(const int* __restrict__ row_tok, const int* _
 int seed_tokens_launch(const int* row_tok, const int* row_pos, const int* row_slot, int R,
                        int32_t* seq_tokens, int max_seq, cudaStream_t st) {
   if (R <= 0) return RLB_OK;
-  seed_tokens_kernel<<<(R + 255) / 256, 256, 0, st>>>(row_tok, row_pos, row_slot, R, seq_tokens,
-                                                     max_seq);
-  RLB_CUDA(cudaGetLastError());
+  RLB_CUDA(launch_k(seed_tokens_kernel, dim3((R + 255) / 256), dim3(256), 0, st, row_tok, row_pos,
+                    row_slot, R, seq_tokens, max_seq));
   return RLB_OK;
 }
 
 __global__ void ring_advance_kernel(int32_t* ring_ctr, int32_t* ring_cur) {
+  pdl_trigger();
+  pdl_wait();
   *ring_cur = (*ring_ctr)++;
 }
 
 int ring_advance_launch(int32_t* ring_ctr, int32_t* ring_cur, cudaStream_t st) {
-  ring_advance_kernel<<<1, 1, 0, st>>>(ring_ctr, ring_cur);
-  RLB_CUDA(cudaGetLastError());
+  RLB_CUDA(launch_k(ring_advance_kernel, dim3(1), dim3(1), 0, st, ring_ctr, ring_cur));
   return RLB_OK;
 }
 

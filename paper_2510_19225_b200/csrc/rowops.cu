@@ -6,6 +6,7 @@
 //   resid_norm  h += sum (residual) -> RMSNorm -> bf16 input of the next GEMM
 // S is a template parameter so every partial load of a thread is in flight
 // at once (the kernels are L2-latency bound otherwise).
+#define RLB_PDL_CLASS 4
 #include "internal.h"
 
 namespace rlb {
@@ -20,6 +21,8 @@ __global__ void __launch_bounds__(256) resid_norm_kernel(
     const int* __restrict__ src_rows, const bf16* __restrict__ w, int H, float eps,
     bf16* __restrict__ xn, int write_h) {
   __shared__ float red[8];
+  pdl_trigger();
+  pdl_wait();
   const int i = blockIdx.x;
   const int r = src_rows ? src_rows[i] : i;
   float* hr = h + static_cast<size_t>(r) * H;
@@ -73,14 +76,16 @@ int resid_norm_launch(float* h, const float* part, int S, int Mp, const int* src
   RLB_CHECK(H <= 256 * NORM_MAX_PER_THREAD, RLB_ERR_ARG, "hidden size too large for RMSNorm");
   const int wh = write_h ? 1 : 0;
 #define RN_CASE(s) \
-  case s: resid_norm_kernel<s><<<R, 256, 0, st>>>(h, part, Mp, src_rows, w, H, eps, xn, wh); break;
+  case s:                                                                                        \
+    RLB_CUDA(launch_k(resid_norm_kernel<s>, dim3(R), dim3(256), 0, st, h, part, Mp, src_rows, w, H, \
+                      eps, xn, wh));                                                              \
+    break;
   switch (S) {
     RN_CASE(0) RN_CASE(1) RN_CASE(2) RN_CASE(3) RN_CASE(4) RN_CASE(5) RN_CASE(6) RN_CASE(7)
     RN_CASE(8)
     default: RLB_CHECK(false, RLB_ERR_ARG, "split-K factor must be <= 8");
   }
 #undef RN_CASE
-  RLB_CUDA(cudaGetLastError());
   return RLB_OK;
 }
 
@@ -93,6 +98,8 @@ __global__ void __launch_bounds__(256) qkv_rope_kernel(
     const int* __restrict__ row_slot, const int* __restrict__ row_pos,
     const float2* __restrict__ rope, int NQ, int NKV, int D, bf16* __restrict__ qout, int ldq,
     bf16* __restrict__ kv, const int* __restrict__ block_table, int bt_stride) {
+  pdl_trigger();
+  pdl_wait();
   const int r = blockIdx.x;
   const int half = D / 2;
   const int N = (NQ + 2 * NKV) * D;
@@ -146,15 +153,14 @@ int qkv_rope_launch(const float* part, int S, int Mp, const bf16* bias, const in
   if (R <= 0) return RLB_OK;
 #define QR_CASE(s)                                                                           \
   case s:                                                                                    \
-    qkv_rope_kernel<s><<<R, 256, 0, st>>>(part, Mp, bias, row_slot, row_pos, rope, NQ, NKV, D, \
-                                          qout, ldq, kv, block_table, bt_stride);            \
+    RLB_CUDA(launch_k(qkv_rope_kernel<s>, dim3(R), dim3(256), 0, st, part, Mp, bias, row_slot, \
+                      row_pos, rope, NQ, NKV, D, qout, ldq, kv, block_table, bt_stride));     \
     break;
   switch (S) {
     QR_CASE(1) QR_CASE(2) QR_CASE(3) QR_CASE(4) QR_CASE(5) QR_CASE(6) QR_CASE(7) QR_CASE(8)
     default: RLB_CHECK(false, RLB_ERR_ARG, "split-K factor must be 1..8");
   }
 #undef QR_CASE
-  RLB_CUDA(cudaGetLastError());
   return RLB_OK;
 }
 

@@ -24,6 +24,7 @@ continuation is bit-identical to an uninterrupted run.
 from __future__ import annotations
 
 import ctypes
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -52,6 +53,8 @@ class RolloutInstance:
         self.device = device
         self.max_slots = max_slots
         self.max_seq_len = max_seq_len
+        if os.environ.get("RLB_GRAPH_STEPS"):
+            graph_steps = int(os.environ["RLB_GRAPH_STEPS"])
         self._cfg = _lib.ModelCfg.from_shape(shape)
         ecfg = _lib.EngineCfg(max_slots, max_seq_len, num_pages, max_prefill_rows, graph_steps)
         h = ctypes.c_void_p()
