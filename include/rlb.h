@@ -120,6 +120,9 @@ int rlb_relayout_copy_range(int device, const rlb_model_cfg* model, const void* 
  * fan-out copies engine-layout slices between rollout GPUs. */
 int rlb_copy_bytes(int device, void* dst, const void* src, int64_t nbytes, void* stream);
 
+/* Let `device` read `peer`'s memory directly (single-process multi-GPU pulls). */
+int rlb_enable_peer(int device, int peer);
+
 /* ---- CUDA IPC (pull sessions between processes) ------------------------ */
 /* Handle of the allocation containing dev_ptr, plus dev_ptr's byte offset in it. */
 int rlb_ipc_handle(const void* dev_ptr, uint8_t out_handle[64], int64_t* out_offset);
@@ -178,6 +181,10 @@ int rlb_score(rlb_instance* h, const int32_t* tokens, int32_t n, float* out_logi
  * All device pointers. */
 int rlb_gemm(int device, int32_t M, int32_t N, int32_t K, const void* A, const void* B,
              const void* bias, void* C, int32_t epilogue, int32_t block_n, int32_t splits);
+/* Average time of `iters` back-to-back launches of one GEMM configuration on
+ * scratch buffers (tile / split-K tuning; epilogue 4 = argmax partials). */
+int rlb_bench_gemm(int device, int32_t M, int32_t N, int32_t K, int32_t epilogue, int32_t block_n,
+                   int32_t splits, int32_t iters, double* avg_ms);
 
 #ifdef __cplusplus
 }

@@ -88,6 +88,7 @@ _SIGS = {
     "rlb_copy_bytes": (ctypes.c_int, [ctypes.c_int, _P, _P, ctypes.c_int64, _P]),
     "rlb_relayout_copy_range": (ctypes.c_int, [ctypes.c_int, ctypes.POINTER(ModelCfg), _P,
                                                ctypes.c_int32, _P, ctypes.c_int64, ctypes.c_int64, _P]),
+    "rlb_enable_peer": (ctypes.c_int, [ctypes.c_int, ctypes.c_int]),
     "rlb_ipc_handle": (ctypes.c_int, [_P, _P, ctypes.POINTER(ctypes.c_int64)]),
     "rlb_ipc_open": (ctypes.c_int, [ctypes.c_int, _P, ctypes.POINTER(_P)]),
     "rlb_ipc_close": (ctypes.c_int, [ctypes.c_int, _P]),
@@ -101,6 +102,8 @@ _SIGS = {
     "rlb_status": (ctypes.c_int, [_P, ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_int32),
                                   ctypes.POINTER(ctypes.c_uint64)]),
     "rlb_score": (ctypes.c_int, [_P, _P, ctypes.c_int32, _P]),
+    "rlb_bench_gemm": (ctypes.c_int, [ctypes.c_int] + [ctypes.c_int32] * 7 +
+                       [ctypes.POINTER(ctypes.c_double)]),
     "rlb_gemm": (ctypes.c_int, [ctypes.c_int, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, _P, _P,
                                 _P, _P, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32]),
 }

@@ -24,6 +24,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <deque>
@@ -220,6 +221,18 @@ int rlb_instance::init() {
   sp_qkv = pick_splits(QKV, H, BN_QKV);
   sp_o = pick_splits(H, NQ * D, BN_O);
   sp_down = pick_splits(H, F, BN_DOWN);
+  if (const char* ov = std::getenv("RLB_SPLITS")) {   // "qkv,o,down" (tuning; process-wide)
+    int a = 0, b = 0, c = 0;
+    if (std::sscanf(ov, "%d,%d,%d", &a, &b, &c) == 3) {
+      const int kq = H / 64, ko = NQ * D / 64, kd = F / 64;
+      RLB_CHECK(a >= 1 && a <= 8 && kq % a == 0 && b >= 1 && b <= 8 && ko % b == 0 && c >= 1 &&
+                    c <= 8 && kd % c == 0,
+                RLB_ERR_ARG, "RLB_SPLITS must divide the K blocks (<= 8)");
+      sp_qkv = a;
+      sp_o = b;
+      sp_down = c;
+    }
+  }
 
   RLB_CUDA(cudaSetDevice(device));
   RLB_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));

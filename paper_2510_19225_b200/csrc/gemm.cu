@@ -27,6 +27,9 @@
 #define RLB_PDL_CLASS 1
 #include "internal.h"
 
+#include <cstdio>
+#include <cstdlib>
+
 namespace rlb {
 
 constexpr int BM = 256;      // rows per CTA (two UMMA_M=128 accumulators)
@@ -44,7 +47,7 @@ struct GemmCfg {
   static constexpr uint32_t TMEM_COLS = 2 * BN;
 };
 
-__device__ __forceinline__ float silu_f(float g) { return g / (1.0f + expf(-g)); }
+__device__ __forceinline__ float silu_f(float g) { return __fdividef(g, 1.0f + __expf(-g)); }
 
 // Generic split-K reduce (kernel-level test entry rlb_gemm only; the engine
 // fuses the reduction into its row-wise consumer kernels): sum the fp32
@@ -107,6 +110,13 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   const int lane = threadIdx.x & 31;
   const int n_blk = blockIdx.x;
   const int m_blk = blockIdx.y;
+  const bool stamp = p.dbg != nullptr && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0;
+  auto gtime = []() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+  };
+  if (stamp && threadIdx.x == 0) p.dbg[0] = gtime();
   const int nk_total = p.K / BK;
   const int nk = nk_total / p.splits;          // k-blocks of this split
   const int kb0 = blockIdx.z * nk;
@@ -126,8 +136,10 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  if (stamp && threadIdx.x == 0) p.dbg[1] = gtime();
   pdl_trigger();
   pdl_wait();   // A (activations) is the previous kernel's output
+  if (stamp && threadIdx.x == 0) p.dbg[2] = gtime();
 
   if (warp == 0) {
     if (lane == 0) {
@@ -164,6 +176,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         umma_commit(smem_u32(&empty[s]));
       }
       umma_commit(smem_u32(tfull));
+      if (stamp) p.dbg[3] = gtime();
     }
   } else if (warp >= 4) {
     const int half = (warp - 4) >> 2;          // accumulator 0 or 1
@@ -171,6 +184,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     const int m = m_blk * BM + half * HM + q * 32 + lane;
     const bool live = m < p.M;
     mbar_wait(smem_u32(tfull), 0);
+    if (stamp && threadIdx.x == 128) p.dbg[4] = gtime();
     tc_fence_after();
     const uint32_t tbase = tmem + half * BN + (static_cast<uint32_t>(q * 32) << 16);
     if constexpr (EPI == EPI_SWIGLU) {
@@ -178,24 +192,24 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
 #pragma unroll 1
       for (int g = 0; g < BN / 128; ++g) {
 #pragma unroll 1
-        for (int jc = 0; jc < 64; jc += 16) {
-          uint32_t rg[16], ru[16];
-          tmem_ld16(tbase + g * 128 + jc, rg);
-          tmem_ld16(tbase + g * 128 + 64 + jc, ru);
+        for (int jc = 0; jc < 64; jc += 32) {
+          uint32_t rg[32], ru[32];
+          tmem_ld32(tbase + g * 128 + jc, rg);
+          tmem_ld32(tbase + g * 128 + 64 + jc, ru);
           tmem_ld_wait();
           const int col = n_blk * (BN / 2) + g * 64 + jc;
           if (live && col < p.N / 2) {
-            uint32_t pk[8];
+            uint32_t pk[16];
 #pragma unroll
-            for (int i = 0; i < 8; ++i) {
+            for (int i = 0; i < 16; ++i) {
               const float a0 = silu_f(__uint_as_float(rg[2 * i])) * __uint_as_float(ru[2 * i]);
               const float a1 =
                   silu_f(__uint_as_float(rg[2 * i + 1])) * __uint_as_float(ru[2 * i + 1]);
               pk[i] = pack_bf2(a0, a1);
             }
             uint4* dst = reinterpret_cast<uint4*>(out + static_cast<size_t>(m) * p.ldo + col);
-            dst[0] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
-            dst[1] = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) dst[i] = make_uint4(pk[4 * i], pk[4 * i + 1], pk[4 * i + 2], pk[4 * i + 3]);
           }
         }
       }
@@ -205,13 +219,13 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       float best = -INFINITY;
       int bidx = 0x7fffffff;
 #pragma unroll 1
-      for (int c = 0; c < BN; c += 16) {
-        uint32_t r[16];
-        tmem_ld16(tbase + c, r);
+      for (int c = 0; c < BN; c += 32) {
+        uint32_t r[32];
+        tmem_ld32(tbase + c, r);
         tmem_ld_wait();
         const int n = n_blk * BN + c;
 #pragma unroll
-        for (int i = 0; i < 16; ++i) {
+        for (int i = 0; i < 32; ++i) {
           const float v = __uint_as_float(r[i]);
           if (n + i < p.N && v > best) {
             best = v;
@@ -223,57 +237,78 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         float2* part = reinterpret_cast<float2*>(p.out) + static_cast<size_t>(m) * p.ldo + n_blk;
         *part = make_float2(best, __int_as_float(bidx));
       }
-    } else if constexpr (EPI == EPI_PARTIAL) {
-      // split-K: store this K range's fp32 partial [z][M][N]; the row-wise
-      // consumer kernel sums the splits in order and applies the epilogue.
-      float* part = p.ws + static_cast<size_t>(blockIdx.z) * p.M * p.N;
+    } else if constexpr ((EPI == EPI_PARTIAL || EPI == EPI_F32) && BN == 128) {
+      // fp32 tile out through shared memory so every global store is a full
+      // 512-byte row (a thread-per-row store would issue 32 scattered 16-byte
+      // requests per instruction).  The pipeline stages are free: the MMA
+      // that consumed them has completed.  EPI_PARTIAL = this K range's fp32
+      // partial [z][M][N], reduced in split order by the row-wise consumer.
+      constexpr int LDS = BN + 4;                          // padded row (bank spread)
+      float* stage = reinterpret_cast<float*>(smem);
+      const int row = half * HM + q * 32 + lane;           // row within the CTA tile
 #pragma unroll 1
-      for (int c = 0; c < BN; c += 16) {
-        uint32_t r[16];
-        tmem_ld16(tbase + c, r);
+      for (int c = 0; c < BN; c += 32) {
+        uint32_t r[32];
+        tmem_ld32(tbase + c, r);
         tmem_ld_wait();
-        const int n = n_blk * BN + c;
-        if (!live || n >= p.N) continue;
-        float4* o = reinterpret_cast<float4*>(part + static_cast<size_t>(m) * p.N + n);
+        float4* s4 = reinterpret_cast<float4*>(stage + row * LDS + c);
 #pragma unroll
-        for (int i = 0; i < 4; ++i)
-          o[i] = make_float4(__uint_as_float(r[4 * i]), __uint_as_float(r[4 * i + 1]),
-                             __uint_as_float(r[4 * i + 2]), __uint_as_float(r[4 * i + 3]));
+        for (int i = 0; i < 8; ++i)
+          s4[i] = make_float4(__uint_as_float(r[4 * i]), __uint_as_float(r[4 * i + 1]),
+                              __uint_as_float(r[4 * i + 2]), __uint_as_float(r[4 * i + 3]));
+      }
+      asm volatile("bar.sync 1, 256;" ::: "memory");
+      float* base = EPI == EPI_PARTIAL ? p.ws + static_cast<size_t>(blockIdx.z) * p.M * p.N
+                                       : reinterpret_cast<float*>(p.out);
+      const int ld = EPI == EPI_PARTIAL ? p.N : p.ldo;
+      const int ew = warp - 4;                              // 8 epilogue warps
+      const int n = n_blk * BN + lane * 4;
+#pragma unroll 4
+      for (int rr = ew; rr < BM; rr += 8) {
+        const int mm = m_blk * BM + rr;
+        if (mm >= p.M || n >= p.N) continue;
+        *reinterpret_cast<float4*>(base + static_cast<size_t>(mm) * ld + n) =
+            *reinterpret_cast<const float4*>(stage + rr * LDS + lane * 4);
       }
     } else {
+      // EPI_F32 / EPI_PARTIAL with BN=256, EPI_BF16(+bias), EPI_RESADD.
+      float* f32 = EPI == EPI_PARTIAL ? p.ws + static_cast<size_t>(blockIdx.z) * p.M * p.N
+                                      : reinterpret_cast<float*>(p.out);
+      const int ld = EPI == EPI_PARTIAL ? p.N : p.ldo;
 #pragma unroll 1
-      for (int c = 0; c < BN; c += 16) {
-        uint32_t r[16];
-        tmem_ld16(tbase + c, r);
+      for (int c = 0; c < BN; c += 32) {
+        uint32_t r[32];
+        tmem_ld32(tbase + c, r);
         tmem_ld_wait();
         const int n = n_blk * BN + c;
         if (!live || n >= p.N) continue;
         if constexpr (EPI == EPI_BF16) {
           bf16* out = reinterpret_cast<bf16*>(p.out);
-          float v[16];
+          float v[32];
 #pragma unroll
-          for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+          for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
           if (p.bias != nullptr) {
-            const uint4* bp = reinterpret_cast<const uint4*>(p.bias + n);
-            const uint4 b0 = bp[0], b1 = bp[1];
-            const uint32_t bb[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
 #pragma unroll
-            for (int i = 0; i < 8; ++i) {
-              v[2 * i] += bf_lo(bb[i]);
-              v[2 * i + 1] += bf_hi(bb[i]);
+            for (int h = 0; h < 4; ++h) {
+              const uint4 b = reinterpret_cast<const uint4*>(p.bias + n)[h];
+              const uint32_t bb[4] = {b.x, b.y, b.z, b.w};
+#pragma unroll
+              for (int i = 0; i < 4; ++i) {
+                v[8 * h + 2 * i] += bf_lo(bb[i]);
+                v[8 * h + 2 * i + 1] += bf_hi(bb[i]);
+              }
             }
           }
-          uint32_t pk[8];
+          uint32_t pk[16];
 #pragma unroll
-          for (int i = 0; i < 8; ++i) pk[i] = pack_bf2(v[2 * i], v[2 * i + 1]);
+          for (int i = 0; i < 16; ++i) pk[i] = pack_bf2(v[2 * i], v[2 * i + 1]);
           uint4* dst = reinterpret_cast<uint4*>(out + static_cast<size_t>(m) * p.ldo + n);
-          dst[0] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
-          dst[1] = make_uint4(pk[4], pk[5], pk[6], pk[7]);
-        } else if constexpr (EPI == EPI_RESADD) {
-          float4* h = reinterpret_cast<float4*>(reinterpret_cast<float*>(p.out) +
-                                                static_cast<size_t>(m) * p.ldo + n);
 #pragma unroll
-          for (int i = 0; i < 4; ++i) {
+          for (int i = 0; i < 4; ++i) dst[i] = make_uint4(pk[4 * i], pk[4 * i + 1], pk[4 * i + 2], pk[4 * i + 3]);
+        } else if constexpr (EPI == EPI_RESADD) {
+          float4* h = reinterpret_cast<float4*>(f32 + static_cast<size_t>(m) * ld + n);
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
             float4 x = h[i];
             x.x += __uint_as_float(r[4 * i]);
             x.y += __uint_as_float(r[4 * i + 1]);
@@ -281,22 +316,23 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
             x.w += __uint_as_float(r[4 * i + 3]);
             h[i] = x;
           }
-        } else {  // EPI_F32
-          float* base = reinterpret_cast<float*>(p.out);
-          float4* o = reinterpret_cast<float4*>(base + static_cast<size_t>(m) * p.ldo + n);
+        } else {  // EPI_F32, EPI_PARTIAL
+          float4* o = reinterpret_cast<float4*>(f32 + static_cast<size_t>(m) * ld + n);
 #pragma unroll
-          for (int i = 0; i < 4; ++i)
+          for (int i = 0; i < 8; ++i)
             o[i] = make_float4(__uint_as_float(r[4 * i]), __uint_as_float(r[4 * i + 1]),
                                __uint_as_float(r[4 * i + 2]), __uint_as_float(r[4 * i + 3]));
         }
       }
     }
   }
+  if (stamp && threadIdx.x == 128) p.dbg[6] = gtime();
   tc_fence_before();
   __syncthreads();
   if (warp == 2) {
     tc_fence_after();
     tmem_dealloc(tmem, C::TMEM_COLS);
+    if (stamp && lane == 0) p.dbg[5] = gtime();
   }
 }
 
@@ -407,6 +443,61 @@ int gemm_launch(const CUtensorMap& a, const CUtensorMap& b, int block_n, int epi
 }
 
 }  // namespace rlb
+
+// Microbenchmark: `iters` back-to-back launches of one GEMM configuration on
+// scratch buffers, timed with CUDA events (tile / split tuning).
+extern "C" int rlb_bench_gemm(int device, int32_t M, int32_t N, int32_t K, int32_t epilogue,
+                              int32_t block_n, int32_t splits, int32_t iters, double* avg_ms) {
+  using namespace rlb;
+  RLB_CUDA(cudaSetDevice(device));
+  int rc = gemm_prepare();
+  if (rc) return rc;
+  bf16 *A = nullptr, *B = nullptr;
+  float* C = nullptr;
+  const int S = splits < 1 ? 1 : splits;
+  RLB_CUDA(cudaMalloc(&A, sizeof(bf16) * static_cast<size_t>(M) * K));
+  RLB_CUDA(cudaMalloc(&B, sizeof(bf16) * static_cast<size_t>(N) * K));
+  RLB_CUDA(cudaMalloc(&C, sizeof(float) * static_cast<size_t>(S) * M * N));
+  RLB_CUDA(cudaMemset(A, 0, sizeof(bf16) * static_cast<size_t>(M) * K));
+  RLB_CUDA(cudaMemset(B, 0, sizeof(bf16) * static_cast<size_t>(N) * K));
+  CUtensorMap ma, mb;
+  if ((rc = make_kmajor_map(&ma, A, M, K, HM)) || (rc = make_kmajor_map(&mb, B, N, K, block_n)))
+    return rc;
+  GemmParams p{M, N, K, nullptr, C, epilogue == EPI_SWIGLU ? N / 2 : N, S, C};
+  if (epilogue == EPI_ARGMAX) p.ldo = (N + block_n - 1) / block_n;
+  const int epi = S > 1 ? static_cast<int>(EPI_PARTIAL) : epilogue;
+  cudaEvent_t e0, e1;
+  RLB_CUDA(cudaEventCreate(&e0));
+  RLB_CUDA(cudaEventCreate(&e1));
+  if ((rc = gemm_launch(ma, mb, block_n, epi, p, 0))) return rc;
+  RLB_CUDA(cudaEventRecord(e0, 0));
+  for (int i = 0; i < iters && !rc; ++i) rc = gemm_launch(ma, mb, block_n, epi, p, 0);
+  RLB_CUDA(cudaEventRecord(e1, 0));
+  RLB_CUDA(cudaEventSynchronize(e1));
+  float ms = 0.f;
+  RLB_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+  *avg_ms = ms / iters;
+  if (std::getenv("RLB_GEMM_DBG")) {   // latency breakdown of CTA 0 of one more launch
+    unsigned long long* d = nullptr;
+    unsigned long long h[8] = {0};
+    RLB_CUDA(cudaMalloc(&d, sizeof(h)));
+    RLB_CUDA(cudaMemset(d, 0, sizeof(h)));
+    p.dbg = d;
+    rc = gemm_launch(ma, mb, block_n, epi, p, 0);
+    RLB_CUDA(cudaMemcpy(h, d, sizeof(h), cudaMemcpyDeviceToHost));
+    std::fprintf(stderr, "gemm dbg (ns from CTA start): setup %lld wait %lld mma_done %lld "
+                 "epi_start %lld epi_end %lld dealloc %lld\n",
+                 (long long)(h[1] - h[0]), (long long)(h[2] - h[0]), (long long)(h[3] - h[0]),
+                 (long long)(h[4] - h[0]), (long long)(h[6] - h[0]), (long long)(h[5] - h[0]));
+    cudaFree(d);
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaFree(A);
+  cudaFree(B);
+  cudaFree(C);
+  return rc;
+}
 
 extern "C" int rlb_gemm(int device, int32_t M, int32_t N, int32_t K, const void* A, const void* B,
                         const void* bias, void* Cout, int32_t epilogue, int32_t block_n,

@@ -19,6 +19,7 @@ struct GemmParams {
   int ldo;
   int splits;     // split-K factor (1 = no split)
   float* ws;      // EPI_PARTIAL: fp32 partials [splits][M][N]
+  unsigned long long* dbg;  // optional: globaltimer stamps of CTA 0 (latency breakdown)
 };
 
 int make_kmajor_map(CUtensorMap* map, const void* ptr, int64_t rows, int64_t k, int box_rows);

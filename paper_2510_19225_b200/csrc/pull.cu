@@ -221,6 +221,17 @@ int rlb_relayout_copy(int device, const rlb_model_cfg* m, const void* const* hf_
   return rlb::relayout_copy(*m, hf_ptrs, n_tensors, dst_arena, static_cast<cudaStream_t>(stream));
 }
 
+int rlb_enable_peer(int device, int peer) {
+  RLB_CUDA(cudaSetDevice(device));
+  const cudaError_t e = cudaDeviceEnablePeerAccess(peer, 0);
+  if (e == cudaErrorPeerAccessAlreadyEnabled) {
+    cudaGetLastError();
+    return RLB_OK;
+  }
+  RLB_CUDA(e);
+  return RLB_OK;
+}
+
 int rlb_relayout_copy_range(int device, const rlb_model_cfg* m, const void* const* hf_ptrs,
                             int32_t n_tensors, void* dst_arena, int64_t lo, int64_t hi,
                             void* stream) {
