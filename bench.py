@@ -41,6 +41,7 @@ NEW_TOKENS = 1024
 P_LO, P_HI = 128, 384
 MAX_SEQ = 1408            # P_HI + NEW_TOKENS
 CPU_SAMPLE = (4, 32)      # prompts x new tokens for the CPU oracle sample
+NCU_ATTN_FILE = "profiles/r1_attn_ncu.json"   # ncu --set full capture of K1 (traffic)
 
 
 def parse():
@@ -53,6 +54,7 @@ def parse():
     ap.add_argument("--new-tokens", type=int, default=NEW_TOKENS)
     ap.add_argument("--flush-steps", type=int, default=64, help="decode steps per rlb_step call")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--prefill-rows", type=int, default=16384, help="token rows per prefill chunk")
     return ap.parse_args()
 
 
@@ -173,12 +175,13 @@ def main():
     ws, rank, local = dist_env()
     torch.cuda.set_device(local)
     if ws > 1:
+        os.environ.setdefault("NCCL_DEBUG", "ERROR")   # keep stdout to the one JSON line
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     shape = QWEN25_1_5B
     n_prompts, new = args.prompts, args.new_tokens
     w = synth_hf_weights(shape, seed=0, device=f"cuda:{local}")
     inst = RolloutInstance(shape, local, max_slots=n_prompts, max_seq_len=MAX_SEQ,
-                           max_prefill_rows=16384, graph_steps=16)
+                           max_prefill_rows=args.prefill_rows, graph_steps=16)
     pull = inst.load_weights(w, version=1)
     prompts = synth_prompts(n_prompts, shape.vocab, P_LO, P_HI, seed=1000 + rank)
     h2d_prompt_bytes = 4 * sum(len(p) for p in prompts)
@@ -244,6 +247,12 @@ def main():
         except OSError:
             pass
         hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
+        ncu_ratio = None
+        try:
+            nc = _j.load(open(os.path.join(ROOT, NCU_ATTN_FILE)))
+            ncu_ratio = nc["dram_bytes"] / nc["algorithmic_bytes"]
+        except (OSError, KeyError, ValueError):
+            pass
         att_ms, att_bytes = prof["attention"]
         achieved = att_bytes / (att_ms / 1e3) / 1e9
         kern = {k: {"avg_ms": round(v[0], 4), "work": v[1],
@@ -264,12 +273,18 @@ def main():
             "e2e": {"value": total_tokens / wall_max, "unit": "tokens/s",
                     "h2d_bytes_per_step": int(h2d_step), "d2h_bytes_per_step": int(d2h_step)},
             "gpu_launches": launches,
-            "roofline": {"bound": "hbm", "kernel": "attn_split_kernel (K1, split-K paged decode attention)",
+            "roofline": {"bound": "hbm", "kernel": "attn_mma_kernel<128> (K1, paged GQA decode attention)",
                          "achieved": round(achieved, 1), "peak": hbm_peak, "unit": "GB/s",
-                         "frac": round(achieved / hbm_peak, 4), "traffic": None,
+                         "frac": round(achieved / hbm_peak, 4),
+                         "traffic": (round(att_bytes * ncu_ratio) if ncu_ratio else None),
+                         "traffic_source": (f"ncu --set full DRAM read+write / algorithmic bytes = "
+                                            f"{ncu_ratio:.3f} on the captured launch ({NCU_ATTN_FILE}), "
+                                            "scaled to this launch" if ncu_ratio else None),
                          "bytes_per_launch": att_bytes, "avg_launch_ms": att_ms,
                          "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback"},
             "kernels_mid_rollout": kern,
+            "phases_ms_rank0": {"prefill": round(st["prefill_ms"], 1), "decode": round(st["decode_ms"], 1),
+                                "prefill_rows": st["prefill_rows"], "decode_steps": st["decode_steps"]},
             "weight_load_local": {"bytes": pull.bytes, "seconds": pull.seconds, "GB/s": round(pull.gbps, 1)},
             "clocks": clocks.summary(),
         }
