@@ -14,7 +14,7 @@ build/%.o: $(SRC_DIR)/%.cu $(SRC_DIR)/*.cuh $(SRC_DIR)/*.h include/rlb.h
 	$(NVCC) $(NVFLAGS) -c $< -o $@
 
 $(LIB): $(OBJS)
-	$(NVCC) $(ARCH) -shared -o $@ $(OBJS) -lcudart
+	$(NVCC) $(ARCH) -shared -o $@ $(OBJS) -lcudart -ldl
 
 clean:
 	rm -rf build $(LIB)

@@ -30,7 +30,7 @@ NVLINK_GBS = 900.0
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--mode", choices=["fanout", "direct", "both"], default="both")
+    ap.add_argument("--mode", choices=["fanout", "direct", "nccl", "all"], default="all")
     ap.add_argument("--shape", default="qwen2.5-7b")
     ap.add_argument("--rounds", type=int, default=8)
     ap.add_argument("--repeats", type=int, default=3)
@@ -40,7 +40,8 @@ def main():
     import torch.distributed as dist
     from paper_2510_19225_b200 import _lib
     from paper_2510_19225_b200.instance import RolloutInstance
-    from paper_2510_19225_b200.pull import FanoutReceiver, MappedSource, TrainerWeights, map_arena
+    from paper_2510_19225_b200.pull import (FanoutReceiver, MappedSource, NcclFanout,
+                                           TrainerWeights, map_arena)
     from paper_2510_19225_b200.shapes import SHAPES
     from paper_2510_19225_b200.synth import synth_hf_weights
 
@@ -99,12 +100,35 @@ def main():
 
     results = {}
     version_ctr = [0]
-    modes = ["fanout", "direct"] if args.mode == "both" else [args.mode]
+    modes = ["fanout", "nccl", "direct"] if args.mode == "all" else [args.mode]
+    ncf = None
+    stage_s = None
+    if ws > 1:
+        def share_id(uid):
+            box = [uid]
+            dist.broadcast_object_list(box, src=0)
+            return box[0]
+        ncf = NcclFanout(local, ws, rank, share_id)
+        if rank == 0:
+            stage_s = ncf.stage(trainer)
     for mode in modes:
         times = []
         for rep in range(args.repeats + 1):     # first repetition warms up
             dt = 0.0
-            if is_recv and mode == "fanout":
+            if mode == "nccl" and ws > 1:
+                # trainer staged the engine layout once; one NCCL broadcast lands
+                # it in every receiver's arena
+                barrier()
+                torch.cuda.synchronize()
+                t0 = time.perf_counter()
+                if is_recv:
+                    version_ctr[0] += 1
+                    ncf.broadcast(inst, version_ctr[0])
+                else:
+                    ncf.broadcast(None)
+                dt = time.perf_counter() - t0 if is_recv else 0.0
+                barrier()
+            elif is_recv and mode == "fanout":
                 version_ctr[0] += 1
                 dt = fan.pull(src_ptrs, version=version_ctr[0])
             elif is_recv:
@@ -114,7 +138,7 @@ def main():
                 inst.load_weights(src_ptrs, version=version_ctr[0])
                 dt = time.perf_counter() - t0
                 barrier()
-            else:   # the trainer only serves memory; match the receivers' barriers
+            elif mode != "nccl":   # the trainer only serves memory; match the receivers' barriers
                 for _ in range(3 if mode == "fanout" else 2):
                     barrier()
             t = torch.tensor([dt], dtype=torch.float64)
@@ -153,7 +177,8 @@ def main():
                           f"trainer GPU -> {len(receivers)} rollout GPU(s)",
                           "n_gpus": ws, "receivers": len(receivers),
                           "link": "NVLink5/NVSwitch" if ws > 1 else "local HBM (single GPU)",
-                          "bytewise_equal": bool(ok[0]), "modes": results}), flush=True)
+                          "bytewise_equal": bool(ok[0]), "modes": results,
+                          "nccl_stage_seconds": stage_s}), flush=True)
     if fan:
         fan.close()
     if src:

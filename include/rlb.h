@@ -116,10 +116,21 @@ int rlb_relayout_copy(int device, const rlb_model_cfg* model, const void* const*
 int rlb_relayout_copy_range(int device, const rlb_model_cfg* model, const void* const* hf_ptrs,
                             int32_t n_tensors, void* dst_arena, int64_t lo, int64_t hi,
                             void* stream);
+/* A list of byte-range copies (src[i] -> dst[i], nbytes[i]) as one chunked
+ * copy kernel: the re-layout of one received piece of a broadcast blob. */
+int rlb_copy_segments(int device, int32_t n, const void* const* src, void* const* dst,
+                      const int64_t* nbytes, void* stream);
 /* Plain chunked device copy (peer or local): the all-gather phase of the
  * fan-out copies engine-layout slices between rollout GPUs. */
 int rlb_copy_bytes(int device, void* dst, const void* src, int64_t nbytes, void* stream);
 
+/* NCCL broadcast fan-out of a staged engine-layout weight set (1->N pulls at
+ * once): unique id (out: 128 bytes), per-rank communicator on `device`, in-place
+ * byte broadcast from `root` on `stream`.  libnccl.so.2 is resolved at runtime. */
+int rlb_nccl_unique_id(uint8_t out[128]);
+int rlb_nccl_init(int device, int nranks, int rank, const uint8_t id[128], void** comm);
+int rlb_nccl_broadcast(void* comm, void* buf, int64_t nbytes, int root, void* stream);
+int rlb_nccl_destroy(void* comm);
 /* Let `device` read `peer`'s memory directly (single-process multi-GPU pulls). */
 int rlb_enable_peer(int device, int peer);
 

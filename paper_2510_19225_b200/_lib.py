@@ -86,9 +86,15 @@ _SIGS = {
     "rlb_relayout_copy": (ctypes.c_int, [ctypes.c_int, ctypes.POINTER(ModelCfg), _P,
                                          ctypes.c_int32, _P, _P]),
     "rlb_copy_bytes": (ctypes.c_int, [ctypes.c_int, _P, _P, ctypes.c_int64, _P]),
+    "rlb_copy_segments": (ctypes.c_int, [ctypes.c_int, ctypes.c_int32, _P, _P, _P, _P]),
     "rlb_relayout_copy_range": (ctypes.c_int, [ctypes.c_int, ctypes.POINTER(ModelCfg), _P,
                                                ctypes.c_int32, _P, ctypes.c_int64, ctypes.c_int64, _P]),
     "rlb_enable_peer": (ctypes.c_int, [ctypes.c_int, ctypes.c_int]),
+    "rlb_nccl_unique_id": (ctypes.c_int, [_P]),
+    "rlb_nccl_init": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_int, _P,
+                                     ctypes.POINTER(_P)]),
+    "rlb_nccl_broadcast": (ctypes.c_int, [_P, _P, ctypes.c_int64, ctypes.c_int, _P]),
+    "rlb_nccl_destroy": (ctypes.c_int, [_P]),
     "rlb_ipc_handle": (ctypes.c_int, [_P, _P, ctypes.POINTER(ctypes.c_int64)]),
     "rlb_ipc_open": (ctypes.c_int, [ctypes.c_int, _P, ctypes.POINTER(_P)]),
     "rlb_ipc_close": (ctypes.c_int, [ctypes.c_int, _P]),

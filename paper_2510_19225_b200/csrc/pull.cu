@@ -12,7 +12,11 @@
 // 16-byte vector loads, 4 in flight per thread, L1 no-allocate.
 #include "internal.h"
 
+#include <dlfcn.h>
+#include <nccl.h>
+
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 
 namespace rlb {
@@ -134,7 +138,9 @@ static int run_chunks(const std::vector<CopyChunk>& chunks, cudaStream_t st) {
   int sms = 148, dev = 0;
   RLB_CUDA(cudaGetDevice(&dev));
   RLB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-  const int grid = static_cast<int>(std::min<size_t>(chunks.size(), static_cast<size_t>(sms) * 4));
+  int cap = sms * 4;
+  if (const char* c = std::getenv("RLB_COPY_CTAS")) cap = std::max(1, std::atoi(c));
+  const int grid = static_cast<int>(std::min<size_t>(chunks.size(), static_cast<size_t>(cap)));
   chunk_copy_kernel<<<grid, COPY_THREADS, 0, st>>>(d, static_cast<int>(chunks.size()));
   RLB_CUDA(cudaGetLastError());
   RLB_CUDA(cudaFreeAsync(d, st));
@@ -221,6 +227,80 @@ int rlb_relayout_copy(int device, const rlb_model_cfg* m, const void* const* hf_
   return rlb::relayout_copy(*m, hf_ptrs, n_tensors, dst_arena, static_cast<cudaStream_t>(stream));
 }
 
+// ---- NCCL broadcast fan-out (libnccl resolved at runtime; no link dependency)
+namespace {
+struct NcclApi {
+  ncclResult_t (*unique_id)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*init_rank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*bcast)(const void*, void*, size_t, ncclDataType_t, int, ncclComm_t,
+                        cudaStream_t) = nullptr;
+  ncclResult_t (*destroy)(ncclComm_t) = nullptr;
+  const char* (*err)(ncclResult_t) = nullptr;
+  bool ok = false;
+};
+NcclApi* nccl_api() {
+  static NcclApi api;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (h) {
+      api.unique_id = reinterpret_cast<decltype(api.unique_id)>(dlsym(h, "ncclGetUniqueId"));
+      api.init_rank = reinterpret_cast<decltype(api.init_rank)>(dlsym(h, "ncclCommInitRank"));
+      api.bcast = reinterpret_cast<decltype(api.bcast)>(dlsym(h, "ncclBroadcast"));
+      api.destroy = reinterpret_cast<decltype(api.destroy)>(dlsym(h, "ncclCommDestroy"));
+      api.err = reinterpret_cast<decltype(api.err)>(dlsym(h, "ncclGetErrorString"));
+      api.ok = api.unique_id && api.init_rank && api.bcast && api.destroy && api.err;
+    }
+  }
+  return &api;
+}
+}  // namespace
+
+#define RLB_NCCL(call)                                                              \
+  do {                                                                              \
+    ncclResult_t _r = (call);                                                       \
+    if (_r != ncclSuccess) {                                                        \
+      rlb::set_error(std::string("NCCL: ") + nccl_api()->err(_r));                  \
+      return RLB_ERR_CUDA;                                                          \
+    }                                                                               \
+  } while (0)
+
+int rlb_nccl_unique_id(uint8_t out[128]) {
+  NcclApi* a = nccl_api();
+  RLB_CHECK(a->ok, RLB_ERR_CUDA, "libnccl.so.2 not available");
+  ncclUniqueId id;
+  RLB_NCCL(a->unique_id(&id));
+  memcpy(out, &id, sizeof(id) < 128 ? sizeof(id) : 128);
+  return RLB_OK;
+}
+
+int rlb_nccl_init(int device, int nranks, int rank, const uint8_t id[128], void** comm) {
+  NcclApi* a = nccl_api();
+  RLB_CHECK(a->ok, RLB_ERR_CUDA, "libnccl.so.2 not available");
+  RLB_CUDA(cudaSetDevice(device));
+  ncclUniqueId uid;
+  memcpy(&uid, id, sizeof(uid));
+  ncclComm_t c = nullptr;
+  RLB_NCCL(a->init_rank(&c, nranks, uid, rank));
+  *comm = c;
+  return RLB_OK;
+}
+
+int rlb_nccl_broadcast(void* comm, void* buf, int64_t nbytes, int root, void* stream) {
+  NcclApi* a = nccl_api();
+  RLB_CHECK(a->ok && comm, RLB_ERR_ARG, "no NCCL communicator");
+  RLB_NCCL(a->bcast(buf, buf, static_cast<size_t>(nbytes), ncclUint8, root,
+                    static_cast<ncclComm_t>(comm), static_cast<cudaStream_t>(stream)));
+  return RLB_OK;
+}
+
+int rlb_nccl_destroy(void* comm) {
+  NcclApi* a = nccl_api();
+  if (a->ok && comm) RLB_NCCL(a->destroy(static_cast<ncclComm_t>(comm)));
+  return RLB_OK;
+}
+
 int rlb_enable_peer(int device, int peer) {
   RLB_CUDA(cudaSetDevice(device));
   const cudaError_t e = cudaDeviceEnablePeerAccess(peer, 0);
@@ -239,6 +319,20 @@ int rlb_relayout_copy_range(int device, const rlb_model_cfg* m, const void* cons
   RLB_CUDA(cudaSetDevice(device));
   return rlb::relayout_copy_range(*m, hf_ptrs, n_tensors, dst_arena, lo, hi,
                                   static_cast<cudaStream_t>(stream));
+}
+
+int rlb_copy_segments(int device, int32_t n, const void* const* src, void* const* dst,
+                      const int64_t* nbytes, void* stream) {
+  RLB_CHECK(n >= 0 && (n == 0 || (src && dst && nbytes)), RLB_ERR_ARG, "bad segment list");
+  RLB_CUDA(cudaSetDevice(device));
+  std::vector<rlb::CopyChunk> chunks;
+  for (int32_t i = 0; i < n; ++i) {
+    RLB_CHECK(((reinterpret_cast<uintptr_t>(src[i]) | reinterpret_cast<uintptr_t>(dst[i])) & 15) == 0,
+              RLB_ERR_ARG, "segments must be 16-byte aligned");
+    rlb::split_into(&chunks, static_cast<const uint8_t*>(src[i]), static_cast<uint8_t*>(dst[i]),
+                    nbytes[i]);
+  }
+  return rlb::run_chunks(chunks, static_cast<cudaStream_t>(stream));
 }
 
 int rlb_copy_bytes(int device, void* dst, const void* src, int64_t nbytes, void* stream) {

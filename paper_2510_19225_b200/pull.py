@@ -28,7 +28,7 @@ import torch
 from . import _lib
 from ._lib import check
 from .protocol import cuda_ipc_endpoint, parse_cuda_ipc_endpoint
-from .shapes import ModelShape, hf_manifest
+from .shapes import ModelShape, hf_manifest, relayout_segments
 
 
 def _ipc_handle(ptr: int) -> tuple[bytes, int]:
@@ -38,6 +38,100 @@ def _ipc_handle(ptr: int) -> tuple[bytes, int]:
     return bytes(buf), off.value
 
 
+def blob_layout(shape: ModelShape) -> tuple[list[int], int]:
+    """Byte offset of every HF tensor in the trainer's contiguous weight blob
+    (256-byte aligned, `hf_manifest` order) and the blob size."""
+    offs, total = [], 0
+    for _, s in hf_manifest(shape):
+        offs.append(total)
+        n = 2
+        for d in s:
+            n *= d
+        total += (n + 255) // 256 * 256
+    return offs, total
+
+
+def relayout_by_source(shape: ModelShape, lo: int, hi: int) -> list[tuple[int, int, int]]:
+    """(blob_offset, arena_offset, nbytes) re-layout copies whose source bytes
+    lie in blob range [lo, hi): the piece of the fused re-layout that can run
+    once that range of the blob has arrived."""
+    offs, _ = blob_layout(shape)
+    out = []
+    for hf, so, do, nb in relayout_segments(shape):
+        a, b = offs[hf] + so, offs[hf] + so + nb
+        x, y = max(a, lo), min(b, hi)
+        if x < y:
+            out.append((x, do + (x - a), y - x))
+    return out
+
+
+def copy_segments(device: int, segs: list[tuple[int, int, int]], src_base: int, dst_base: int,
+                  stream) -> None:
+    n = len(segs)
+    if n == 0:
+        return
+    src = (ctypes.c_void_p * n)(*[src_base + s for s, _, _ in segs])
+    dst = (ctypes.c_void_p * n)(*[dst_base + d for _, d, _ in segs])
+    nb = (ctypes.c_int64 * n)(*[b for _, _, b in segs])
+    check(_lib.lib().rlb_copy_segments(device, n, src, dst, nb, stream))
+
+
+class NcclFanout:
+    """1->N pull when several instances pull the same version at once
+    (north_star: "NCCL broadcast when several instances pull at once").
+
+    The trainer stages the version once in engine layout (the fused re-layout
+    runs at staging time, the reference's agent staging step,
+    `pkg/src/spotrl/transfer.py:64-85`), then one NCCL broadcast (ring / NVLS
+    over NVSwitch) writes it straight into every receiver's engine arena: no
+    receiver-side copy, each receiver's NVLink ingress is the only bound."""
+
+    def __init__(self, device: int, nranks: int, rank: int, exchange_id):
+        self.device = device
+        uid = (ctypes.c_uint8 * 128)()
+        if rank == 0:
+            check(_lib.lib().rlb_nccl_unique_id(uid))
+        uid_bytes = exchange_id(bytes(uid))
+        uid = (ctypes.c_uint8 * 128).from_buffer_copy(uid_bytes)
+        comm = ctypes.c_void_p()
+        check(_lib.lib().rlb_nccl_init(device, nranks, rank, uid, ctypes.byref(comm)))
+        self.comm = comm
+        self.staged: torch.Tensor | None = None
+
+    def stage(self, trainer: "TrainerWeights") -> float:
+        """Trainer side: re-layout the HF weights into an engine-layout buffer."""
+        import time
+        cfg = _lib.ModelCfg.from_shape(trainer.shape)
+        nbytes = _lib.lib().rlb_arena_bytes(ctypes.byref(cfg))
+        if self.staged is None or self.staged.numel() != nbytes:
+            self.staged = torch.empty(nbytes, dtype=torch.uint8, device=f"cuda:{self.device}")
+        ptrs = trainer.ptrs
+        arr = (ctypes.c_void_p * len(ptrs))(*ptrs)
+        torch.cuda.synchronize(self.device)
+        t0 = time.perf_counter()
+        check(_lib.lib().rlb_relayout_copy(self.device, ctypes.byref(cfg), arr, len(ptrs),
+                                           self.staged.data_ptr(), None))
+        torch.cuda.synchronize(self.device)
+        return time.perf_counter() - t0
+
+    def broadcast(self, instance=None, version: int = 0, root: int = 0) -> None:
+        """Root: send the staged buffer; receivers: land it in `instance`'s arena."""
+        if instance is None:
+            ptr, nbytes = self.staged.data_ptr(), self.staged.numel()
+        else:
+            ptr, nbytes = instance.arena()
+        stream = torch.cuda.current_stream(self.device).cuda_stream
+        check(_lib.lib().rlb_nccl_broadcast(self.comm, ptr, nbytes, root, stream))
+        torch.cuda.current_stream(self.device).synchronize()
+        if instance is not None:
+            instance.mark_weights(version)
+
+    def close(self) -> None:
+        if self.comm:
+            _lib.lib().rlb_nccl_destroy(self.comm)
+            self.comm = None
+
+
 class TrainerWeights:
     """HF-layout bf16 weights of one trainer GPU, contiguous, IPC-exportable."""
 
@@ -45,13 +139,7 @@ class TrainerWeights:
         self.shape = shape
         self.device = device
         manifest = hf_manifest(shape)
-        offs, total = [], 0
-        for _, s in manifest:
-            offs.append(total)
-            n = 2
-            for d in s:
-                n *= d
-            total += (n + 255) // 256 * 256
+        offs, total = blob_layout(shape)
         self.blob = torch.empty(total, dtype=torch.uint8, device=f"cuda:{device}")
         self.views: dict[str, torch.Tensor] = {}
         self.nbytes: list[int] = []
