@@ -168,6 +168,7 @@ def main():
         return run_reference(args)
     import torch
     import torch.distributed as dist
+    from paper_2510_19225_b200 import multi
     from paper_2510_19225_b200.instance import RolloutInstance
     from paper_2510_19225_b200.shapes import QWEN25_1_5B
     from paper_2510_19225_b200.synth import synth_hf_weights, synth_prompts
@@ -225,19 +226,12 @@ def main():
     dev_s = (st["prefill_ms"] + st["decode_ms"]) / 1000.0
     _, prof = rollout("p", profile=True)
 
-    agg = torch.tensor([dev_s, wall, float(tokens), float(st["kernel_launches"]),
-                        float(st["h2d_bytes"] + h2d_prompt_bytes * args.steps), float(st["d2h_bytes"])],
-                       dtype=torch.float64, device="cuda")
-    if ws > 1:
-        mx = agg.clone()
-        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
-        sm = agg.clone()
-        dist.all_reduce(sm, op=dist.ReduceOp.SUM)
-    else:
-        mx = sm = agg
-    dev_max, wall_max = float(mx[0]), float(mx[1])
-    total_tokens, launches = float(sm[2]), int(sm[3])
-    h2d_step, d2h_step = float(agg[4]) / args.steps, float(agg[5]) / args.steps
+    agg = [dev_s, wall, float(tokens), float(st["kernel_launches"]),
+           float(st["h2d_bytes"] + h2d_prompt_bytes * args.steps), float(st["d2h_bytes"])]
+    mx, sm = multi.reduce_max_sum(agg, device="cuda")   # max over ranks (time), sums (work)
+    dev_max, wall_max = mx[0], mx[1]
+    total_tokens, launches = sm[2], int(sm[3])
+    h2d_step, d2h_step = agg[4] / args.steps, agg[5] / args.steps
 
     if rank == 0:
         import json as _j
