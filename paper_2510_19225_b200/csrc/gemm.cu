@@ -108,8 +108,11 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  const int n_blk = blockIdx.x;
-  const int m_blk = blockIdx.y;
+  // row tiles vary fastest: the CTAs sharing a weight (B) tile are dispatched
+  // together, so a weight tile is read from HBM once even when the whole
+  // weight matrix does not fit in L2 (lm_head: 467 MB)
+  const int m_blk = blockIdx.x;
+  const int n_blk = blockIdx.y;
   const bool stamp = p.dbg != nullptr && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0;
   auto gtime = []() {
     unsigned long long t;
@@ -404,7 +407,8 @@ template <int BN, int EPI>
 static int launch_one(const CUtensorMap& a, const CUtensorMap& b, const GemmParams& p,
                       cudaStream_t st) {
   using C = GemmCfg<BN>;
-  dim3 grid((p.N + BN - 1) / BN, (p.M + BM - 1) / BM, p.splits);
+  RLB_CHECK((p.N + BN - 1) / BN <= 65535, RLB_ERR_ARG, "too many N tiles");
+  dim3 grid((p.M + BM - 1) / BM, (p.N + BN - 1) / BN, p.splits);
   RLB_CUDA(launch_k(gemm_bf16_tc<BN, EPI>, grid, dim3(GEMM_THREADS), C::SMEM, st, a, b, p));
   return RLB_OK;
 }
