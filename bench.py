@@ -41,7 +41,8 @@ NEW_TOKENS = 1024
 P_LO, P_HI = 128, 384
 MAX_SEQ = 1408            # P_HI + NEW_TOKENS
 CPU_SAMPLE = (4, 32)      # prompts x new tokens for the CPU oracle sample
-NCU_ATTN_FILE = "profiles/r1_attn_ncu.json"   # ncu --set full capture of K1 (traffic)
+NCU_ATTN_FILE = "profiles/r1_attn_ncu.json"
+HBM_KERNELS = ("attention", "resid_norm", "qkv_rope")   # bytes-bound (others: FLOPs)   # ncu --set full capture of K1 (traffic)
 
 
 def parse():
@@ -196,7 +197,8 @@ def main():
             out = inst.step(args.flush_steps)
             got += sum(len(t) for _, t, _ in out)
             if profile and not prof and got >= n_prompts * (new // 2):
-                for k in ("attention", "gate_up", "down", "qkv", "o_proj", "lm_head"):
+                for k in ("attention", "gate_up", "down", "qkv", "o_proj", "lm_head",
+                          "resid_norm", "qkv_rope"):
                     prof[k] = inst.profile_kernel(k, iters=20)
             st = inst.status()
             if st["m_pending"] == 0 and st["m_exec"] == 0:
@@ -250,8 +252,8 @@ def main():
         att_ms, att_bytes = prof["attention"]
         achieved = att_bytes / (att_ms / 1e3) / 1e9
         kern = {k: {"avg_ms": round(v[0], 4), "work": v[1],
-                    ("GB/s" if k == "attention" else "TFLOP/s"):
-                        round(v[1] / (v[0] / 1e3) / (1e9 if k == "attention" else 1e12), 1)}
+                    ("GB/s" if k in HBM_KERNELS else "TFLOP/s"):
+                        round(v[1] / (v[0] / 1e3) / (1e9 if k in HBM_KERNELS else 1e12), 1)}
                 for k, v in prof.items()}
         line = {
             "metric": "rollout tokens/s", "value": total_tokens / dev_max, "unit": "tokens/s",

@@ -161,6 +161,9 @@ struct rlb_instance {
   }
   int proj(const CUtensorMap& a, const CUtensorMap& b, int bn, int splits, int epi, int R, int N,
            int K, const bf16* bias, void* out, int ldo);
+  // KV target of rlb_profile_kernel's qkv_rope timing (clobbers the last
+  // layer's entries of the current positions: only for a throw-away rollout)
+  bf16* kv_scratch() const { return kv + layer_stride * (m.layers - 1); }
 
   ~rlb_instance();
   int init();
@@ -909,6 +912,13 @@ int rlb_profile_kernel(rlb_instance* h, int32_t which, int32_t iters, double* av
                              nullptr, 0);
       case 5: return h->proj(h->m_xn, h->m_lm, BN_LM, 1, EPI_ARGMAX, R, h->V, H, nullptr,
                              h->d_logits, (h->V + BN_LM - 1) / BN_LM);
+      // row consumers, on the partial buffer as the last projection left it
+      // (timing only; writes go to scratch outputs)
+      case 6: return resid_norm_launch(h->d_h, h->d_part, h->sp_down, R, nullptr, R, w.ln2, H,
+                                       h->m.rms_eps, h->d_xn, false, h->st);
+      case 7: return qkv_rope_launch(h->d_part, h->sp_qkv, R, w.bqkv, h->d_row_slot,
+                                     h->d_row_pos, R, h->d_rope, NQ, h->NKV, D, h->d_q, NQ * D,
+                                     h->kv_scratch(), h->d_bt, h->pps, h->st);
     }
     set_error("unknown kernel id");
     return RLB_ERR_ARG;
@@ -927,6 +937,8 @@ int rlb_profile_kernel(rlb_instance* h, int32_t which, int32_t iters, double* av
     case 3: work = 2.0 * R * h->QKV * H; break;
     case 4: work = 2.0 * R * H * NQ * D; break;
     case 5: work = 2.0 * R * h->V * static_cast<double>(H); break;
+    case 6: work = R * (h->sp_down + 2.0) * H * 4.0 + R * H * 2.0; break;      // bytes
+    case 7: work = R * (h->sp_qkv * 4.0 + 2.0) * h->QKV; break;                 // bytes
     default: RLB_CHECK(false, RLB_ERR_ARG, "unknown kernel id");
   }
   int rc = launch();  // warm

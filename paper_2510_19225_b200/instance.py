@@ -223,7 +223,8 @@ class RolloutInstance:
         check(_lib.lib().rlb_score(self._h, ptr(t), len(t), ptr(out)))
         return out
 
-    KERNELS = {"attention": 0, "gate_up": 1, "down": 2, "qkv": 3, "o_proj": 4, "lm_head": 5}
+    KERNELS = {"attention": 0, "gate_up": 1, "down": 2, "qkv": 3, "o_proj": 4, "lm_head": 5,
+               "resid_norm": 6, "qkv_rope": 7}
 
     def stats(self, reset: bool = False) -> dict:
         """Cumulative device-time accounting (CUDA events on the instance stream)."""
