@@ -42,7 +42,7 @@ P_LO, P_HI = 128, 384
 MAX_SEQ = 1408            # P_HI + NEW_TOKENS
 CPU_SAMPLE = (4, 32)      # prompts x new tokens for the CPU oracle sample
 NCU_ATTN_FILE = "profiles/r1_attn_ncu.json"
-HBM_KERNELS = ("attention", "resid_norm", "qkv_rope")   # bytes-bound (others: FLOPs)   # ncu --set full capture of K1 (traffic)
+HBM_KERNELS = ("attention", "resid_norm")   # bytes-bound (others: FLOPs)   # ncu --set full capture of K1 (traffic)
 
 
 def parse():
@@ -198,7 +198,7 @@ def main():
             got += sum(len(t) for _, t, _ in out)
             if profile and not prof and got >= n_prompts * (new // 2):
                 for k in ("attention", "gate_up", "down", "qkv", "o_proj", "lm_head",
-                          "resid_norm", "qkv_rope"):
+                          "resid_norm"):
                     prof[k] = inst.profile_kernel(k, iters=20)
             st = inst.status()
             if st["m_pending"] == 0 and st["m_exec"] == 0:

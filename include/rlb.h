@@ -175,9 +175,13 @@ typedef struct {
 int rlb_get_stats(rlb_instance* h, rlb_stats* out, int32_t reset);
 /* Re-launch one kernel of the last decode step `iters` times on the instance
  * stream (rows, KV and weights as that step left them) and time it with CUDA
- * events.  which: 0 attention (layer 0), 1 gate_up GEMM, 2 down GEMM, 3 QKV
- * GEMM, 4 O GEMM, 5 lm_head GEMM.  Returns the average launch time and the
- * algorithmic bytes (attention) or FLOPs (GEMMs) of one launch. */
+ * events.  which: 0 attention (layer 0), 1 gate_up GEMM, 2 down GEMM (+ fused
+ * residual add), 3 QKV GEMM (+ fused RoPE / KV append), 4 O GEMM (+ residual
+ * add), 5 lm_head GEMM (+ argmax partials), 6 RMSNorm row kernel.  Timing
+ * only: it overwrites scratch and the last layer's KV entries of the current
+ * positions, so the rollout being profiled must be discarded.  Returns the
+ * average launch time and the algorithmic bytes (attention, norm) or FLOPs
+ * (GEMMs) of one launch. */
 int rlb_profile_kernel(rlb_instance* h, int32_t which, int32_t iters, double* avg_ms,
                        double* work_per_launch);
 /* Teacher-forced scoring: fp32 logits of every row of `tokens` (one sequence,
@@ -188,14 +192,18 @@ int rlb_score(rlb_instance* h, const int32_t* tokens, int32_t n, float* out_logi
 /* C = A[M,K] . B[N,K]^T with epilogue: 0 bf16 out (+bias if bias!=NULL),
  * 1 fp32 residual add (C fp32 in/out), 2 SwiGLU over 64-row interleaved
  * gate/up blocks (bf16 out [M, N/2]), 3 fp32 out.  block_n 128 or 256;
- * splits > 1 runs split-K (fp32 partials + ordered reduce; epilogues 0,1,3).
- * All device pointers. */
+ * block_m 256 (two 128-row accumulators per CTA) or 128 (one).  splits > 1
+ * runs split-K: epilogue 1 with block_n 128 reduces the splits inside a
+ * thread-block cluster (the engine's path); epilogues 0 and 3 write fp32
+ * partials and reduce them in order in a second kernel.  All device
+ * pointers. */
 int rlb_gemm(int device, int32_t M, int32_t N, int32_t K, const void* A, const void* B,
-             const void* bias, void* C, int32_t epilogue, int32_t block_n, int32_t splits);
+             const void* bias, void* C, int32_t epilogue, int32_t block_n, int32_t splits,
+             int32_t block_m);
 /* Average time of `iters` back-to-back launches of one GEMM configuration on
  * scratch buffers (tile / split-K tuning; epilogue 4 = argmax partials). */
 int rlb_bench_gemm(int device, int32_t M, int32_t N, int32_t K, int32_t epilogue, int32_t block_n,
-                   int32_t splits, int32_t iters, double* avg_ms);
+                   int32_t splits, int32_t block_m, int32_t iters, double* avg_ms);
 
 #ifdef __cplusplus
 }

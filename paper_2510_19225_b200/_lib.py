@@ -10,7 +10,10 @@ import os
 
 import numpy as np
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "librlb.so")
+# RLB_LIB selects another build of the same ABI (A/B bit-identity checks of a
+# kernel change against the previous build); the default is the in-tree build.
+LIB_PATH = os.environ.get("RLB_LIB") or os.path.join(
+    os.path.dirname(os.path.abspath(__file__)), "librlb.so")
 
 RLB_OK, RLB_ERR_ARG, RLB_ERR_CUDA, RLB_ERR_STATE, RLB_ERR_CAPACITY = 0, -1, -2, -3, -4
 
@@ -108,10 +111,11 @@ _SIGS = {
     "rlb_status": (ctypes.c_int, [_P, ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_int32),
                                   ctypes.POINTER(ctypes.c_uint64)]),
     "rlb_score": (ctypes.c_int, [_P, _P, ctypes.c_int32, _P]),
-    "rlb_bench_gemm": (ctypes.c_int, [ctypes.c_int] + [ctypes.c_int32] * 7 +
+    "rlb_bench_gemm": (ctypes.c_int, [ctypes.c_int] + [ctypes.c_int32] * 8 +
                        [ctypes.POINTER(ctypes.c_double)]),
     "rlb_gemm": (ctypes.c_int, [ctypes.c_int, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, _P, _P,
-                                _P, _P, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32]),
+                                _P, _P, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,
+                                ctypes.c_int32]),
 }
 EXPORTED = tuple(_SIGS)
 

@@ -75,9 +75,9 @@ constexpr int RING_ROWS = 512;
 // Split-K factor of an [N, K] projection: the largest divisor d of the K
 // blocks with (N-tiles x 2 row tiles of a 512-row decode step) x d <= max_ctas
 // and >= 4 K blocks per split.  Depends on the weight shape only.  The short-K
-// projections (qkv, o) stop at half the SMs: each extra split adds an fp32
-// partial that the row consumer must read (measured: 100.4k vs 98.7k tok/s
-// for splits 2/3/5 vs 4/6/5 on config 2).
+// O projection stops at half the SMs: each extra split adds an fp32 partial
+// that the row consumer must read (measured: 100.4k vs 98.7k tok/s for O /
+// down splits 3/5 vs 6/5 on config 2).
 static int pick_splits(int N, int K, int bn, int max_ctas) {
   const int nk = K / 64;
   const int tiles = ((N + bn - 1) / bn) * 2;
@@ -150,18 +150,28 @@ struct rlb_instance {
   // shape only (never of M or of the engine config), so every instance of
   // the same model reduces every row identically.
   int sp_qkv = 1, sp_o = 1, sp_down = 1;
-  float* d_part = nullptr;  // split-K partials [splits][max_rows][N]
-  int pending_rows = 0;     // rows of the forward whose last down partials await the head
+  // rows per GEMM CTA: QKV uses 128-row tiles instead of split-K (twice the
+  // CTAs, and its RoPE / KV-append epilogue runs straight from TMEM); the
+  // others share each weight stage between two 128-row accumulators
+  int bm_qkv = 128, bm_o = 256, bm_gu = 256, bm_down = 256;
+  // split-K O / down: sum the splits inside a cluster and add into h in the
+  // GEMM epilogue (true), or write fp32 partials that the following RMSNorm
+  // kernel sums in split order (false)
+  // (measured on B200, 1.5B shape, 512 rows: cluster for down (5 splits),
+  // partials for O (3 splits); scripts/sweep_bm.sh)
+  bool cl_o = false, cl_down = true;
+  int pending_rows = 0;     // partial mode: rows whose last down partials await the head
+  float* d_part = nullptr;  // split-K partials [splits][max_rows][H] (partial mode)
   int64_t launches_per_forward(int R_logits) const {
-    // embed + first norm + per layer (4 GEMMs, qkv_rope, attention [+window
-    // combine], 2 residual norms; the last layer's second one is the head's)
-    // + head (norm, lm_head, argmax)
-    const int per_layer = 8 + (max_splits > 1 ? 1 : 0);
+    // embed + first norm + per layer (4 GEMMs, attention [+window combine],
+    // 2 norms; the last layer's second one is the head's) + head (norm,
+    // lm_head, argmax)
+    const int per_layer = 7 + (max_splits > 1 ? 1 : 0);
     return 2 + static_cast<int64_t>(m.layers) * per_layer - 1 + (R_logits > 0 ? 3 : 0);
   }
   int proj(const CUtensorMap& a, const CUtensorMap& b, int bn, int splits, int epi, int R, int N,
-           int K, const bf16* bias, void* out, int ldo);
-  // KV target of rlb_profile_kernel's qkv_rope timing (clobbers the last
+           int K, const bf16* bias, void* out, int ldo, int bm = 256);
+  // KV target of rlb_profile_kernel's qkv timing (clobbers the last
   // layer's entries of the current positions: only for a throw-away rollout)
   bf16* kv_scratch() const { return kv + layer_stride * (m.layers - 1); }
 
@@ -224,7 +234,7 @@ int rlb_instance::init() {
   prefill_rows = std::max(prefill_rows, 128);
   max_rows = std::max(prefill_rows, max_slots);
   max_rows = (max_rows + 255) / 256 * 256;
-  sp_qkv = pick_splits(QKV, H, BN_QKV, 74);
+  sp_qkv = 1;   // 128-row tiles give QKV its parallelism
   sp_o = pick_splits(H, NQ * D, BN_O, 74);
   sp_down = pick_splits(H, F, BN_DOWN, 148);
   if (const char* ov = std::getenv("RLB_SPLITS")) {   // "qkv,o,down" (tuning; process-wide)
@@ -237,6 +247,24 @@ int rlb_instance::init() {
       sp_qkv = a;
       sp_o = b;
       sp_down = c;
+    }
+  }
+
+  if (const char* ov = std::getenv("RLB_CLUSTER")) {   // "o,down" 0/1 (tuning; process-wide)
+    int a = 0, b = 0;
+    if (std::sscanf(ov, "%d,%d", &a, &b) == 2) {
+      cl_o = a != 0;
+      cl_down = b != 0;
+    }
+  }
+  if (const char* ov = std::getenv("RLB_BM")) {   // "qkv,o,gate_up,down" (tuning; process-wide)
+    int a = 0, b = 0, c = 0, d = 0;
+    if (std::sscanf(ov, "%d,%d,%d,%d", &a, &b, &c, &d) == 4) {
+      for (int v : {a, b, c, d}) RLB_CHECK(v == 128 || v == 256, RLB_ERR_ARG, "RLB_BM: 128 or 256");
+      bm_qkv = a;
+      bm_o = b;
+      bm_gu = c;
+      bm_down = d;
     }
   }
 
@@ -282,8 +310,7 @@ int rlb_instance::init() {
   const int logit_rows = (max_slots + 127) / 128 * 128;
   if ((rc = dalloc(&d_logits, static_cast<size_t>(logit_rows) * V))) return rc;
   if ((rc = dalloc(&d_ws, R * ws_row / sizeof(float)))) return rc;
-  const size_t part = std::max({static_cast<size_t>(sp_qkv) * QKV, static_cast<size_t>(sp_o) * H,
-                                static_cast<size_t>(sp_down) * H});
+  const size_t part = std::max({static_cast<size_t>(sp_o) * H, static_cast<size_t>(sp_down) * H});
   if ((rc = dalloc(&d_part, part * R))) return rc;
   if ((rc = dalloc(&d_ring, static_cast<size_t>(RING_ROWS) * max_slots))) return rc;
   if ((rc = dalloc(&d_ring_ctr, 1)) || (rc = dalloc(&d_ring_cur, 1))) return rc;
@@ -346,12 +373,15 @@ int rlb_instance::bind_arena() {
 }
 
 int rlb_instance::forward_layers(int R) {
-  // Per layer: QKV / O / down GEMMs write split-K fp32 partials that their
-  // row-wise consumers reduce in split order, fused with what they do anyway:
-  //   qkv partials -> [sum + bias + RoPE + KV append]        (qkv_rope)
-  //   o partials   -> [h += sum; xn = RMSNorm(h) * ln2]       (resid_norm)
-  //   down partials-> [h += sum; xn = RMSNorm(h) * ln1(l+1)]  (resid_norm; the
-  //                    last layer's is folded into the head's final norm)
+  // Per layer:
+  //   qkv  GEMM -> [sum + bias + RoPE -> q, K/V into the paged cache] in its
+  //               epilogue (EPI_ROPE; splits reduced in a cluster if split)
+  //   attention
+  //   o    GEMM -> h += sum (EPI_RESADD, cluster) or fp32 partials that
+  //               resid_norm sums in split order -> RMSNorm(ln2) -> xn
+  //   gate_up GEMM -> SwiGLU -> act
+  //   down GEMM -> as o, then RMSNorm(ln1 of the next layer); the last
+  //               layer's partials are summed by the head's norm
   int rc;
   if ((rc = embed_launch(embed, H, d_row_tok, R, d_h, st))) return rc;
   if ((rc = resid_norm_launch(d_h, nullptr, 0, R, nullptr, R, L[0].ln1, H, m.rms_eps, d_xn, false,
@@ -360,46 +390,62 @@ int rlb_instance::forward_layers(int R) {
   for (int l = 0; l < m.layers; ++l) {
     const LayerW& w = L[l];
     bf16* kv_l = kv + layer_stride * l;
-    if ((rc = proj(m_xn, w.m_qkv, BN_QKV, sp_qkv, EPI_PARTIAL, R, QKV, H, nullptr, nullptr, 0)))
-      return rc;
-    if ((rc = qkv_rope_launch(d_part, sp_qkv, R, w.bqkv, d_row_slot, d_row_pos, R, d_rope, NQ, NKV,
-                              D, d_q, NQ * D, kv_l, d_bt, pps, st)))
-      return rc;
+    GemmParams pq{R, QKV, H, w.bqkv, nullptr, 0, sp_qkv, nullptr};
+    pq.rope = RopeDst{d_row_slot, d_row_pos, d_rope, d_q, NQ * D, kv_l, d_bt, pps, NQ, NKV, D};
+    if ((rc = gemm_launch(m_xn, w.m_qkv, BN_QKV, EPI_ROPE, pq, st, bm_qkv))) return rc;
     AttnArgs a{d_q, NQ * D, kv_l, d_bt, pps, d_row_slot, d_row_pos, R, NQ, NKV, D, max_splits,
                d_ws, d_attn, NQ * D};
     if ((rc = attention_launch(a, st))) return rc;
-    if ((rc = proj(m_attn, w.m_o, BN_O, sp_o, EPI_PARTIAL, R, H, NQ * D, nullptr, nullptr, 0)))
+    if (cl_o) {
+      if ((rc = proj(m_attn, w.m_o, BN_O, sp_o, EPI_RESADD, R, H, NQ * D, nullptr, d_h, H, bm_o)) ||
+          (rc = resid_norm_launch(d_h, nullptr, 0, R, nullptr, R, w.ln2, H, m.rms_eps, d_xn, false,
+                                  st)))
+        return rc;
+    } else {
+      if ((rc = proj(m_attn, w.m_o, BN_O, sp_o, EPI_PARTIAL, R, H, NQ * D, nullptr, nullptr, 0,
+                     bm_o)) ||
+          (rc = resid_norm_launch(d_h, d_part, sp_o, R, nullptr, R, w.ln2, H, m.rms_eps, d_xn, true,
+                                  st)))
+        return rc;
+    }
+    if ((rc = proj(m_xn, w.m_gu, BN_GU, 1, EPI_SWIGLU, R, 2 * F, H, nullptr, d_act, F, bm_gu)))
       return rc;
-    if ((rc = resid_norm_launch(d_h, d_part, sp_o, R, nullptr, R, w.ln2, H, m.rms_eps, d_xn, true,
-                                st)))
-      return rc;
-    if ((rc = proj(m_xn, w.m_gu, BN_GU, 1, EPI_SWIGLU, R, 2 * F, H, nullptr, d_act, F))) return rc;
-    if ((rc = proj(m_act, w.m_down, BN_DOWN, sp_down, EPI_PARTIAL, R, H, F, nullptr, nullptr, 0)))
-      return rc;
-    if (l + 1 < m.layers &&
-        (rc = resid_norm_launch(d_h, d_part, sp_down, R, nullptr, R, L[l + 1].ln1, H, m.rms_eps,
-                                d_xn, true, st)))
-      return rc;
+    const bool last = l + 1 == m.layers;
+    if (cl_down) {
+      if ((rc = proj(m_act, w.m_down, BN_DOWN, sp_down, EPI_RESADD, R, H, F, nullptr, d_h, H,
+                     bm_down)))
+        return rc;
+      if (!last && (rc = resid_norm_launch(d_h, nullptr, 0, R, nullptr, R, L[l + 1].ln1, H,
+                                           m.rms_eps, d_xn, false, st)))
+        return rc;
+    } else {
+      if ((rc = proj(m_act, w.m_down, BN_DOWN, sp_down, EPI_PARTIAL, R, H, F, nullptr, nullptr, 0,
+                     bm_down)))
+        return rc;
+      // the last layer's partials are summed by the head's norm (its rows only)
+      if (!last && (rc = resid_norm_launch(d_h, d_part, sp_down, R, nullptr, R, L[l + 1].ln1, H,
+                                           m.rms_eps, d_xn, true, st)))
+        return rc;
+    }
   }
-  pending_rows = R;   // the last down projection's partials wait for the head
+  pending_rows = R;
   return RLB_OK;
 }
 
 int rlb_instance::proj(const CUtensorMap& a, const CUtensorMap& b, int bn, int splits, int epi,
-                       int R, int N, int K, const bf16* bias, void* out, int ldo) {
+                       int R, int N, int K, const bf16* bias, void* out, int ldo, int bm) {
   GemmParams p{R, N, K, bias, out, ldo, splits < 1 ? 1 : splits, d_part};
-  return gemm_launch(a, b, bn, epi, p, st);
+  return gemm_launch(a, b, bn, epi, p, st, bm);
 }
 
-// Final residual (last down projection's partials) + RMSNorm over the rows
-// listed in d_logit_src, lm_head, and (optionally) argmax + append into the
+// Final RMSNorm over the rows listed in d_logit_src, lm_head, and (optionally) argmax + append into the
 // slots listed in d_logit_slot.  h is not written, so the head can run over
 // several row blocks of one forward.
 int rlb_instance::head(int Lrows, bool append) {
   if (Lrows <= 0) return RLB_OK;
   int rc;
-  if ((rc = resid_norm_launch(d_h, d_part, sp_down, pending_rows, d_logit_src, Lrows, norm, H,
-                              m.rms_eps, d_xn, false, st)))
+  if ((rc = resid_norm_launch(d_h, cl_down ? nullptr : d_part, cl_down ? 0 : sp_down, pending_rows,
+                              d_logit_src, Lrows, norm, H, m.rms_eps, d_xn, false, st)))
     return rc;
   if (!append) return proj(m_xn, m_lm, BN_LM, 1, EPI_F32, Lrows, V, H, nullptr, d_logits, V);
   const int ntiles = (V + BN_LM - 1) / BN_LM;
@@ -900,25 +946,28 @@ int rlb_profile_kernel(rlb_instance* h, int32_t which, int32_t iters, double* av
                    h->NKV, D, h->max_splits, h->d_ws, h->d_attn, NQ * D};
         return attention_launch(a, h->st);
       }
-      // split projections: the GEMM writing its split-K partials (the reduce
-      // is fused into the consumer kernel and not counted here)
+      // projections with their fused epilogues, outputs to scratch where the
+      // product writes state (fp32 h -> the partial workspace; qkv's K/V go
+      // to the last layer's pages: timing only, the rollout that was
+      // profiled is discarded)
       case 1: return h->proj(h->m_xn, w.m_gu, BN_GU, 1, EPI_SWIGLU, R, 2 * F, H, nullptr,
-                             h->d_act, F);
-      case 2: return h->proj(h->m_act, w.m_down, BN_DOWN, h->sp_down, EPI_PARTIAL, R, H, F,
-                             nullptr, nullptr, 0);
-      case 3: return h->proj(h->m_xn, w.m_qkv, BN_QKV, h->sp_qkv, EPI_PARTIAL, R, h->QKV, H,
-                             nullptr, nullptr, 0);
-      case 4: return h->proj(h->m_attn, w.m_o, BN_O, h->sp_o, EPI_PARTIAL, R, H, NQ * D, nullptr,
-                             nullptr, 0);
+                             h->d_act, F, h->bm_gu);
+      case 2: return h->proj(h->m_act, w.m_down, BN_DOWN, h->sp_down,
+                             h->cl_down ? EPI_RESADD : EPI_PARTIAL, R, H, F, nullptr, h->d_part, H,
+                             h->bm_down);
+      case 3: {
+        GemmParams pq{R, h->QKV, H, w.bqkv, nullptr, 0, h->sp_qkv, nullptr};
+        pq.rope = RopeDst{h->d_row_slot, h->d_row_pos, h->d_rope, h->d_q, NQ * D, h->kv_scratch(),
+                          h->d_bt, h->pps, NQ, h->NKV, D};
+        return gemm_launch(h->m_xn, w.m_qkv, BN_QKV, EPI_ROPE, pq, h->st, h->bm_qkv);
+      }
+      case 4: return h->proj(h->m_attn, w.m_o, BN_O, h->sp_o, h->cl_o ? EPI_RESADD : EPI_PARTIAL,
+                             R, H, NQ * D, nullptr, h->d_part, H, h->bm_o);
       case 5: return h->proj(h->m_xn, h->m_lm, BN_LM, 1, EPI_ARGMAX, R, h->V, H, nullptr,
                              h->d_logits, (h->V + BN_LM - 1) / BN_LM);
-      // row consumers, on the partial buffer as the last projection left it
-      // (timing only; writes go to scratch outputs)
-      case 6: return resid_norm_launch(h->d_h, h->d_part, h->sp_down, R, nullptr, R, w.ln2, H,
+      case 6: return resid_norm_launch(h->d_h, h->cl_down ? nullptr : h->d_part,
+                                       h->cl_down ? 0 : h->sp_down, R, nullptr, R, w.ln2, H,
                                        h->m.rms_eps, h->d_xn, false, h->st);
-      case 7: return qkv_rope_launch(h->d_part, h->sp_qkv, R, w.bqkv, h->d_row_slot,
-                                     h->d_row_pos, R, h->d_rope, NQ, h->NKV, D, h->d_q, NQ * D,
-                                     h->kv_scratch(), h->d_bt, h->pps, h->st);
     }
     set_error("unknown kernel id");
     return RLB_ERR_ARG;
@@ -937,8 +986,7 @@ int rlb_profile_kernel(rlb_instance* h, int32_t which, int32_t iters, double* av
     case 3: work = 2.0 * R * h->QKV * H; break;
     case 4: work = 2.0 * R * H * NQ * D; break;
     case 5: work = 2.0 * R * h->V * static_cast<double>(H); break;
-    case 6: work = R * (h->sp_down + 2.0) * H * 4.0 + R * H * 2.0; break;      // bytes
-    case 7: work = R * (h->sp_qkv * 4.0 + 2.0) * h->QKV; break;                 // bytes
+    case 6: work = R * H * (4.0 * (h->cl_down ? 1 : 1 + h->sp_down) + 2.0); break;  // bytes
     default: RLB_CHECK(false, RLB_ERR_ARG, "unknown kernel id");
   }
   int rc = launch();  // warm

@@ -17,13 +17,18 @@
 //               accumulator 1 (tcgen05.ld 32 lanes x 16 columns) and apply the
 //               fused op: bias+bf16 / fp32 residual add / SwiGLU / fp32 /
 //               greedy argmax partials.
-// Split-K (grid.z = splits) covers the small-N projections of a decode step:
-// each split stores an fp32 partial and the last CTA of the tile to arrive
-// (atomic tile counter) sums the partials in split order and applies the
-// epilogue -- no extra launch.  The split count is a property of the weight
-// matrix (never of M), so a token row's result is bit-identical in a 512-row
-// decode batch and in a varlen prefill chunk -- migration resume relies on
-// this (SURVEY.md §7 hard part 2).
+// Split-K (grid.z = splits) covers the small-N projections of a decode step.
+// The S split CTAs of a tile form one (1,1,S) thread-block cluster: each
+// stages its fp32 partial tile in its own shared memory, and after a cluster
+// barrier CTA z sums rows [z*256/S, (z+1)*256/S) of all S partials through
+// distributed shared memory in split order (z = 0..S-1) and applies the
+// epilogue -- residual add into h (EPI_RESADD) or bias + RoPE + q / paged
+// K,V stores (EPI_ROPE).  No partial reaches HBM and no consumer kernel
+// re-reads it.  The split count is a property of the weight matrix (never of
+// M), so a token row's result is bit-identical in a 512-row decode batch and
+// in a varlen prefill chunk -- migration resume relies on this (SURVEY.md §7
+// hard part 2).  EPI_PARTIAL (fp32 partials to a workspace) remains for the
+// kernel-level test entry rlb_gemm.
 #define RLB_PDL_CLASS 1
 #include "internal.h"
 
@@ -32,19 +37,22 @@
 
 namespace rlb {
 
-constexpr int BM = 256;      // rows per CTA (two UMMA_M=128 accumulators)
-constexpr int HM = 128;      // rows per accumulator
+constexpr int HM = 128;      // rows per accumulator (UMMA_M)
 constexpr int BK = 64;       // K elements per stage (one 128 B swizzle atom)
 constexpr int GEMM_THREADS = 384;
 
-template <int BN>
+// NACC accumulators of 128 rows per CTA: 2 (256-row tiles, the B stage is
+// shared by both) or 1 (128-row tiles: twice the CTAs for short-K / small-N
+// projections that would otherwise need split-K).
+template <int BN, int NACC>
 struct GemmCfg {
-  static constexpr int A_BYTES = HM * BK * 2;          // one half
+  static constexpr int BMT = HM * NACC;                // rows per CTA
+  static constexpr int A_BYTES = HM * BK * 2;          // one accumulator's rows
   static constexpr int B_BYTES = BN * BK * 2;
-  static constexpr int STAGE_BYTES = 2 * A_BYTES + B_BYTES;
-  static constexpr int STAGES = BN == 256 ? 3 : 4;
+  static constexpr int STAGE_BYTES = NACC * A_BYTES + B_BYTES;
+  static constexpr int STAGES = BN == 256 ? 3 : (NACC == 2 ? 4 : 6);
   static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 256;
-  static constexpr uint32_t TMEM_COLS = 2 * BN;
+  static constexpr uint32_t TMEM_COLS = NACC * BN;
 };
 
 __device__ __forceinline__ float silu_f(float g) { return __fdividef(g, 1.0f + __expf(-g)); }
@@ -92,11 +100,237 @@ __global__ void __launch_bounds__(256) splitk_reduce_kernel(GemmParams p) {
   }
 }
 
-template <int BN, int EPI>
+constexpr int EPI_LDS = 128 + 4;   // padded fp32 row of a staged 128-column tile
+
+// Split-K reduction of one BMT x 128 tile inside its cluster: this CTA (rank
+// z of S) owns tile rows [z*BMT/S, (z+1)*BMT/S); epilogue warp ew (of NW)
+// takes every NW-th of them (<= 32 rows, so lane k can hold row k's
+// metadata).  Partials are summed in split order 0..S-1 (the association of
+// a sequential sum), then the epilogue is applied.  Rows go in groups of G
+// with every load of the group issued before any store, so the L2 / DSMEM
+// latencies overlap.
+template <int EPI, int BMT, int NW>
+__device__ __forceinline__ void cluster_epilogue(const GemmParams& p, uint32_t stage_u32,
+                                                 int m_blk, int n_blk, int ew, int lane) {
+  constexpr int G = 4;
+  const int S = p.splits;
+  const int z = static_cast<int>(cluster_rank());
+  const int r0 = z * BMT / S, r1 = (z + 1) * BMT / S;
+  uint32_t base[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) base[i] = i < S ? dsmem_addr(stage_u32, i) : 0u;
+  const int last = min(r1, p.M - m_blk * BMT);
+  const int nrows = last > r0 + ew ? (last - (r0 + ew) + NW - 1) / NW : 0;
+  if constexpr (EPI == EPI_RESADD) {
+    // h[m, n..n+3] += sum_z part_z: one row per warp step, one float4 per lane
+    const int n = n_blk * 128 + lane * 4;
+    if (n >= p.N) return;
+    float* h = reinterpret_cast<float*>(p.out);
+#pragma unroll 1
+    for (int k0 = 0; k0 < nrows; k0 += G) {
+      float4 x[G], acc[G];
+#pragma unroll
+      for (int g = 0; g < G; ++g) {
+        if (k0 + g < nrows) {
+          const int rr = r0 + ew + NW * (k0 + g);
+          x[g] = *reinterpret_cast<const float4*>(h + static_cast<size_t>(m_blk * BMT + rr) * p.ldo + n);
+          const uint32_t off = static_cast<uint32_t>((rr * EPI_LDS + lane * 4) * 4);
+          acc[g] = dsmem_ld4(base[0] + off);
+#pragma unroll
+          for (int i = 1; i < 8; ++i) {
+            if (i < S) {
+              const float4 v = dsmem_ld4(base[i] + off);
+              acc[g].x += v.x;
+              acc[g].y += v.y;
+              acc[g].z += v.z;
+              acc[g].w += v.w;
+            }
+          }
+        }
+      }
+#pragma unroll
+      for (int g = 0; g < G; ++g) {
+        if (k0 + g < nrows) {
+          const int rr = r0 + ew + NW * (k0 + g);
+          x[g].x += acc[g].x;
+          x[g].y += acc[g].y;
+          x[g].z += acc[g].z;
+          x[g].w += acc[g].w;
+          *reinterpret_cast<float4*>(h + static_cast<size_t>(m_blk * BMT + rr) * p.ldo + n) = x[g];
+        }
+      }
+    }
+  } else if constexpr (EPI == EPI_ROPE) {
+    // 64 rotation pairs (c1, c1 + D/2) per 128-column tile; lane takes pairs
+    // lane and lane + 32.  x = sum_z part + bias; q/k rotated, v copied; K/V
+    // into the slot's page.
+    const RopeDst& d = p.rope;
+    const int hd = d.d / 2;
+    const size_t head_stride = static_cast<size_t>(2) * PAGE * d.d;
+    int pos_l = 0;
+    size_t kvo_l = 0;
+    if (lane < nrows) {
+      const int m = m_blk * BMT + r0 + ew + NW * lane;
+      pos_l = d.row_pos[m];
+      const int page = d.block_table[static_cast<size_t>(d.row_slot[m]) * d.bt_stride + pos_l / PAGE];
+      kvo_l = static_cast<size_t>(page) * head_stride * d.nkv + static_cast<size_t>(pos_l % PAGE) * d.d;
+    }
+    int jv[2], c1v[2], headv[2];
+    float b1[2], b2[2];
+#pragma unroll
+    for (int t = 0; t < 2; ++t) {
+      const int pi = lane + 32 * t;
+      jv[t] = pi % hd;
+      c1v[t] = (pi / hd) * d.d + jv[t];
+      const int col1 = n_blk * 128 + c1v[t];
+      headv[t] = col1 / d.d;
+      b1[t] = __bfloat162float(p.bias[col1]);
+      b2[t] = __bfloat162float(p.bias[col1 + hd]);
+    }
+#pragma unroll 1
+    for (int k0 = 0; k0 < nrows; k0 += G) {
+      float x1[G][2], x2[G][2];
+      float2 cs[G][2];
+#pragma unroll
+      for (int g = 0; g < G; ++g) {
+        const int posg = __shfl_sync(0xffffffffu, pos_l, (k0 + g) & 31);
+        if (k0 + g < nrows) {
+          const int rr = r0 + ew + NW * (k0 + g);
+#pragma unroll
+          for (int t = 0; t < 2; ++t) {
+            const uint32_t o1 = static_cast<uint32_t>((rr * EPI_LDS + c1v[t]) * 4);
+            const uint32_t o2 = o1 + static_cast<uint32_t>(hd * 4);
+            float a1 = dsmem_ld(base[0] + o1), a2 = dsmem_ld(base[0] + o2);
+#pragma unroll
+            for (int i = 1; i < 8; ++i) {
+              if (i < S) {
+                a1 += dsmem_ld(base[i] + o1);
+                a2 += dsmem_ld(base[i] + o2);
+              }
+            }
+            x1[g][t] = a1;
+            x2[g][t] = a2;
+            cs[g][t] = d.rope[static_cast<size_t>(posg) * hd + jv[t]];
+          }
+        }
+      }
+#pragma unroll
+      for (int g = 0; g < G; ++g) {
+        const unsigned long long kvo =
+            __shfl_sync(0xffffffffu, static_cast<unsigned long long>(kvo_l), (k0 + g) & 31);
+        if (k0 + g >= nrows) continue;
+        const int m = m_blk * BMT + r0 + ew + NW * (k0 + g);
+        bf16* kv_page = d.kv + kvo;
+#pragma unroll
+        for (int t = 0; t < 2; ++t) {
+          const int j = jv[t], head = headv[t];
+          const float v1 = x1[g][t] + b1[t];
+          const float v2 = x2[g][t] + b2[t];
+          if (head < d.nq + d.nkv) {
+            const float2 c = cs[g][t];
+            const float y1 = __fmaf_rn(v1, c.x, -v2 * c.y);
+            const float y2 = __fmaf_rn(v2, c.x, v1 * c.y);
+            bf16* o = head < d.nq ? d.q + static_cast<size_t>(m) * d.ldq + head * d.d
+                                  : kv_page + static_cast<size_t>(head - d.nq) * head_stride;
+            o[j] = __float2bfloat16_rn(y1);
+            o[j + hd] = __float2bfloat16_rn(y2);
+          } else {
+            bf16* o = kv_page + static_cast<size_t>(head - d.nq - d.nkv) * head_stride +
+                      static_cast<size_t>(PAGE) * d.d;
+            o[j] = __float2bfloat16_rn(v1);
+            o[j + hd] = __float2bfloat16_rn(v2);
+          }
+        }
+      }
+    }
+  }
+}
+
+// EPI_ROPE without split-K, straight from TMEM: the thread owns row m (its
+// TMEM lane) and the tile's 128 columns (one head of D=128, two of D=64).
+// Rotation partners c and c + D/2 are loaded as two 32-column chunks.
+__device__ __forceinline__ void rope_direct(const GemmParams& p, uint32_t tbase, int m, bool live,
+                                            int n_blk) {
+  const RopeDst& d = p.rope;
+  const int hd = d.d / 2;
+  const size_t head_stride = static_cast<size_t>(2) * PAGE * d.d;
+  int pos = 0;
+  bf16* kv_page = nullptr;
+  if (live) {
+    pos = d.row_pos[m];
+    const int page = d.block_table[static_cast<size_t>(d.row_slot[m]) * d.bt_stride + pos / PAGE];
+    kv_page = d.kv + static_cast<size_t>(page) * head_stride * d.nkv +
+              static_cast<size_t>(pos % PAGE) * d.d;
+  }
+#pragma unroll 1
+  for (int cp = 0; cp < 2; ++cp) {
+    const int a = (cp * 32 / hd) * d.d + (cp * 32) % hd;   // first column of the chunk
+    uint32_t r1[32], r2[32];
+    tmem_ld32(tbase + a, r1);
+    tmem_ld32(tbase + a + hd, r2);
+    tmem_ld_wait();
+    if (!live) continue;
+    const int col1 = n_blk * 128 + a;
+    const int head = col1 / d.d;
+    const int j0 = col1 % d.d;                               // < hd
+    const uint4* bb1 = reinterpret_cast<const uint4*>(p.bias + col1);
+    const uint4* bb2 = reinterpret_cast<const uint4*>(p.bias + col1 + hd);
+    float v1[32], v2[32];
+#pragma unroll
+    for (int h4 = 0; h4 < 4; ++h4) {
+      const uint4 u1 = bb1[h4], u2 = bb2[h4];
+      const uint32_t w1[4] = {u1.x, u1.y, u1.z, u1.w}, w2[4] = {u2.x, u2.y, u2.z, u2.w};
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        v1[8 * h4 + 2 * i] = __uint_as_float(r1[8 * h4 + 2 * i]) + bf_lo(w1[i]);
+        v1[8 * h4 + 2 * i + 1] = __uint_as_float(r1[8 * h4 + 2 * i + 1]) + bf_hi(w1[i]);
+        v2[8 * h4 + 2 * i] = __uint_as_float(r2[8 * h4 + 2 * i]) + bf_lo(w2[i]);
+        v2[8 * h4 + 2 * i + 1] = __uint_as_float(r2[8 * h4 + 2 * i + 1]) + bf_hi(w2[i]);
+      }
+    }
+    uint32_t o1[16], o2[16];
+    bf16* dst;
+    if (head < d.nq + d.nkv) {
+      const float4* cs4 = reinterpret_cast<const float4*>(d.rope + static_cast<size_t>(pos) * hd + j0);
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        const float4 c = cs4[i];                   // (cos, sin) of j0+2i, j0+2i+1
+        const float y1a = __fmaf_rn(v1[2 * i], c.x, -v2[2 * i] * c.y);
+        const float y2a = __fmaf_rn(v2[2 * i], c.x, v1[2 * i] * c.y);
+        const float y1b = __fmaf_rn(v1[2 * i + 1], c.z, -v2[2 * i + 1] * c.w);
+        const float y2b = __fmaf_rn(v2[2 * i + 1], c.z, v1[2 * i + 1] * c.w);
+        o1[i] = pack_bf2(y1a, y1b);
+        o2[i] = pack_bf2(y2a, y2b);
+      }
+      dst = head < d.nq ? d.q + static_cast<size_t>(m) * d.ldq + head * d.d
+                        : kv_page + static_cast<size_t>(head - d.nq) * head_stride;
+    } else {
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        o1[i] = pack_bf2(v1[2 * i], v1[2 * i + 1]);
+        o2[i] = pack_bf2(v2[2 * i], v2[2 * i + 1]);
+      }
+      dst = kv_page + static_cast<size_t>(head - d.nq - d.nkv) * head_stride +
+            static_cast<size_t>(PAGE) * d.d;
+    }
+    uint4* d1 = reinterpret_cast<uint4*>(dst + j0);
+    uint4* d2 = reinterpret_cast<uint4*>(dst + j0 + hd);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      d1[i] = make_uint4(o1[4 * i], o1[4 * i + 1], o1[4 * i + 2], o1[4 * i + 3]);
+      d2[i] = make_uint4(o2[4 * i], o2[4 * i + 1], o2[4 * i + 2], o2[4 * i + 3]);
+    }
+  }
+}
+
+template <int BN, int EPI, int NACC>
 __global__ void __launch_bounds__(GEMM_THREADS, 1)
     gemm_bf16_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                  GemmParams p) {
-  using C = GemmCfg<BN>;
+  using C = GemmCfg<BN, NACC>;
+  constexpr int BMT = C::BMT;
+  constexpr int NEW = 4 * NACC;                 // epilogue warps with an accumulator
+  constexpr bool kClusterEpi = cluster_epi(EPI) && BN == 128;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~static_cast<uintptr_t>(1023));
@@ -123,6 +357,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   const int nk_total = p.K / BK;
   const int nk = nk_total / p.splits;          // k-blocks of this split
   const int kb0 = blockIdx.z * nk;
+  // split-K cluster epilogue (S > 1) or direct from TMEM (S == 1)
+  const bool via_cluster = kClusterEpi && p.splits > 1;
 
   if (warp == 0 && lane == 0) {
     tma_prefetch(&tmA);
@@ -153,9 +389,11 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         mbar_wait(smem_u32(&empty[s]), ph ^ 1);
         mbar_expect_tx(smem_u32(&full[s]), C::STAGE_BYTES);
         const int kx = (kb0 + kb) * BK;
-        tma_load_2d(smem_u32(st), &tmA, smem_u32(&full[s]), kx, m_blk * BM);
-        tma_load_2d(smem_u32(st + C::A_BYTES), &tmA, smem_u32(&full[s]), kx, m_blk * BM + HM);
-        tma_load_2d(smem_u32(st + 2 * C::A_BYTES), &tmB, smem_u32(&full[s]), kx, n_blk * BN);
+#pragma unroll
+        for (int a = 0; a < NACC; ++a)
+          tma_load_2d(smem_u32(st + a * C::A_BYTES), &tmA, smem_u32(&full[s]), kx,
+                      m_blk * BMT + a * HM);
+        tma_load_2d(smem_u32(st + NACC * C::A_BYTES), &tmB, smem_u32(&full[s]), kx, n_blk * BN);
       }
     }
   } else if (warp == 1) {
@@ -167,24 +405,24 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         const uint32_t st = smem_u32(smem + s * C::STAGE_BYTES);
         mbar_wait(smem_u32(&full[s]), ph);
         tc_fence_after();
-        const uint64_t a0 = umma_desc_sw128(st);
-        const uint64_t a1 = umma_desc_sw128(st + C::A_BYTES);
-        const uint64_t bd = umma_desc_sw128(st + 2 * C::A_BYTES);
+        const uint64_t bd = umma_desc_sw128(st + NACC * C::A_BYTES);
 #pragma unroll
         for (int k = 0; k < BK / 16; ++k) {
           // +32 bytes per K=16 step inside the 128 B swizzle atom (encoded >> 4)
-          umma_bf16(tmem, a0 + 2 * k, bd + 2 * k, idesc, (kb | k) != 0);
-          umma_bf16(tmem + BN, a1 + 2 * k, bd + 2 * k, idesc, (kb | k) != 0);
+#pragma unroll
+          for (int a = 0; a < NACC; ++a)
+            umma_bf16(tmem + a * BN, umma_desc_sw128(st + a * C::A_BYTES) + 2 * k, bd + 2 * k,
+                      idesc, (kb | k) != 0);
         }
         umma_commit(smem_u32(&empty[s]));
       }
       umma_commit(smem_u32(tfull));
       if (stamp) p.dbg[3] = gtime();
     }
-  } else if (warp >= 4) {
-    const int half = (warp - 4) >> 2;          // accumulator 0 or 1
+  } else if (warp >= 4 && warp < 4 + NEW) {
+    const int half = (warp - 4) >> 2;          // accumulator
     const int q = warp & 3;                    // TMEM lane quadrant
-    const int m = m_blk * BM + half * HM + q * 32 + lane;
+    const int m = m_blk * BMT + half * HM + q * 32 + lane;
     const bool live = m < p.M;
     mbar_wait(smem_u32(tfull), 0);
     if (stamp && threadIdx.x == 128) p.dbg[4] = gtime();
@@ -240,13 +478,31 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         float2* part = reinterpret_cast<float2*>(p.out) + static_cast<size_t>(m) * p.ldo + n_blk;
         *part = make_float2(best, __int_as_float(bidx));
       }
+    } else if constexpr (EPI == EPI_ROPE) {
+      if (via_cluster) {
+        // stage this split's fp32 tile for the cluster reduction
+        float* stage = reinterpret_cast<float*>(smem);
+        const int row = half * HM + q * 32 + lane;
+#pragma unroll 1
+        for (int c = 0; c < BN; c += 32) {
+          uint32_t r[32];
+          tmem_ld32(tbase + c, r);
+          tmem_ld_wait();
+          float4* s4 = reinterpret_cast<float4*>(stage + row * EPI_LDS + c);
+#pragma unroll
+          for (int i = 0; i < 8; ++i)
+            s4[i] = make_float4(__uint_as_float(r[4 * i]), __uint_as_float(r[4 * i + 1]),
+                                __uint_as_float(r[4 * i + 2]), __uint_as_float(r[4 * i + 3]));
+        }
+      } else {
+        rope_direct(p, tbase, m, live, n_blk);
+      }
     } else if constexpr ((EPI == EPI_PARTIAL || EPI == EPI_F32) && BN == 128) {
       // fp32 tile out through shared memory so every global store is a full
       // 512-byte row (a thread-per-row store would issue 32 scattered 16-byte
       // requests per instruction).  The pipeline stages are free: the MMA
       // that consumed them has completed.  EPI_PARTIAL = this K range's fp32
-      // partial [z][M][N], reduced in split order by the row-wise consumer.
-      constexpr int LDS = BN + 4;                          // padded row (bank spread)
+      // partial [z][M][N], reduced in split order by the consumer.
       float* stage = reinterpret_cast<float*>(smem);
       const int row = half * HM + q * 32 + lane;           // row within the CTA tile
 #pragma unroll 1
@@ -254,27 +510,29 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         uint32_t r[32];
         tmem_ld32(tbase + c, r);
         tmem_ld_wait();
-        float4* s4 = reinterpret_cast<float4*>(stage + row * LDS + c);
+        float4* s4 = reinterpret_cast<float4*>(stage + row * EPI_LDS + c);
 #pragma unroll
         for (int i = 0; i < 8; ++i)
           s4[i] = make_float4(__uint_as_float(r[4 * i]), __uint_as_float(r[4 * i + 1]),
                               __uint_as_float(r[4 * i + 2]), __uint_as_float(r[4 * i + 3]));
       }
-      asm volatile("bar.sync 1, 256;" ::: "memory");
+      if (NACC == 2) asm volatile("bar.sync 1, 256;" ::: "memory");
+      else asm volatile("bar.sync 1, 128;" ::: "memory");
       float* base = EPI == EPI_PARTIAL ? p.ws + static_cast<size_t>(blockIdx.z) * p.M * p.N
                                        : reinterpret_cast<float*>(p.out);
       const int ld = EPI == EPI_PARTIAL ? p.N : p.ldo;
-      const int ew = warp - 4;                              // 8 epilogue warps
+      const int ew = warp - 4;
       const int n = n_blk * BN + lane * 4;
 #pragma unroll 4
-      for (int rr = ew; rr < BM; rr += 8) {
-        const int mm = m_blk * BM + rr;
+      for (int rr = ew; rr < BMT; rr += NEW) {
+        const int mm = m_blk * BMT + rr;
         if (mm >= p.M || n >= p.N) continue;
         *reinterpret_cast<float4*>(base + static_cast<size_t>(mm) * ld + n) =
-            *reinterpret_cast<const float4*>(stage + rr * LDS + lane * 4);
+            *reinterpret_cast<const float4*>(stage + rr * EPI_LDS + lane * 4);
       }
     } else {
-      // EPI_F32 / EPI_PARTIAL with BN=256, EPI_BF16(+bias), EPI_RESADD.
+      // EPI_F32 / EPI_PARTIAL with BN=256, EPI_BF16(+bias), EPI_RESADD
+      // (direct when not split, else staged for the cluster reduction).
       float* f32 = EPI == EPI_PARTIAL ? p.ws + static_cast<size_t>(blockIdx.z) * p.M * p.N
                                       : reinterpret_cast<float*>(p.out);
       const int ld = EPI == EPI_PARTIAL ? p.N : p.ldo;
@@ -283,6 +541,18 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         uint32_t r[32];
         tmem_ld32(tbase + c, r);
         tmem_ld_wait();
+        if constexpr (kClusterEpi) {
+          if (via_cluster) {
+            float* stage = reinterpret_cast<float*>(smem);
+            const int row = half * HM + q * 32 + lane;
+            float4* s4 = reinterpret_cast<float4*>(stage + row * EPI_LDS + c);
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+              s4[i] = make_float4(__uint_as_float(r[4 * i]), __uint_as_float(r[4 * i + 1]),
+                                  __uint_as_float(r[4 * i + 2]), __uint_as_float(r[4 * i + 3]));
+            continue;
+          }
+        }
         const int n = n_blk * BN + c;
         if (!live || n >= p.N) continue;
         if constexpr (EPI == EPI_BF16) {
@@ -327,6 +597,14 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
                                __uint_as_float(r[4 * i + 2]), __uint_as_float(r[4 * i + 3]));
         }
       }
+    }
+  }
+  if constexpr (kClusterEpi) {
+    if (via_cluster) {                       // uniform over the grid
+      cluster_sync();                        // every split's partial tile is staged
+      if (warp >= 4 && warp < 4 + NEW)
+        cluster_epilogue<EPI, BMT, NEW>(p, smem_u32(smem), m_blk, n_blk, warp - 4, lane);
+      cluster_sync();                        // remote reads done before any CTA exits
     }
   }
   if (stamp && threadIdx.x == 128) p.dbg[6] = gtime();
@@ -375,20 +653,24 @@ int make_kmajor_map(CUtensorMap* map, const void* ptr, int64_t rows, int64_t k, 
   return RLB_OK;
 }
 
-template <int BN, int EPI>
+template <int BN, int EPI, int NACC>
 static int set_attr() {
-  RLB_CUDA(cudaFuncSetAttribute(gemm_bf16_tc<BN, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                GemmCfg<BN>::SMEM));
+  RLB_CUDA(cudaFuncSetAttribute(gemm_bf16_tc<BN, EPI, NACC>,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                GemmCfg<BN, NACC>::SMEM));
   return RLB_OK;
 }
 
-template <int BN>
+template <int BN, int NACC>
 static int set_attr_bn() {
   int rc;
-  if ((rc = set_attr<BN, EPI_BF16>()) || (rc = set_attr<BN, EPI_RESADD>()) ||
-      (rc = set_attr<BN, EPI_F32>()) || (rc = set_attr<BN, EPI_ARGMAX>()) ||
-      (rc = set_attr<BN, EPI_SWIGLU>()) || (rc = set_attr<BN, EPI_PARTIAL>()))
+  if ((rc = set_attr<BN, EPI_BF16, NACC>()) || (rc = set_attr<BN, EPI_RESADD, NACC>()) ||
+      (rc = set_attr<BN, EPI_F32, NACC>()) || (rc = set_attr<BN, EPI_ARGMAX, NACC>()) ||
+      (rc = set_attr<BN, EPI_SWIGLU, NACC>()) || (rc = set_attr<BN, EPI_PARTIAL, NACC>()))
     return rc;
+  if constexpr (BN == 128) {
+    if ((rc = set_attr<BN, EPI_ROPE, NACC>())) return rc;
+  }
   return RLB_OK;
 }
 
@@ -398,49 +680,80 @@ int gemm_prepare() {
   RLB_CUDA(cudaGetDevice(&dev));
   if (done[dev & 63]) return RLB_OK;
   int rc;
-  if ((rc = set_attr_bn<128>()) || (rc = set_attr_bn<256>())) return rc;
+  if ((rc = set_attr_bn<128, 2>()) || (rc = set_attr_bn<256, 2>()) || (rc = set_attr_bn<128, 1>()) ||
+      (rc = set_attr_bn<256, 1>()))
+    return rc;
   done[dev & 63] = true;
   return RLB_OK;
 }
 
-template <int BN, int EPI>
+template <int BN, int EPI, int NACC>
 static int launch_one(const CUtensorMap& a, const CUtensorMap& b, const GemmParams& p,
                       cudaStream_t st) {
-  using C = GemmCfg<BN>;
+  using C = GemmCfg<BN, NACC>;
   RLB_CHECK((p.N + BN - 1) / BN <= 65535, RLB_ERR_ARG, "too many N tiles");
-  dim3 grid((p.M + BM - 1) / BM, (p.N + BN - 1) / BN, p.splits);
-  RLB_CUDA(launch_k(gemm_bf16_tc<BN, EPI>, grid, dim3(GEMM_THREADS), C::SMEM, st, a, b, p));
+  dim3 grid((p.M + C::BMT - 1) / C::BMT, (p.N + BN - 1) / BN, p.splits);
+  if (cluster_epi(EPI) && BN == 128 && p.splits > 1) {
+    // the split CTAs of a tile form one cluster (DSMEM reduction)
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = dim3(GEMM_THREADS);
+    cfg.dynamicSmemBytes = C::SMEM;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[2];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 1;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = static_cast<unsigned>(p.splits);
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[1].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl_enabled(RLB_PDL_CLASS) ? 2 : 1;
+    RLB_CUDA(cudaLaunchKernelEx(&cfg, gemm_bf16_tc<BN, EPI, NACC>, a, b, p));
+    return RLB_OK;
+  }
+  RLB_CUDA(launch_k(gemm_bf16_tc<BN, EPI, NACC>, grid, dim3(GEMM_THREADS), C::SMEM, st, a, b, p));
   return RLB_OK;
 }
 
-template <int BN>
+template <int BN, int NACC>
 static int launch_bn(const CUtensorMap& a, const CUtensorMap& b, int epi, const GemmParams& p,
                      cudaStream_t st) {
   switch (epi) {
-    case EPI_BF16: return launch_one<BN, EPI_BF16>(a, b, p, st);
-    case EPI_RESADD: return launch_one<BN, EPI_RESADD>(a, b, p, st);
-    case EPI_SWIGLU: return launch_one<BN, EPI_SWIGLU>(a, b, p, st);
-    case EPI_F32: return launch_one<BN, EPI_F32>(a, b, p, st);
-    case EPI_ARGMAX: return launch_one<BN, EPI_ARGMAX>(a, b, p, st);
-    case EPI_PARTIAL: return launch_one<BN, EPI_PARTIAL>(a, b, p, st);
+    case EPI_BF16: return launch_one<BN, EPI_BF16, NACC>(a, b, p, st);
+    case EPI_RESADD: return launch_one<BN, EPI_RESADD, NACC>(a, b, p, st);
+    case EPI_SWIGLU: return launch_one<BN, EPI_SWIGLU, NACC>(a, b, p, st);
+    case EPI_F32: return launch_one<BN, EPI_F32, NACC>(a, b, p, st);
+    case EPI_ARGMAX: return launch_one<BN, EPI_ARGMAX, NACC>(a, b, p, st);
+    case EPI_PARTIAL: return launch_one<BN, EPI_PARTIAL, NACC>(a, b, p, st);
+    case EPI_ROPE:
+      if constexpr (BN == 128) return launch_one<BN, EPI_ROPE, NACC>(a, b, p, st);
+      break;
   }
   set_error("bad epilogue");
   return RLB_ERR_ARG;
 }
 
 int gemm_launch(const CUtensorMap& a, const CUtensorMap& b, int block_n, int epi,
-                const GemmParams& p, cudaStream_t st) {
+                const GemmParams& p, cudaStream_t st, int block_m) {
   if (p.M <= 0) return RLB_OK;
   RLB_CHECK(p.K % BK == 0 && p.N % 16 == 0, RLB_ERR_ARG, "GEMM shape not tileable");
   RLB_CHECK(p.splits >= 1 && (p.K / BK) % p.splits == 0, RLB_ERR_ARG,
             "split-K must divide the K blocks");
-  RLB_CHECK((p.splits == 1 && epi != EPI_PARTIAL) || (epi == EPI_PARTIAL && p.ws != nullptr),
-            RLB_ERR_ARG, "split-K GEMMs write fp32 partials to a workspace (EPI_PARTIAL)");
+  RLB_CHECK(p.splits == 1 || (epi == EPI_PARTIAL && p.ws != nullptr) ||
+                (cluster_epi(epi) && block_n == 128 && p.splits <= 8),
+            RLB_ERR_ARG,
+            "split-K needs EPI_PARTIAL (workspace) or a cluster epilogue (BN=128, <= 8 splits)");
+  RLB_CHECK(epi != EPI_ROPE || (block_n == 128 && p.bias != nullptr && p.N % 128 == 0 &&
+                                128 % p.rope.d == 0),
+            RLB_ERR_ARG, "EPI_ROPE needs 128-column head tiles and a bias");
   RLB_CHECK(epi != EPI_SWIGLU || (block_n % 128 == 0 && p.N % 128 == 0), RLB_ERR_ARG,
             "SwiGLU GEMM needs 128-column gate/up tiles");
+  RLB_CHECK(block_m == 128 || block_m == 256, RLB_ERR_ARG, "block_m must be 128 or 256");
+  const bool two = block_m == 256;
   switch (block_n) {
-    case 128: return launch_bn<128>(a, b, epi, p, st);
-    case 256: return launch_bn<256>(a, b, epi, p, st);
+    case 128: return two ? launch_bn<128, 2>(a, b, epi, p, st) : launch_bn<128, 1>(a, b, epi, p, st);
+    case 256: return two ? launch_bn<256, 2>(a, b, epi, p, st) : launch_bn<256, 1>(a, b, epi, p, st);
   }
   set_error("block_n must be 128 or 256");
   return RLB_ERR_ARG;
@@ -451,7 +764,8 @@ int gemm_launch(const CUtensorMap& a, const CUtensorMap& b, int block_n, int epi
 // Microbenchmark: `iters` back-to-back launches of one GEMM configuration on
 // scratch buffers, timed with CUDA events (tile / split tuning).
 extern "C" int rlb_bench_gemm(int device, int32_t M, int32_t N, int32_t K, int32_t epilogue,
-                              int32_t block_n, int32_t splits, int32_t iters, double* avg_ms) {
+                              int32_t block_n, int32_t splits, int32_t block_m, int32_t iters,
+                              double* avg_ms) {
   using namespace rlb;
   RLB_CUDA(cudaSetDevice(device));
   int rc = gemm_prepare();
@@ -469,13 +783,14 @@ extern "C" int rlb_bench_gemm(int device, int32_t M, int32_t N, int32_t K, int32
     return rc;
   GemmParams p{M, N, K, nullptr, C, epilogue == EPI_SWIGLU ? N / 2 : N, S, C};
   if (epilogue == EPI_ARGMAX) p.ldo = (N + block_n - 1) / block_n;
-  const int epi = S > 1 ? static_cast<int>(EPI_PARTIAL) : epilogue;
+  RLB_CHECK(epilogue != EPI_ROPE, RLB_ERR_ARG, "EPI_ROPE needs an instance (rlb_profile_kernel)");
+  const int epi = S > 1 && !cluster_epi(epilogue) ? static_cast<int>(EPI_PARTIAL) : epilogue;
   cudaEvent_t e0, e1;
   RLB_CUDA(cudaEventCreate(&e0));
   RLB_CUDA(cudaEventCreate(&e1));
-  if ((rc = gemm_launch(ma, mb, block_n, epi, p, 0))) return rc;
+  if ((rc = gemm_launch(ma, mb, block_n, epi, p, 0, block_m))) return rc;
   RLB_CUDA(cudaEventRecord(e0, 0));
-  for (int i = 0; i < iters && !rc; ++i) rc = gemm_launch(ma, mb, block_n, epi, p, 0);
+  for (int i = 0; i < iters && !rc; ++i) rc = gemm_launch(ma, mb, block_n, epi, p, 0, block_m);
   RLB_CUDA(cudaEventRecord(e1, 0));
   RLB_CUDA(cudaEventSynchronize(e1));
   float ms = 0.f;
@@ -487,7 +802,7 @@ extern "C" int rlb_bench_gemm(int device, int32_t M, int32_t N, int32_t K, int32
     RLB_CUDA(cudaMalloc(&d, sizeof(h)));
     RLB_CUDA(cudaMemset(d, 0, sizeof(h)));
     p.dbg = d;
-    rc = gemm_launch(ma, mb, block_n, epi, p, 0);
+    rc = gemm_launch(ma, mb, block_n, epi, p, 0, block_m);
     RLB_CUDA(cudaMemcpy(h, d, sizeof(h), cudaMemcpyDeviceToHost));
     std::fprintf(stderr, "gemm dbg (ns from CTA start): setup %lld wait %lld mma_done %lld "
                  "epi_start %lld epi_end %lld dealloc %lld\n",
@@ -505,7 +820,7 @@ extern "C" int rlb_bench_gemm(int device, int32_t M, int32_t N, int32_t K, int32
 
 extern "C" int rlb_gemm(int device, int32_t M, int32_t N, int32_t K, const void* A, const void* B,
                         const void* bias, void* Cout, int32_t epilogue, int32_t block_n,
-                        int32_t splits) {
+                        int32_t splits, int32_t block_m) {
   using namespace rlb;
   RLB_CUDA(cudaSetDevice(device));
   int rc = gemm_prepare();
@@ -523,11 +838,11 @@ extern "C" int rlb_gemm(int device, int32_t M, int32_t N, int32_t K, const void*
   p.out = Cout;
   p.ldo = epilogue == EPI_SWIGLU ? N / 2 : N;
   p.splits = splits < 1 ? 1 : splits;
-  if (p.splits == 1) {
-    rc = gemm_launch(ma, mb, block_n, epilogue, p, 0);
+  if (p.splits == 1 || (epilogue == EPI_RESADD && block_n == 128)) {
+    rc = gemm_launch(ma, mb, block_n, epilogue, p, 0, block_m);   // RESADD: cluster split-K
   } else {
     RLB_CUDA(cudaMalloc(&p.ws, sizeof(float) * static_cast<size_t>(p.splits) * M * N));
-    rc = gemm_launch(ma, mb, block_n, EPI_PARTIAL, p, 0);
+    rc = gemm_launch(ma, mb, block_n, EPI_PARTIAL, p, 0, block_m);
     if (!rc) {
       switch (epilogue) {
         case EPI_BF16: splitk_reduce_kernel<EPI_BF16><<<M, 256>>>(p); break;

@@ -10,7 +10,23 @@ namespace rlb {
 constexpr int PAGE = 64;      // tokens per KV page
 
 enum Epi { EPI_BF16 = 0, EPI_RESADD = 1, EPI_SWIGLU = 2, EPI_F32 = 3, EPI_ARGMAX = 4,
-           EPI_PARTIAL = 5 };
+           EPI_PARTIAL = 5, EPI_ROPE = 6 };
+// Split-K epilogues reduced inside a (1,1,splits) thread-block cluster
+// through distributed shared memory (BN = 128): RESADD (h += sum) and ROPE.
+constexpr bool cluster_epi(int epi) { return epi == EPI_RESADD || epi == EPI_ROPE; }
+
+// EPI_ROPE destination: q rows, the layer's paged KV cache, RoPE table.
+struct RopeDst {
+  const int* row_slot;
+  const int* row_pos;
+  const float2* rope;        // [pos][D/2] (cos, sin)
+  bf16* q;
+  int ldq;
+  bf16* kv;                  // this layer's pages [page][kv_head][K|V][PAGE][D]
+  const int* block_table;
+  int bt_stride;
+  int nq, nkv, d;
+};
 
 struct GemmParams {
   int M, N, K;
@@ -20,12 +36,13 @@ struct GemmParams {
   int splits;     // split-K factor (1 = no split)
   float* ws;      // EPI_PARTIAL: fp32 partials [splits][M][N]
   unsigned long long* dbg;  // optional: globaltimer stamps of CTA 0 (latency breakdown)
+  RopeDst rope;   // EPI_ROPE only
 };
 
 int make_kmajor_map(CUtensorMap* map, const void* ptr, int64_t rows, int64_t k, int box_rows);
 int gemm_prepare();  // set smem attributes of every GEMM variant on the current device
 int gemm_launch(const CUtensorMap& a, const CUtensorMap& b, int block_n, int epi,
-                const GemmParams& p, cudaStream_t st);
+                const GemmParams& p, cudaStream_t st, int block_m = 256);
 
 // ---- elementwise / attention launchers (kernels.cu) ----
 struct AttnArgs {
@@ -43,10 +60,6 @@ int attention_windows(int max_seq);   // CTA windows per row (AttnArgs.max_split
 int embed_launch(const bf16* embed, int H, const int* tok, int R, float* h, cudaStream_t st);
 int resid_norm_launch(float* h, const float* part, int S, int Mp, const int* src_rows, int R,
                       const bf16* w, int H, float eps, bf16* xn, bool write_h, cudaStream_t st);
-int qkv_rope_launch(const float* part, int S, int Mp, const bf16* bias, const int* row_slot,
-                    const int* row_pos, int R, const float2* rope, int NQ, int NKV, int D,
-                    bf16* qout, int ldq, bf16* kv, const int* block_table, int bt_stride,
-                    cudaStream_t st);
 int argmax_append_launch(const float2* part, int ntiles, int L, const int* logit_slot,
                          int32_t* seq_tokens, int32_t* seq_len, const int32_t* seq_target,
                          int max_seq, int32_t* ring, const int32_t* ring_cur, int max_slots,

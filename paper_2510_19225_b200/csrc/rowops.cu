@@ -1,11 +1,7 @@
-// Row-wise consumers of the split-K projections (K3).  The QKV, O and down
-// GEMMs write fp32 partials [S][M][N]; these kernels reduce them in split
-// order (z = 0..S-1, the same for every row and every batch composition) and
-// fuse the reduction with the work that follows it anyway:
-//   qkv_rope    sum + bias -> RoPE(q, k) -> q buffer, K/V into the paged cache
-//   resid_norm  h += sum (residual) -> RMSNorm -> bf16 input of the next GEMM
-// S is a template parameter so every partial load of a thread is in flight
-// at once (the kernels are L2-latency bound otherwise).
+// K3 row kernel: residual stream -> RMSNorm -> bf16 input of the next GEMM.
+// The projections add their (cluster-reduced) split-K sums into h in their
+// epilogues, so the engine runs this with S = 0; S > 0 reduces fp32 partials
+// [S][M][N] in split order first (kept for partial-producing callers).
 #define RLB_PDL_CLASS 4
 #include "internal.h"
 
@@ -86,81 +82,6 @@ int resid_norm_launch(float* h, const float* part, int S, int Mp, const int* src
     default: RLB_CHECK(false, RLB_ERR_ARG, "split-K factor must be <= 8");
   }
 #undef RN_CASE
-  return RLB_OK;
-}
-
-// x = sum_z part[z][r] + bias (fp32).  q heads: rotated into qout; k heads:
-// rotated and written to the slot's KV page; v heads: copied to the page.
-// rope[pos][j] = (cos, sin) of pos * theta^(-2j/D).  Thread = rotation pair.
-template <int S>
-__global__ void __launch_bounds__(256) qkv_rope_kernel(
-    const float* __restrict__ part, int Mp, const bf16* __restrict__ bias,
-    const int* __restrict__ row_slot, const int* __restrict__ row_pos,
-    const float2* __restrict__ rope, int NQ, int NKV, int D, bf16* __restrict__ qout, int ldq,
-    bf16* __restrict__ kv, const int* __restrict__ block_table, int bt_stride) {
-  pdl_trigger();
-  pdl_wait();
-  const int r = blockIdx.x;
-  const int half = D / 2;
-  const int N = (NQ + 2 * NKV) * D;
-  const int pos = row_pos[r];
-  const int page = block_table[static_cast<size_t>(row_slot[r]) * bt_stride + pos / PAGE];
-  const size_t head_stride = static_cast<size_t>(2) * PAGE * D;
-  bf16* kv_page = kv + static_cast<size_t>(page) * head_stride * NKV +
-                  static_cast<size_t>(pos % PAGE) * D;
-  const size_t slab = static_cast<size_t>(Mp) * N;
-  const float* pr = part + static_cast<size_t>(r) * N;
-  const float2* cs = rope + static_cast<size_t>(pos) * half;
-  const int total = (NQ + 2 * NKV) * half;
-  for (int i = threadIdx.x; i < total; i += blockDim.x) {
-    const int head = i / half, j = i % half;
-    const int c1 = head * D + j, c2 = c1 + half;
-    float p1[S], p2[S];
-#pragma unroll
-    for (int z = 0; z < S; ++z) {
-      p1[z] = pr[z * slab + c1];
-      p2[z] = pr[z * slab + c2];
-    }
-    float x1 = p1[0], x2 = p2[0];
-#pragma unroll
-    for (int z = 1; z < S; ++z) {
-      x1 += p1[z];
-      x2 += p2[z];
-    }
-    x1 += __bfloat162float(bias[c1]);
-    x2 += __bfloat162float(bias[c2]);
-    if (head < NQ + NKV) {
-      const float2 c = cs[j];
-      const float y1 = __fmaf_rn(x1, c.x, -x2 * c.y);
-      const float y2 = __fmaf_rn(x2, c.x, x1 * c.y);
-      bf16* o = head < NQ ? qout + static_cast<size_t>(r) * ldq + head * D
-                          : kv_page + static_cast<size_t>(head - NQ) * head_stride;
-      o[j] = __float2bfloat16_rn(y1);
-      o[j + half] = __float2bfloat16_rn(y2);
-    } else {
-      bf16* o = kv_page + static_cast<size_t>(head - NQ - NKV) * head_stride +
-                static_cast<size_t>(PAGE) * D;
-      o[j] = __float2bfloat16_rn(x1);
-      o[j + half] = __float2bfloat16_rn(x2);
-    }
-  }
-}
-
-int qkv_rope_launch(const float* part, int S, int Mp, const bf16* bias, const int* row_slot,
-                    const int* row_pos, int R, const float2* rope, int NQ, int NKV, int D,
-                    bf16* qout, int ldq, bf16* kv, const int* block_table, int bt_stride,
-                    cudaStream_t st) {
-  if (R <= 0) return RLB_OK;
-#define QR_CASE(s)                                                                           \
-  case s:                                                                                    \
-    RLB_CUDA(launch_k(qkv_rope_kernel<s>, dim3(R), dim3(256), 0, st, part, Mp, bias, row_slot, \
-                      row_pos, rope, NQ, NKV, D, qout, ldq, kv, block_table, bt_stride));     \
-    break;
-  switch (S) {
-    QR_CASE(1) QR_CASE(2) QR_CASE(3) QR_CASE(4) QR_CASE(5) QR_CASE(6) QR_CASE(7) QR_CASE(8)
-    default: RLB_CHECK(false, RLB_ERR_ARG, "split-K factor must be 1..8");
-  }
-#undef QR_CASE
   return RLB_OK;
 }
 

@@ -224,7 +224,7 @@ class RolloutInstance:
         return out
 
     KERNELS = {"attention": 0, "gate_up": 1, "down": 2, "qkv": 3, "o_proj": 4, "lm_head": 5,
-               "resid_norm": 6, "qkv_rope": 7}
+               "resid_norm": 6}
 
     def stats(self, reset: bool = False) -> dict:
         """Cumulative device-time accounting (CUDA events on the instance stream)."""
@@ -254,7 +254,7 @@ class RolloutInstance:
 
 
 def gemm(device: int, A, B, bias=None, out=None, epilogue: int = 0, block_n: int = 128,
-         splits: int = 1):
+         splits: int = 1, block_m: int = 256):
     """Kernel-level entry point rlb_gemm on torch CUDA tensors (parity tests)."""
     import torch
     M, K = A.shape
@@ -268,5 +268,5 @@ def gemm(device: int, A, B, bias=None, out=None, epilogue: int = 0, block_n: int
             out = torch.zeros(M, N, dtype=torch.float32, device=A.device)
     check(_lib.lib().rlb_gemm(device, M, N, K, A.data_ptr(), B.data_ptr(),
                               bias.data_ptr() if bias is not None else None, out.data_ptr(),
-                              epilogue, block_n, splits))
+                              epilogue, block_n, splits, block_m))
     return out

@@ -24,7 +24,7 @@ def main():
     lib = _lib.lib()
     for name, M, N, K, epi, bn, sp in CASES:
         ms = ctypes.c_double()
-        _lib.check(lib.rlb_bench_gemm(0, M, N, K, epi, bn, sp, 50, ctypes.byref(ms)))
+        _lib.check(lib.rlb_bench_gemm(0, M, N, K, epi, bn, sp, 256, 50, ctypes.byref(ms)))
         tf = 2.0 * M * N * K / (ms.value * 1e-3) / 1e12
         print(f"{name:22s} M={M:5d} N={N:6d} K={K:5d} bn={bn} s={sp}: {ms.value * 1e3:8.2f} us  {tf:7.1f} TFLOP/s")
 

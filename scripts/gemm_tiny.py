@@ -4,5 +4,5 @@ from paper_2510_19225_b200 import _lib
 lib = _lib.lib()
 ms = ctypes.c_double()
 for case in [(512, 128, 64, 3, 128, 1), (512, 2048, 1536, 5, 128, 4), (4096, 17920, 1536, 2, 256, 1)]:
-    _lib.check(lib.rlb_bench_gemm(0, *case, 10, ctypes.byref(ms)))
+    _lib.check(lib.rlb_bench_gemm(0, *case, 256, 10, ctypes.byref(ms)))
     print(case, ms.value * 1e3, "us")

@@ -6,8 +6,9 @@
 set -e
 OUT=${OUT:-gpurun_out}
 CMD="python bench.py --steps 1 --warmup 1 --no-cpu-baseline"
+# the same command as the bench line minus the CPU baseline (the launch list is a share check)
 $CMD > $OUT/plain.json 2> $OUT/plain.err
-ncu --metrics gpu__time_duration.sum --clock-control none -s 120000 -c 800 --csv \
+ncu --metrics gpu__time_duration.sum --clock-control none -s 150000 -c 600 --csv \
     --log-file $OUT/launches.csv $CMD > $OUT/ncu_launch.log 2>&1
 ncu --set full --clock-control none --import-source on -k regex:attn_mma -s 3000 -c 2 \
     -o $OUT/prof_attn $CMD > $OUT/ncu_attn.log 2>&1
