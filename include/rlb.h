@@ -108,6 +108,31 @@ int rlb_weights_arena(rlb_instance* h, void** arena, int64_t* bytes);
 /* Declare the arena filled with `version` by an external copy (the fan-out
  * writes it with rlb_relayout_copy_range / rlb_copy_bytes). */
 int rlb_mark_weights(rlb_instance* h, uint64_t version);
+
+/* ---- double-buffered weights ------------------------
+ * Replaces the pull lifecycle mark_pulling -> pull -> mark_active
+ * (pkg/src/spotrl/sim/engine.py:597-656, manager.py:147-154): version v+1 is
+ * pulled into a second (shadow) arena on the instance's copy stream while v
+ * keeps serving, and swapped in at the step boundary (manager.begin_step,
+ * manager.py:416-426) with no pull stall.
+ *   rlb_shadow_arena   shadow arena pointer + bytes (allocated on first use;
+ *                      the target of external fan-out / IPC / NCCL pulls)
+ *   rlb_load_shadow    fused re-layout copy of HF tensors into the shadow,
+ *                      enqueued on the copy stream; returns immediately
+ *   rlb_mark_shadow    the shadow was filled externally by work enqueued on
+ *                      `stream` (NULL = legacy default stream) with `version`
+ *   rlb_shadow_status  state 0 empty / 1 copy in flight / 2 filled; seconds =
+ *                      device time of an rlb_load_shadow copy once filled
+ *   rlb_swap_weights   step boundary (no requests on the instance, else
+ *                      RLB_ERR_STATE): the shadow becomes the active set (the
+ *                      compute stream waits for its copy on the device), the
+ *                      old set becomes the empty shadow; out = active version */
+int rlb_shadow_arena(rlb_instance* h, void** arena, int64_t* bytes);
+int rlb_load_shadow(rlb_instance* h, const void* const* hf_ptrs, int32_t n_tensors,
+                    uint64_t version);
+int rlb_mark_shadow(rlb_instance* h, uint64_t version, void* stream);
+int rlb_shadow_status(rlb_instance* h, uint64_t* version, int32_t* state, double* seconds);
+int rlb_swap_weights(rlb_instance* h, uint64_t* version);
 /* Stand-alone fused re-layout copy on `device` (stream 0 if stream==NULL). */
 int rlb_relayout_copy(int device, const rlb_model_cfg* model, const void* const* hf_ptrs,
                       int32_t n_tensors, void* dst_arena, void* stream);

@@ -111,6 +111,14 @@ _SIGS = {
     "rlb_status": (ctypes.c_int, [_P, ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_int32),
                                   ctypes.POINTER(ctypes.c_uint64)]),
     "rlb_score": (ctypes.c_int, [_P, _P, ctypes.c_int32, _P]),
+    "rlb_shadow_arena": (ctypes.c_int, [_P, ctypes.POINTER(ctypes.c_void_p),
+                                        ctypes.POINTER(ctypes.c_int64)]),
+    "rlb_load_shadow": (ctypes.c_int, [_P, _P, ctypes.c_int32, ctypes.c_uint64]),
+    "rlb_mark_shadow": (ctypes.c_int, [_P, ctypes.c_uint64, _P]),
+    "rlb_shadow_status": (ctypes.c_int, [_P, ctypes.POINTER(ctypes.c_uint64),
+                                         ctypes.POINTER(ctypes.c_int32),
+                                         ctypes.POINTER(ctypes.c_double)]),
+    "rlb_swap_weights": (ctypes.c_int, [_P, ctypes.POINTER(ctypes.c_uint64)]),
     "rlb_bench_gemm": (ctypes.c_int, [ctypes.c_int] + [ctypes.c_int32] * 8 +
                        [ctypes.POINTER(ctypes.c_double)]),
     "rlb_gemm": (ctypes.c_int, [ctypes.c_int, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, _P, _P,

@@ -113,6 +113,32 @@ struct rlb_instance {
   bf16 *embed = nullptr, *norm = nullptr, *lm_head = nullptr;
   std::vector<LayerW> L;
   CUtensorMap m_lm;
+  // double-buffered weights: version v+1 is pulled into
+  // the shadow arena on the copy stream while v serves; rlb_swap_weights
+  // exchanges the two sets at a step boundary.
+  struct WeightSet {
+    uint8_t* arena = nullptr;
+    uint64_t version = 0;
+    bool has = false;
+    bf16 *embed = nullptr, *norm = nullptr, *lm_head = nullptr;
+    std::vector<LayerW> L;
+    CUtensorMap m_lm;
+  } shadow;
+  int shadow_state = 0;               // 0 empty, 1 copy enqueued, 2 filled
+  bool shadow_timed = false;          // ev_s0/ev_s1 bracket an internal copy
+  cudaStream_t st_copy = nullptr;
+  cudaEvent_t ev_shadow = nullptr, ev_s0 = nullptr, ev_s1 = nullptr;
+  void swap_sets() {
+    std::swap(arena, shadow.arena);
+    std::swap(version, shadow.version);
+    std::swap(has_weights, shadow.has);
+    std::swap(embed, shadow.embed);
+    std::swap(norm, shadow.norm);
+    std::swap(lm_head, shadow.lm_head);
+    std::swap(L, shadow.L);
+    std::swap(m_lm, shadow.m_lm);
+  }
+  int ensure_shadow();
   // KV
   bf16* kv = nullptr;
   size_t layer_stride = 0;  // elements
@@ -141,7 +167,8 @@ struct rlb_instance {
   std::deque<Req*> pending;
   std::unordered_map<uint64_t, Req*> reqs;
   std::vector<int> dec_list;
-  std::map<int, cudaGraphExec_t> graphs;
+  // decode graphs per (rows, weight arena): kernel parameters hold the arena
+  std::map<std::pair<int, const uint8_t*>, cudaGraphExec_t> graphs;
   int graph_built_for_version = -1;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr, evA = nullptr, evB = nullptr;
   rlb_stats stats{};
@@ -198,6 +225,13 @@ rlb_instance::~rlb_instance() {
                   d_part};
   for (void* b : bufs)
     if (b) cudaFree(b);
+  if (shadow.arena) cudaFree(shadow.arena);
+  if (st_copy) {
+    cudaStreamSynchronize(st_copy);
+    cudaStreamDestroy(st_copy);
+  }
+  for (cudaEvent_t ev : {ev_shadow, ev_s0, ev_s1})
+    if (ev) cudaEventDestroy(ev);
   if (h_stage) cudaFreeHost(h_stage);
   if (h_ring) cudaFreeHost(h_ring);
   if (ev0) cudaEventDestroy(ev0);
@@ -370,6 +404,25 @@ int rlb_instance::bind_arena() {
   lm_head = m.tied ? embed : put(static_cast<int64_t>(V) * H);
   RLB_CHECK(off == arena_bytes, RLB_ERR_STATE, "arena carve mismatch");
   return make_kmajor_map(&m_lm, lm_head, V, H, BN_LM);
+}
+
+// Allocate and carve the shadow arena on first use (bind_arena works on the
+// active members, so the sets are swapped around it).
+int rlb_instance::ensure_shadow() {
+  if (shadow.arena) return RLB_OK;
+  uint8_t* a = nullptr;
+  int rc;
+  if ((rc = dalloc(&a, arena_bytes))) return rc;
+  RLB_CUDA(cudaMemset(a, 0, arena_bytes));
+  RLB_CUDA(cudaStreamCreateWithFlags(&st_copy, cudaStreamNonBlocking));
+  RLB_CUDA(cudaEventCreateWithFlags(&ev_shadow, cudaEventDisableTiming));
+  RLB_CUDA(cudaEventCreate(&ev_s0));
+  RLB_CUDA(cudaEventCreate(&ev_s1));
+  shadow.arena = a;
+  swap_sets();
+  rc = bind_arena();
+  swap_sets();
+  return rc;
 }
 
 int rlb_instance::forward_layers(int R) {
@@ -613,7 +666,8 @@ int rlb_instance::run_decode(int steps, int* steps_run) {
       stats.decode_rows += static_cast<int64_t>(k) * R;
       stats.kernel_launches += k * per_step;
       if (gs > 0 && burst >= gs) {
-        auto it = graphs.find(R);
+        const auto gkey = std::make_pair(R, static_cast<const uint8_t*>(arena));
+        auto it = graphs.find(gkey);
         if (it == graphs.end()) {
           cudaGraph_t g;
           RLB_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
@@ -626,7 +680,7 @@ int rlb_instance::run_decode(int steps, int* steps_run) {
           cudaGraphExec_t ge;
           RLB_CUDA(cudaGraphInstantiate(&ge, g, 0));
           RLB_CUDA(cudaGraphDestroy(g));
-          it = graphs.emplace(R, ge).first;
+          it = graphs.emplace(gkey, ge).first;
         }
         RLB_CUDA(cudaGraphLaunch(it->second, st));
         burst -= gs;
@@ -769,6 +823,93 @@ int rlb_mark_weights(rlb_instance* h, uint64_t version) {
             "weight version " + std::to_string(version) + " < " + std::to_string(h->version));
   h->version = version;
   h->has_weights = true;
+  return RLB_OK;
+}
+
+// ---- double-buffered weights ---------------------------------------------
+
+int rlb_shadow_arena(rlb_instance* h, void** arena, int64_t* bytes) {
+  RLB_CHECK(h, RLB_ERR_ARG, "null handle");
+  RLB_CUDA(cudaSetDevice(h->device));
+  int rc = h->ensure_shadow();
+  if (rc) return rc;
+  if (arena) *arena = h->shadow.arena;
+  if (bytes) *bytes = h->arena_bytes;
+  return RLB_OK;
+}
+
+int rlb_load_shadow(rlb_instance* h, const void* const* hf_ptrs, int32_t n_tensors,
+                    uint64_t version) {
+  RLB_CHECK(h && hf_ptrs, RLB_ERR_ARG, "null argument");
+  RLB_CHECK(!h->has_weights || version >= h->version, RLB_ERR_ARG,
+            "weight version " + std::to_string(version) + " < " + std::to_string(h->version));
+  RLB_CUDA(cudaSetDevice(h->device));
+  int rc = h->ensure_shadow();
+  if (rc) return rc;
+  // the previous fill of this arena (if any) and every decode step that read
+  // it as the active set are ordered before the overwrite
+  RLB_CUDA(cudaEventRecord(h->ev_shadow, h->st));
+  RLB_CUDA(cudaStreamWaitEvent(h->st_copy, h->ev_shadow, 0));
+  RLB_CUDA(cudaEventRecord(h->ev_s0, h->st_copy));
+  if ((rc = relayout_copy(h->m, hf_ptrs, n_tensors, h->shadow.arena, h->st_copy))) return rc;
+  RLB_CUDA(cudaEventRecord(h->ev_s1, h->st_copy));
+  RLB_CUDA(cudaEventRecord(h->ev_shadow, h->st_copy));
+  h->shadow.version = version;
+  h->shadow.has = true;
+  h->shadow_state = 1;
+  h->shadow_timed = true;
+  return RLB_OK;
+}
+
+int rlb_mark_shadow(rlb_instance* h, uint64_t version, void* stream) {
+  RLB_CHECK(h, RLB_ERR_ARG, "null handle");
+  RLB_CHECK(h->shadow.arena, RLB_ERR_STATE, "no shadow arena (rlb_shadow_arena first)");
+  RLB_CHECK(!h->has_weights || version >= h->version, RLB_ERR_ARG,
+            "weight version " + std::to_string(version) + " < " + std::to_string(h->version));
+  RLB_CUDA(cudaSetDevice(h->device));
+  RLB_CUDA(cudaEventRecord(h->ev_shadow, static_cast<cudaStream_t>(stream)));
+  h->shadow.version = version;
+  h->shadow.has = true;
+  h->shadow_state = 1;
+  h->shadow_timed = false;
+  return RLB_OK;
+}
+
+int rlb_shadow_status(rlb_instance* h, uint64_t* version, int32_t* state, double* seconds) {
+  RLB_CHECK(h, RLB_ERR_ARG, "null handle");
+  if (h->shadow_state == 1) {
+    RLB_CUDA(cudaSetDevice(h->device));
+    const cudaError_t q = cudaEventQuery(h->ev_shadow);
+    if (q == cudaSuccess) h->shadow_state = 2;
+    else if (q != cudaErrorNotReady) RLB_CUDA(q);
+  }
+  if (version) *version = h->shadow.version;
+  if (state) *state = h->shadow_state;
+  if (seconds) {
+    *seconds = 0.0;
+    if (h->shadow_state == 2 && h->shadow_timed) {
+      float ms = 0.f;
+      RLB_CUDA(cudaEventElapsedTime(&ms, h->ev_s0, h->ev_s1));
+      *seconds = ms * 1e-3;
+    }
+  }
+  return RLB_OK;
+}
+
+int rlb_swap_weights(rlb_instance* h, uint64_t* version) {
+  RLB_CHECK(h, RLB_ERR_ARG, "null handle");
+  RLB_CHECK(h->shadow.has && h->shadow_state > 0, RLB_ERR_STATE, "shadow arena holds no weights");
+  RLB_CHECK(h->reqs.empty(), RLB_ERR_STATE,
+            "weights swap only at a step boundary (" + std::to_string(h->reqs.size()) +
+                " requests on the instance)");
+  RLB_CUDA(cudaSetDevice(h->device));
+  // the copy finishes before any later kernel on the compute stream runs;
+  // the host does not wait
+  RLB_CUDA(cudaStreamWaitEvent(h->st, h->ev_shadow, 0));
+  h->swap_sets();
+  h->shadow.has = false;              // the old set is free for the next pull
+  h->shadow_state = 0;
+  if (version) *version = h->version;
   return RLB_OK;
 }
 

@@ -111,6 +111,51 @@ class RolloutInstance:
         check(_lib.lib().rlb_weights_arena(self._h, ctypes.byref(p), ctypes.byref(n)))
         return int(p.value or 0), int(n.value)
 
+    # -- double-buffered weights -------------------------
+
+    def shadow_arena(self) -> tuple[int, int]:
+        """Device pointer + bytes of the second weight arena (allocated on
+        first use): the target of a pull that must not disturb serving."""
+        p, n = ctypes.c_void_p(), ctypes.c_int64()
+        check(_lib.lib().rlb_shadow_arena(self._h, ctypes.byref(p), ctypes.byref(n)))
+        return int(p.value or 0), int(n.value)
+
+    def pull_shadow(self, hf_weights, version: int) -> None:
+        """Start pulling `version` into the shadow arena (fused re-layout on the
+        copy stream); returns at once while the active weights keep serving."""
+        if isinstance(hf_weights, dict):
+            ptrs = [int(hf_weights[name].data_ptr()) for name, _ in hf_manifest(self.shape)]
+        else:
+            ptrs = [int(p) for p in hf_weights]
+        arr = (ctypes.c_void_p * len(ptrs))(*ptrs)
+        check(_lib.lib().rlb_load_shadow(self._h, arr, len(ptrs), version))
+
+    @property
+    def pull_bytes(self) -> int:
+        """Bytes one pull moves (the HF tensors of the weight set)."""
+        return sum(2 * int(np.prod(shape)) for _, shape in hf_manifest(self.shape))
+
+    def mark_shadow(self, version: int, stream: int | None = None) -> None:
+        """The shadow arena was filled externally by work on `stream`."""
+        check(_lib.lib().rlb_mark_shadow(self._h, version, stream))
+
+    SHADOW_STATES = ("empty", "pulling", "ready")
+
+    def shadow_status(self) -> tuple[int, str, float]:
+        """(version, 'empty'|'pulling'|'ready', device seconds of the copy)."""
+        v, st, sec = ctypes.c_uint64(), ctypes.c_int32(), ctypes.c_double()
+        check(_lib.lib().rlb_shadow_status(self._h, ctypes.byref(v), ctypes.byref(st),
+                                           ctypes.byref(sec)))
+        return int(v.value), self.SHADOW_STATES[st.value], float(sec.value)
+
+    def swap_weights(self) -> int:
+        """Step boundary: the shadow set becomes active (no host wait; the next
+        decode kernels wait for its copy on the device).  Raises
+        RlbStateError if requests are still on the instance."""
+        v = ctypes.c_uint64()
+        check(_lib.lib().rlb_swap_weights(self._h, ctypes.byref(v)))
+        return int(v.value)
+
     # -- requests ----------------------------------------------------------
 
     def _key(self, request_id: str, create: bool) -> int:

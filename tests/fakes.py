@@ -41,6 +41,26 @@ class FakeInstance:
 
     load_weights = pull_weights
 
+    # double-buffered weights (RolloutInstance.pull_shadow / swap_weights)
+    shadow_version, shadow_state = 0, "empty"
+
+    def pull_shadow(self, source, version):
+        self.shadow_version, self.shadow_state = version, "ready"
+
+    def shadow_status(self):
+        return self.shadow_version, self.shadow_state, 1e-3
+
+    def swap_weights(self):
+        if self.active:
+            from paper_2510_19225_b200._lib import RlbStateError
+            raise RlbStateError("weights swap only at a step boundary")
+        if self.shadow_state == "empty":
+            from paper_2510_19225_b200._lib import RlbStateError
+            raise RlbStateError("shadow arena holds no weights")
+        self.version, self.shadow_version = self.shadow_version, self.version
+        self.shadow_state = "empty"
+        return self.version
+
     def generate(self, request_id, prompt_tokens, prefix_tokens=(), *, target_len):
         if request_id in self.active or request_id in self.pending:
             raise ValueError(f"duplicate request {request_id!r}")

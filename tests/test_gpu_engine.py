@@ -142,3 +142,53 @@ def test_pull_bytewise(mid):
         src = w[names[hf]].contiguous().view(torch.uint8).flatten()
         expect[do:do + nb] = src[so:so + nb]
     assert torch.equal(arena, expect)
+
+
+def test_shadow_pull_while_serving_then_swap(tiny):
+    """Double-buffered weights: pulling v2 into the shadow
+    arena during a v1 rollout leaves that rollout bit-identical; after the
+    swap the instance generates exactly what a fresh v2 instance does; a
+    second swap (v3 into the old arena) works with the per-arena graphs."""
+    from paper_2510_19225_b200._lib import RlbStateError
+    w1, _ = tiny
+    w2 = synth_hf_weights(TINY, seed=1, device="cuda")
+    w3 = synth_hf_weights(TINY, seed=2, device="cuda")
+    prompts = synth_prompts(24, TINY.vocab, 16, 48, seed=9)
+    ref = {}
+    for v, w in ((1, w1), (2, w2), (3, w3)):
+        ref[v] = _rollout(_instance(TINY, w, max_slots=32, max_seq_len=256), prompts, 80)
+    assert ref[1] != ref[2]
+    inst = _instance(TINY, w1, max_slots=32, max_seq_len=256)
+    for i, p in enumerate(prompts):
+        inst.generate(f"r{i}", p, target_len=80)
+    got = {}
+    for rid, toks, _ in inst.step(16):
+        got.setdefault(rid, []).extend(toks.tolist())
+    inst.pull_shadow(w2, version=2)            # in flight while v1 serves
+    with pytest.raises(RlbStateError):
+        inst.swap_weights()                    # requests still on the instance
+    for rid, toks in inst.run_to_completion().items():
+        got.setdefault(rid, []).extend(toks)
+    assert [got[f"r{i}"] for i in range(len(prompts))] == ref[1]
+    v, state, sec = inst.shadow_status()
+    assert v == 2 and state == "ready" and sec > 0
+    assert inst.swap_weights() == 2 and inst.status()["weight_version"] == 2
+    assert inst.shadow_status()[1] == "empty"
+    assert _rollout(inst, prompts, 80) == ref[2]
+    inst.pull_shadow(w3, version=3)
+    assert inst.swap_weights() == 3            # no host wait: ordered on the device
+    assert _rollout(inst, prompts, 80) == ref[3]
+    # the shadow arena matches the fused re-layout bytewise
+    from paper_2510_19225_b200 import _lib
+    a_ptr, nbytes = inst.shadow_arena()
+    inst.pull_shadow(w1, version=4)
+    while inst.shadow_status()[1] != "ready":
+        pass
+    act = _instance(TINY, w1, max_slots=8, max_seq_len=256)
+    p_act, n_act = act.arena()
+    assert n_act == nbytes
+    bufs = [torch.empty(nbytes, dtype=torch.uint8, device="cuda") for _ in range(2)]
+    for buf, src in zip(bufs, (a_ptr, p_act)):
+        _lib.check(_lib.lib().rlb_copy_bytes(0, buf.data_ptr(), src, nbytes, None))
+    torch.cuda.synchronize()
+    assert torch.equal(bufs[0], bufs[1])

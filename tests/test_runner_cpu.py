@@ -61,3 +61,57 @@ def test_recompute_policy_regenerates_from_scratch():
     preempt_outs = [r for r in recs if r["type"] == "migrate_out" and r["reason"] == "preempt"]
     assert preempt_outs and all(r["kept_tokens"] == 0 for r in preempt_outs)
     run.close()
+
+
+def test_step_boundary_swap_has_no_pull_window():
+    """Version 2 is pulled into every instance's shadow arena while version 1
+    still serves; begin_step(2) swaps it in and the instances are Active at 2
+    immediately (no pull between step_start and instance_active)."""
+    run = make_runner(n_inst=3)
+    m, pool = run.manager, run.pool
+    ps = prompts(18, seed=5)
+    for k, p in enumerate(ps):
+        run.submit(f"a{k}", p, target_len=20)
+    run.pump()
+    run.advance()
+    pool.stage(2, source={"weights": "v2"}, now=run.now())
+    assert run.prefetch(2) == ["i0", "i1", "i2"]
+    assert all(m.records[i].status.value == "active" and m.records[i].weight_version == 1
+               for i in run.instances)
+    run.run()                                  # step 1 finishes on version 1
+    assert m.all_generated()
+    out = run.begin_step(2)
+    assert all(v["swapped"] for v in out.values()) and len(out) == 3
+    assert all(m.records[i].weight_version == 2 for i in run.instances)
+    assert all(inst.version == 2 for inst in run.instances.values())
+    recs = m.log.records
+    t_step = [r for r in recs if r["type"] == "step_start" and r["version"] == 2][0]["t"]
+    swaps = [r for r in recs if r["type"] == "pull_done" and r.get("swapped")]
+    assert len(swaps) == 3 and all(r["t"] >= t_step for r in swaps)
+    for k, p in enumerate(prompts(12, seed=6)):
+        run.submit(f"b{k}", p, target_len=15)
+    run.run()
+    assert assert_version_gating(m.log.records) > 0
+    assert assert_token_conservation(m.log.records) == 30
+    run.close()
+
+
+def test_begin_step_without_prefetch_pulls_blocking():
+    run = make_runner(n_inst=2)
+    for k, p in enumerate(prompts(4, seed=7)):
+        run.submit(f"a{k}", p, target_len=8)
+    run.run()
+    run.pool.stage(2, source={"weights": "v2"}, now=run.now())
+    out = run.begin_step(2)
+    assert out and not any(v["swapped"] for v in out.values())
+    assert all(run.manager.records[i].weight_version == 2 for i in run.instances)
+    run.close()
+
+
+def test_swap_refused_with_requests_in_flight():
+    from paper_2510_19225_b200._lib import RlbStateError
+    inst = FakeInstance()
+    inst.pull_shadow(None, 2)
+    inst.generate("r", [1, 2, 3], target_len=4)
+    with pytest.raises(RlbStateError):
+        inst.swap_weights()
