@@ -198,6 +198,15 @@ typedef struct {
   int64_t d2h_bytes;
 } rlb_stats;
 int rlb_get_stats(rlb_instance* h, rlb_stats* out, int32_t reset);
+/* Measured decode profile (replaces the modelled
+ * instance_throughput + profile_acc capture of _refresh_rate,
+ * pkg/src/spotrl/sim/engine.py:786-802, and _finalize_profile, :928-939):
+ * per batch size b (rows of a decode step), the decode steps run, their
+ * device seconds (CUDA events around every constant-batch burst) and the mean
+ * context length.  decode throughput = b * steps / seconds tokens/s.  Arrays
+ * of `cap` entries (NULL arrays: count only); ascending batch size. */
+int rlb_decode_profile(rlb_instance* h, int32_t cap, int32_t* batch, int64_t* steps,
+                       double* seconds, double* ctx_mean, int32_t* n_out, int32_t reset);
 /* Re-launch one kernel of the last decode step `iters` times on the instance
  * stream (rows, KV and weights as that step left them) and time it with CUDA
  * events.  which: 0 attention (layer 0), 1 gate_up GEMM, 2 down GEMM (+ fused

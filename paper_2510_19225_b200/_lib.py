@@ -119,6 +119,8 @@ _SIGS = {
                                          ctypes.POINTER(ctypes.c_int32),
                                          ctypes.POINTER(ctypes.c_double)]),
     "rlb_swap_weights": (ctypes.c_int, [_P, ctypes.POINTER(ctypes.c_uint64)]),
+    "rlb_decode_profile": (ctypes.c_int, [_P, ctypes.c_int32, _P, _P, _P, _P,
+                                          ctypes.POINTER(ctypes.c_int32), ctypes.c_int32]),
     "rlb_bench_gemm": (ctypes.c_int, [ctypes.c_int] + [ctypes.c_int32] * 8 +
                        [ctypes.POINTER(ctypes.c_double)]),
     "rlb_gemm": (ctypes.c_int, [ctypes.c_int, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, _P, _P,

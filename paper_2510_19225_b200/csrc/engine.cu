@@ -171,6 +171,44 @@ struct rlb_instance {
   std::map<std::pair<int, const uint8_t*>, cudaGraphExec_t> graphs;
   int graph_built_for_version = -1;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr, evA = nullptr, evB = nullptr;
+  // measured decode profile: device time per batch size,
+  // from CUDA events around every constant-batch burst of decode steps
+  struct ProfAcc {
+    int64_t steps = 0;
+    double ms = 0.0, ctx_sum = 0.0;   // ctx_sum: sum over steps of the mean context
+  };
+  std::map<int, ProfAcc> prof;
+  struct Burst {
+    int R, steps;
+    double ctx;
+    size_t e0, e1;
+  };
+  std::vector<Burst> bursts;
+  std::vector<cudaEvent_t> burst_ev;
+  size_t n_burst_ev = 0;
+  int burst_event(size_t* idx) {
+    if (n_burst_ev == burst_ev.size()) {
+      cudaEvent_t e;
+      RLB_CUDA(cudaEventCreate(&e));
+      burst_ev.push_back(e);
+    }
+    *idx = n_burst_ev++;
+    RLB_CUDA(cudaEventRecord(burst_ev[*idx], st));
+    return RLB_OK;
+  }
+  int collect_bursts() {   // after the stream has been synchronized
+    for (const Burst& b : bursts) {
+      float ms = 0.f;
+      RLB_CUDA(cudaEventElapsedTime(&ms, burst_ev[b.e0], burst_ev[b.e1]));
+      ProfAcc& a = prof[b.R];
+      a.steps += b.steps;
+      a.ms += ms;
+      a.ctx_sum += b.ctx * b.steps;
+    }
+    bursts.clear();
+    n_burst_ev = 0;
+    return RLB_OK;
+  }
   rlb_stats stats{};
   int last_R = 0;  // rows of the last decode step (for rlb_profile_kernel)
   // split-K factors of the small-N projections: a property of the model
@@ -232,6 +270,7 @@ rlb_instance::~rlb_instance() {
   }
   for (cudaEvent_t ev : {ev_shadow, ev_s0, ev_s1})
     if (ev) cudaEventDestroy(ev);
+  for (cudaEvent_t ev : burst_ev) cudaEventDestroy(ev);
   if (h_stage) cudaFreeHost(h_stage);
   if (h_ring) cudaFreeHost(h_ring);
   if (ev0) cudaEventDestroy(ev0);
@@ -660,6 +699,10 @@ int rlb_instance::run_decode(int steps, int* steps_run) {
     int burst = std::min(steps - *steps_run, min_left);
     const int gs = e.graph_steps;
     const int64_t per_step = 1 + launches_per_forward(R);
+    double ctx0 = 0.0;
+    for (int s : dec_list) ctx0 += h_seq_len[s];
+    Burst rec{R, burst, ctx0 / R + 0.5 * (burst - 1), 0, 0};
+    if ((rc = burst_event(&rec.e0))) return rc;
     while (burst > 0) {
       const int k = (gs > 0 && burst >= gs) ? gs : 1;
       stats.decode_steps += k;
@@ -693,6 +736,8 @@ int rlb_instance::run_decode(int steps, int* steps_run) {
         for (int s : dec_list) h_seq_len[s] += 1;
       }
     }
+    if ((rc = burst_event(&rec.e1))) return rc;
+    bursts.push_back(rec);
   }
   return RLB_OK;
 }
@@ -966,6 +1011,7 @@ int rlb_step(rlb_instance* h, int32_t n_steps, rlb_token_batch* out) {
   if ((rc = h->run_decode(std::min<int>(std::max(n_steps, 0), max_steps), &steps))) return rc;
   RLB_CUDA(cudaEventRecord(h->ev1, h->st));
   if ((rc = h->flush(out))) return rc;
+  if ((rc = h->collect_bursts())) return rc;
   float ms_pre = 0.f, ms_dec = 0.f;
   RLB_CUDA(cudaEventElapsedTime(&ms_pre, h->evA, h->evB));
   RLB_CUDA(cudaEventElapsedTime(&ms_dec, h->evB, h->ev1));
@@ -975,6 +1021,25 @@ int rlb_step(rlb_instance* h, int32_t n_steps, rlb_token_batch* out) {
     out->steps_run = steps;
     out->prefill_rows = rows;
   }
+  return RLB_OK;
+}
+
+int rlb_decode_profile(rlb_instance* h, int32_t cap, int32_t* batch, int64_t* steps,
+                       double* seconds, double* ctx_mean, int32_t* n_out, int32_t reset) {
+  RLB_CHECK(h && n_out, RLB_ERR_ARG, "null argument");
+  const int n = static_cast<int>(h->prof.size());
+  RLB_CHECK(n <= cap || !(batch || steps || seconds || ctx_mean), RLB_ERR_CAPACITY,
+            "decode profile has " + std::to_string(n) + " batch sizes");
+  int i = 0;
+  for (const auto& kv : h->prof) {
+    if (batch) batch[i] = kv.first;
+    if (steps) steps[i] = kv.second.steps;
+    if (seconds) seconds[i] = kv.second.ms * 1e-3;
+    if (ctx_mean) ctx_mean[i] = kv.second.steps ? kv.second.ctx_sum / kv.second.steps : 0.0;
+    ++i;
+  }
+  *n_out = n;
+  if (reset) h->prof.clear();
   return RLB_OK;
 }
 

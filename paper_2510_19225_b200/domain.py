@@ -95,3 +95,26 @@ class InstanceRecord:
                 f"{self.instance_id}: weight version {version} < {self.weight_version}"
             )
         self.weight_version = version
+
+
+@dataclass(frozen=True)
+class ProfileEntry:
+    """One point of the batch-size -> decode-throughput curve
+    (`pkg/src/spotrl/domain.py:130-133`); tokens/sec of the whole instance."""
+
+    batch_size: int
+    decode_throughput: float
+
+
+@dataclass
+class ProfileTable:
+    """Online decode profile (`pkg/src/spotrl/domain.py:136-148`).  On B200 it
+    is built from measured device time per batch size
+    (`RolloutInstance.decode_profile`, `profile.measured_profile_table`);
+    `context_calibration` is the mean context length the points were taken at."""
+
+    entries: list[ProfileEntry] = field(default_factory=list)
+    context_calibration: float = 0.0
+
+    def distinct_batch_sizes(self) -> int:
+        return len({e.batch_size for e in self.entries})

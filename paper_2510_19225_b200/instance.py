@@ -277,6 +277,19 @@ class RolloutInstance:
         check(_lib.lib().rlb_get_stats(self._h, ctypes.byref(s), int(reset)))
         return s.as_dict()
 
+    def decode_profile(self, reset: bool = False) -> list[tuple[int, int, float, float]]:
+        """Measured decode profile: (batch size, decode steps, device seconds,
+        mean context) per batch size seen so far (`rlb_decode_profile`)."""
+        n = ctypes.c_int32()
+        lib = _lib.lib()
+        check(lib.rlb_decode_profile(self._h, 0, None, None, None, None, ctypes.byref(n), 0))
+        k = max(n.value, 1)
+        b, st = np.zeros(k, np.int32), np.zeros(k, np.int64)
+        sec, ctx = np.zeros(k, np.float64), np.zeros(k, np.float64)
+        check(lib.rlb_decode_profile(self._h, k, ptr(b), ptr(st), ptr(sec), ptr(ctx),
+                                     ctypes.byref(n), int(reset)))
+        return [(int(b[i]), int(st[i]), float(sec[i]), float(ctx[i])) for i in range(n.value)]
+
     def profile_kernel(self, name: str, iters: int = 20) -> tuple[float, float]:
         """(avg launch ms, algorithmic bytes or FLOPs per launch) of one kernel of
         the last decode step, re-launched `iters` times and timed with CUDA events."""

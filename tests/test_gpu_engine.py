@@ -192,3 +192,27 @@ def test_shadow_pull_while_serving_then_swap(tiny):
         _lib.check(_lib.lib().rlb_copy_bytes(0, buf.data_ptr(), src, nbytes, None))
     torch.cuda.synchronize()
     assert torch.equal(bufs[0], bufs[1])
+
+
+def test_decode_profile_measured(tiny):
+    """rlb_decode_profile: per batch size, device-timed decode steps that add
+    up to the instance's decode accounting; it builds a ProfileTable the
+    plateau rule accepts."""
+    from paper_2510_19225_b200.profile import estimate_plateau, measured_profile_table
+    w, _ = tiny
+    prompts = synth_prompts(32, TINY.vocab, 16, 48, seed=12)
+    inst = _instance(TINY, w, max_slots=32, max_seq_len=256)
+    inst.stats(reset=True)
+    for i, p in enumerate(prompts):   # staggered targets: the batch shrinks as requests finish
+        inst.generate(f"r{i}", p, target_len=20 + 4 * i)
+    inst.run_to_completion(16)
+    prof = inst.decode_profile()
+    st = inst.stats()
+    assert sum(s for _, s, _, _ in prof) == st["decode_steps"]
+    assert sum(b * s for b, s, _, _ in prof) == st["decode_rows"]
+    assert len(prof) >= 8 and all(sec > 0 for _, _, sec, _ in prof)
+    assert all(16 <= ctx <= 256 for _, _, _, ctx in prof)
+    t = measured_profile_table(prof)
+    assert t.distinct_batch_sizes() == len(prof)
+    assert 1 <= estimate_plateau(t, t.context_calibration) <= 32
+    assert inst.decode_profile(reset=True) == prof and inst.decode_profile() == []
