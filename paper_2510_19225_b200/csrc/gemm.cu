@@ -377,23 +377,39 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   const uint32_t tmem = *tmem_slot;
   if (stamp && threadIdx.x == 0) p.dbg[1] = gtime();
   pdl_trigger();
-  pdl_wait();   // A (activations) is the previous kernel's output
+  // With programmatic dependent launch this CTA may start while the previous
+  // kernel drains.  The weights (B) do not depend on it: the producer issues
+  // the first stages' B tiles before waiting, then the A tiles after.  Every
+  // other thread waits first (A, h and the outputs belong to the chain).
+  const bool producer = warp == 0 && lane == 0;
+  const int pre = nk < C::STAGES ? nk : C::STAGES;
+  if (producer) {
+    for (int kb = 0; kb < pre; ++kb) {
+      uint8_t* st = smem + kb * C::STAGE_BYTES;
+      mbar_expect_tx(smem_u32(&full[kb]), C::STAGE_BYTES);
+      tma_load_2d(smem_u32(st + NACC * C::A_BYTES), &tmB, smem_u32(&full[kb]),
+                  (kb0 + kb) * BK, n_blk * BN);
+    }
+  }
+  pdl_wait();
   if (stamp && threadIdx.x == 0) p.dbg[2] = gtime();
 
   if (warp == 0) {
-    if (lane == 0) {
+    if (producer) {
       for (int kb = 0; kb < nk; ++kb) {
         const int s = kb % C::STAGES;
         const uint32_t ph = (kb / C::STAGES) & 1;
         uint8_t* st = smem + s * C::STAGE_BYTES;
-        mbar_wait(smem_u32(&empty[s]), ph ^ 1);
-        mbar_expect_tx(smem_u32(&full[s]), C::STAGE_BYTES);
         const int kx = (kb0 + kb) * BK;
+        if (kb >= pre) {
+          mbar_wait(smem_u32(&empty[s]), ph ^ 1);
+          mbar_expect_tx(smem_u32(&full[s]), C::STAGE_BYTES);
+          tma_load_2d(smem_u32(st + NACC * C::A_BYTES), &tmB, smem_u32(&full[s]), kx, n_blk * BN);
+        }
 #pragma unroll
         for (int a = 0; a < NACC; ++a)
           tma_load_2d(smem_u32(st + a * C::A_BYTES), &tmA, smem_u32(&full[s]), kx,
                       m_blk * BMT + a * HM);
-        tma_load_2d(smem_u32(st + NACC * C::A_BYTES), &tmB, smem_u32(&full[s]), kx, n_blk * BN);
       }
     }
   } else if (warp == 1) {
