@@ -66,11 +66,26 @@ struct Req {
 
 struct LayerW {
   bf16 *ln1, *wqkv, *bqkv, *wo, *ln2, *wgu, *wdown;
-  CUtensorMap m_qkv, m_o, m_gu, m_down;
+  CUtensorMap m_qkv, m_o, m_gu, m_gu_small, m_down;
 };
 
-// GEMM tile widths per projection (N-tile of the 128 x BN UMMA tile).
+// GEMM tile widths per projection (N-tile of the 128 x BN UMMA tile).  A
+// forward of at most SMALL_ROWS rows (the rollout tail) runs gate_up and
+// lm_head with 128-wide tiles instead: twice the CTAs for the same weight
+// stream.  The N tiling does not change any output bit (a row's K loop is
+// the same), so batch invariance holds across the switch.
 constexpr int BN_QKV = 128, BN_O = 128, BN_GU = 256, BN_DOWN = 128, BN_LM = 256;
+constexpr int BN_SMALL = 128;
+constexpr int SMALL_ROWS = 256;
+
+// Tile shape of each projection for a forward of R rows.  Measured on B200
+// (scripts/gemm_small_m.py): at <= 256 rows 128-row tiles (and for gate_up
+// 128-wide N tiles) win, because a 256-row tile half empty still streams the
+// same weights through half the CTAs; large prefill chunks want 256-row QKV
+// tiles.  None of these choices changes a bit of any row's result.
+struct TilePlan {
+  int bm_qkv, bm_o, bn_gu, bm_gu, bm_down;
+};
 constexpr int RING_ROWS = 512;
 
 // Split-K factor of an [N, K] projection: the largest divisor d of the K
@@ -113,7 +128,7 @@ struct rlb_instance {
   bool has_weights = false;
   bf16 *embed = nullptr, *norm = nullptr, *lm_head = nullptr;
   std::vector<LayerW> L;
-  CUtensorMap m_lm;
+  CUtensorMap m_lm, m_lm_small;
   // double-buffered weights: version v+1 is pulled into
   // the shadow arena on the copy stream while v serves; rlb_swap_weights
   // exchanges the two sets at a step boundary.
@@ -123,7 +138,7 @@ struct rlb_instance {
     bool has = false;
     bf16 *embed = nullptr, *norm = nullptr, *lm_head = nullptr;
     std::vector<LayerW> L;
-    CUtensorMap m_lm;
+    CUtensorMap m_lm, m_lm_small;
   } shadow;
   int shadow_state = 0;               // 0 empty, 1 copy enqueued, 2 filled
   bool shadow_timed = false;          // ev_s0/ev_s1 bracket an internal copy
@@ -138,6 +153,7 @@ struct rlb_instance {
     std::swap(lm_head, shadow.lm_head);
     std::swap(L, shadow.L);
     std::swap(m_lm, shadow.m_lm);
+    std::swap(m_lm_small, shadow.m_lm_small);
   }
   int ensure_shadow();
   // KV
@@ -219,7 +235,13 @@ struct rlb_instance {
   // rows per GEMM CTA: QKV uses 128-row tiles instead of split-K (twice the
   // CTAs, and its RoPE / KV-append epilogue runs straight from TMEM); the
   // others share each weight stage between two 128-row accumulators
-  int bm_qkv = 128, bm_o = 256, bm_gu = 256, bm_down = 256;
+  int bm_qkv = 128, bm_o = 256, bm_gu = 256, bm_down = 256;   // decode batch (> 256 rows)
+  TilePlan plan(int R) const {
+    if (R <= 128) return {128, 128, BN_SMALL, 128, 128};
+    if (R <= SMALL_ROWS) return {128, 128, BN_SMALL, 256, 128};
+    if (R > 512) return {256, bm_o, BN_GU, bm_gu, bm_down};
+    return {bm_qkv, bm_o, BN_GU, bm_gu, bm_down};
+  }
   // split-K O / down: sum the splits inside a cluster and add into h in the
   // GEMM epilogue (true), or write fp32 partials that the following RMSNorm
   // kernel sums in split order (false)
@@ -438,11 +460,13 @@ int rlb_instance::bind_arena() {
     if ((rc = make_kmajor_map(&w.m_qkv, w.wqkv, QKV, H, BN_QKV))) return rc;
     if ((rc = make_kmajor_map(&w.m_o, w.wo, H, NQ * D, BN_O))) return rc;
     if ((rc = make_kmajor_map(&w.m_gu, w.wgu, 2 * F, H, BN_GU))) return rc;
+    if ((rc = make_kmajor_map(&w.m_gu_small, w.wgu, 2 * F, H, BN_SMALL))) return rc;
     if ((rc = make_kmajor_map(&w.m_down, w.wdown, H, F, BN_DOWN))) return rc;
   }
   norm = put(H);
   lm_head = m.tied ? embed : put(static_cast<int64_t>(V) * H);
   RLB_CHECK(off == arena_bytes, RLB_ERR_STATE, "arena carve mismatch");
+  if ((rc = make_kmajor_map(&m_lm_small, lm_head, V, H, BN_SMALL))) return rc;
   return make_kmajor_map(&m_lm, lm_head, V, H, BN_LM);
 }
 
@@ -480,40 +504,43 @@ int rlb_instance::forward_layers(int R) {
   if ((rc = resid_norm_launch(d_h, nullptr, 0, R, nullptr, R, L[0].ln1, H, m.rms_eps, d_xn, false,
                               st)))
     return rc;
+  const TilePlan tp = plan(R);
   for (int l = 0; l < m.layers; ++l) {
     const LayerW& w = L[l];
     bf16* kv_l = kv + layer_stride * l;
     GemmParams pq{R, QKV, H, w.bqkv, nullptr, 0, sp_qkv, nullptr};
     pq.rope = RopeDst{d_row_slot, d_row_pos, d_rope, d_q, NQ * D, kv_l, d_bt, pps, NQ, NKV, D};
-    if ((rc = gemm_launch(m_xn, w.m_qkv, BN_QKV, EPI_ROPE, pq, st, bm_qkv))) return rc;
+    if ((rc = gemm_launch(m_xn, w.m_qkv, BN_QKV, EPI_ROPE, pq, st, tp.bm_qkv))) return rc;
     AttnArgs a{d_q, NQ * D, kv_l, d_bt, pps, d_row_slot, d_row_pos, R, NQ, NKV, D, max_splits,
                d_ws, d_attn, NQ * D};
     if ((rc = attention_launch(a, st))) return rc;
     if (cl_o) {
-      if ((rc = proj(m_attn, w.m_o, BN_O, sp_o, EPI_RESADD, R, H, NQ * D, nullptr, d_h, H, bm_o)) ||
+      if ((rc = proj(m_attn, w.m_o, BN_O, sp_o, EPI_RESADD, R, H, NQ * D, nullptr, d_h, H,
+                     tp.bm_o)) ||
           (rc = resid_norm_launch(d_h, nullptr, 0, R, nullptr, R, w.ln2, H, m.rms_eps, d_xn, false,
                                   st)))
         return rc;
     } else {
       if ((rc = proj(m_attn, w.m_o, BN_O, sp_o, EPI_PARTIAL, R, H, NQ * D, nullptr, nullptr, 0,
-                     bm_o)) ||
+                     tp.bm_o)) ||
           (rc = resid_norm_launch(d_h, d_part, sp_o, R, nullptr, R, w.ln2, H, m.rms_eps, d_xn, true,
                                   st)))
         return rc;
     }
-    if ((rc = proj(m_xn, w.m_gu, BN_GU, 1, EPI_SWIGLU, R, 2 * F, H, nullptr, d_act, F, bm_gu)))
+    if ((rc = proj(m_xn, tp.bn_gu == BN_SMALL ? w.m_gu_small : w.m_gu, tp.bn_gu, 1, EPI_SWIGLU,
+                   R, 2 * F, H, nullptr, d_act, F, tp.bm_gu)))
       return rc;
     const bool last = l + 1 == m.layers;
     if (cl_down) {
       if ((rc = proj(m_act, w.m_down, BN_DOWN, sp_down, EPI_RESADD, R, H, F, nullptr, d_h, H,
-                     bm_down)))
+                     tp.bm_down)))
         return rc;
       if (!last && (rc = resid_norm_launch(d_h, nullptr, 0, R, nullptr, R, L[l + 1].ln1, H,
                                            m.rms_eps, d_xn, false, st)))
         return rc;
     } else {
       if ((rc = proj(m_act, w.m_down, BN_DOWN, sp_down, EPI_PARTIAL, R, H, F, nullptr, nullptr, 0,
-                     bm_down)))
+                     tp.bm_down)))
         return rc;
       // the last layer's partials are summed by the head's norm (its rows only)
       if (!last && (rc = resid_norm_launch(d_h, d_part, sp_down, R, nullptr, R, L[l + 1].ln1, H,
@@ -541,8 +568,12 @@ int rlb_instance::head(int Lrows, bool append) {
                               d_logit_src, Lrows, norm, H, m.rms_eps, d_xn, false, st)))
     return rc;
   if (!append) return proj(m_xn, m_lm, BN_LM, 1, EPI_F32, Lrows, V, H, nullptr, d_logits, V);
-  const int ntiles = (V + BN_LM - 1) / BN_LM;
-  if ((rc = proj(m_xn, m_lm, BN_LM, 1, EPI_ARGMAX, Lrows, V, H, nullptr, d_logits, ntiles)))
+  // lm_head: 128 x 128 tiles between 33 and 128 rows (measured), else 256 x 256
+  const bool small = Lrows > 32 && Lrows <= 128;
+  const int bn = small ? BN_SMALL : BN_LM;
+  const int ntiles = (V + bn - 1) / bn;
+  if ((rc = proj(m_xn, small ? m_lm_small : m_lm, bn, 1, EPI_ARGMAX, Lrows, V, H, nullptr, d_logits,
+                 ntiles, small ? 128 : 256)))
     return rc;
   return argmax_append_launch(reinterpret_cast<const float2*>(d_logits), ntiles, Lrows,
                               d_logit_slot, d_seq_tokens, d_seq_len, d_seq_target, max_seq, d_ring,
@@ -1146,6 +1177,7 @@ int rlb_profile_kernel(rlb_instance* h, int32_t which, int32_t iters, double* av
   const LayerW& w = h->L[0];
   const int NQ = h->NQ, D = h->D, H = h->H, F = h->F;
   double work = 0.0;
+  const TilePlan tp = h->plan(R);
   auto launch = [&]() -> int {
     switch (which) {
       case 0: {
@@ -1157,19 +1189,19 @@ int rlb_profile_kernel(rlb_instance* h, int32_t which, int32_t iters, double* av
       // product writes state (fp32 h -> the partial workspace; qkv's K/V go
       // to the last layer's pages: timing only, the rollout that was
       // profiled is discarded)
-      case 1: return h->proj(h->m_xn, w.m_gu, BN_GU, 1, EPI_SWIGLU, R, 2 * F, H, nullptr,
-                             h->d_act, F, h->bm_gu);
+      case 1: return h->proj(h->m_xn, tp.bn_gu == BN_SMALL ? w.m_gu_small : w.m_gu, tp.bn_gu, 1,
+                             EPI_SWIGLU, R, 2 * F, H, nullptr, h->d_act, F, tp.bm_gu);
       case 2: return h->proj(h->m_act, w.m_down, BN_DOWN, h->sp_down,
                              h->cl_down ? EPI_RESADD : EPI_PARTIAL, R, H, F, nullptr, h->d_part, H,
-                             h->bm_down);
+                             tp.bm_down);
       case 3: {
         GemmParams pq{R, h->QKV, H, w.bqkv, nullptr, 0, h->sp_qkv, nullptr};
         pq.rope = RopeDst{h->d_row_slot, h->d_row_pos, h->d_rope, h->d_q, NQ * D, h->kv_scratch(),
                           h->d_bt, h->pps, NQ, h->NKV, D};
-        return gemm_launch(h->m_xn, w.m_qkv, BN_QKV, EPI_ROPE, pq, h->st, h->bm_qkv);
+        return gemm_launch(h->m_xn, w.m_qkv, BN_QKV, EPI_ROPE, pq, h->st, tp.bm_qkv);
       }
       case 4: return h->proj(h->m_attn, w.m_o, BN_O, h->sp_o, h->cl_o ? EPI_RESADD : EPI_PARTIAL,
-                             R, H, NQ * D, nullptr, h->d_part, H, h->bm_o);
+                             R, H, NQ * D, nullptr, h->d_part, H, tp.bm_o);
       case 5: return h->proj(h->m_xn, h->m_lm, BN_LM, 1, EPI_ARGMAX, R, h->V, H, nullptr,
                              h->d_logits, (h->V + BN_LM - 1) / BN_LM);
       case 6: return resid_norm_launch(h->d_h, h->cl_down ? nullptr : h->d_part,

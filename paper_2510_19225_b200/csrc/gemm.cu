@@ -359,6 +359,10 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   const int kb0 = blockIdx.z * nk;
   // split-K cluster epilogue (S > 1) or direct from TMEM (S == 1)
   const bool via_cluster = kClusterEpi && p.splits > 1;
+  // accumulators with at least one live row (a small-M tile skips the
+  // loads, MMAs and TMEM reads of the empty one)
+  const int live_acc = (NACC == 2 && p.M - m_blk * BMT > HM) ? 2 : 1;
+  const uint32_t stage_tx = static_cast<uint32_t>(live_acc * C::A_BYTES + C::B_BYTES);
 
   if (warp == 0 && lane == 0) {
     tma_prefetch(&tmA);
@@ -386,7 +390,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   if (producer) {
     for (int kb = 0; kb < pre; ++kb) {
       uint8_t* st = smem + kb * C::STAGE_BYTES;
-      mbar_expect_tx(smem_u32(&full[kb]), C::STAGE_BYTES);
+      mbar_expect_tx(smem_u32(&full[kb]), stage_tx);
       tma_load_2d(smem_u32(st + NACC * C::A_BYTES), &tmB, smem_u32(&full[kb]),
                   (kb0 + kb) * BK, n_blk * BN);
     }
@@ -403,13 +407,14 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         const int kx = (kb0 + kb) * BK;
         if (kb >= pre) {
           mbar_wait(smem_u32(&empty[s]), ph ^ 1);
-          mbar_expect_tx(smem_u32(&full[s]), C::STAGE_BYTES);
+          mbar_expect_tx(smem_u32(&full[s]), stage_tx);
           tma_load_2d(smem_u32(st + NACC * C::A_BYTES), &tmB, smem_u32(&full[s]), kx, n_blk * BN);
         }
 #pragma unroll
         for (int a = 0; a < NACC; ++a)
-          tma_load_2d(smem_u32(st + a * C::A_BYTES), &tmA, smem_u32(&full[s]), kx,
-                      m_blk * BMT + a * HM);
+          if (a < live_acc)
+            tma_load_2d(smem_u32(st + a * C::A_BYTES), &tmA, smem_u32(&full[s]), kx,
+                        m_blk * BMT + a * HM);
       }
     }
   } else if (warp == 1) {
@@ -427,8 +432,9 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           // +32 bytes per K=16 step inside the 128 B swizzle atom (encoded >> 4)
 #pragma unroll
           for (int a = 0; a < NACC; ++a)
-            umma_bf16(tmem + a * BN, umma_desc_sw128(st + a * C::A_BYTES) + 2 * k, bd + 2 * k,
-                      idesc, (kb | k) != 0);
+            if (a < live_acc)
+              umma_bf16(tmem + a * BN, umma_desc_sw128(st + a * C::A_BYTES) + 2 * k, bd + 2 * k,
+                        idesc, (kb | k) != 0);
         }
         umma_commit(smem_u32(&empty[s]));
       }
@@ -440,6 +446,9 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     const int q = warp & 3;                    // TMEM lane quadrant
     const int m = m_blk * BMT + half * HM + q * 32 + lane;
     const bool live = m < p.M;
+    // warp-uniform: no row of this warp exists -> no TMEM reads (tcgen05.ld is
+    // warp-collective, so the skip is per warp)
+    const bool warp_dead = m_blk * BMT + half * HM + q * 32 >= p.M;
     mbar_wait(smem_u32(tfull), 0);
     if (stamp && threadIdx.x == 128) p.dbg[4] = gtime();
     tc_fence_after();
@@ -447,7 +456,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     if constexpr (EPI == EPI_SWIGLU) {
       bf16* out = reinterpret_cast<bf16*>(p.out);
 #pragma unroll 1
-      for (int g = 0; g < BN / 128; ++g) {
+      for (int g = 0; g < (warp_dead ? 0 : BN / 128); ++g) {
 #pragma unroll 1
         for (int jc = 0; jc < 64; jc += 32) {
           uint32_t rg[32], ru[32];
@@ -476,7 +485,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       float best = -INFINITY;
       int bidx = 0x7fffffff;
 #pragma unroll 1
-      for (int c = 0; c < BN; c += 32) {
+      for (int c = 0; c < (warp_dead ? 0 : BN); c += 32) {
         uint32_t r[32];
         tmem_ld32(tbase + c, r);
         tmem_ld_wait();
@@ -500,7 +509,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         float* stage = reinterpret_cast<float*>(smem);
         const int row = half * HM + q * 32 + lane;
 #pragma unroll 1
-        for (int c = 0; c < BN; c += 32) {
+        for (int c = 0; c < (warp_dead ? 0 : BN); c += 32) {
           uint32_t r[32];
           tmem_ld32(tbase + c, r);
           tmem_ld_wait();
@@ -510,7 +519,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
             s4[i] = make_float4(__uint_as_float(r[4 * i]), __uint_as_float(r[4 * i + 1]),
                                 __uint_as_float(r[4 * i + 2]), __uint_as_float(r[4 * i + 3]));
         }
-      } else {
+      } else if (!warp_dead) {
         rope_direct(p, tbase, m, live, n_blk);
       }
     } else if constexpr ((EPI == EPI_PARTIAL || EPI == EPI_F32) && BN == 128) {
@@ -522,7 +531,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       float* stage = reinterpret_cast<float*>(smem);
       const int row = half * HM + q * 32 + lane;           // row within the CTA tile
 #pragma unroll 1
-      for (int c = 0; c < BN; c += 32) {
+      for (int c = 0; c < (warp_dead ? 0 : BN); c += 32) {
         uint32_t r[32];
         tmem_ld32(tbase + c, r);
         tmem_ld_wait();
@@ -553,7 +562,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
                                       : reinterpret_cast<float*>(p.out);
       const int ld = EPI == EPI_PARTIAL ? p.N : p.ldo;
 #pragma unroll 1
-      for (int c = 0; c < BN; c += 32) {
+      for (int c = 0; c < (warp_dead ? 0 : BN); c += 32) {
         uint32_t r[32];
         tmem_ld32(tbase + c, r);
         tmem_ld_wait();

@@ -10,6 +10,9 @@ CMD="python bench.py --steps 1 --warmup 1 --no-cpu-baseline"
 $CMD > $OUT/plain.json 2> $OUT/plain.err
 ncu --metrics gpu__time_duration.sum --clock-control none -s 150000 -c 600 --csv \
     --log-file $OUT/launches.csv $CMD > $OUT/ncu_launch.log 2>&1
+# prefill: the first launches of the first rollout (weight load + varlen prefill chunks)
+ncu --metrics gpu__time_duration.sum --clock-control none -c 2400 --csv \
+    --log-file $OUT/launches_prefill.csv $CMD > $OUT/ncu_launch_prefill.log 2>&1
 ncu --set full --clock-control none --import-source on -k regex:attn_mma -s 3000 -c 2 \
     -o $OUT/prof_attn $CMD > $OUT/ncu_attn.log 2>&1
 ncu --set full --clock-control none --import-source on -k regex:gemm_bf16 -s 4000 -c 5 \
