@@ -88,13 +88,20 @@ class RolloutInstance:
 
     # -- weights (pull) ----------------------------------------------------
 
+    def _source_ptrs(self, src) -> list[int]:
+        """HF tensor device pointers (`hf_manifest` order) of a weight source:
+        a name -> tensor dict, an object with `.ptrs` (TrainerWeights,
+        MappedSource, TcpPulledSource) or a pointer list."""
+        if isinstance(src, dict):
+            return [int(src[name].data_ptr()) for name, _ in hf_manifest(self.shape)]
+        if hasattr(src, "ptrs"):
+            return [int(p) for p in src.ptrs]
+        return [int(p) for p in src]
+
     def load_weights(self, hf_weights, version: int) -> PullResult:
         """Pull an HF-layout weight set (dict name -> CUDA tensor, or a list of
         device pointers in `hf_manifest` order) with the fused re-layout."""
-        if isinstance(hf_weights, dict):
-            ptrs = [int(hf_weights[name].data_ptr()) for name, _ in hf_manifest(self.shape)]
-        else:
-            ptrs = [int(p) for p in hf_weights]
+        ptrs = self._source_ptrs(hf_weights)
         arr = (ctypes.c_void_p * len(ptrs))(*ptrs)
         stats = _lib.PullStats()
         check(_lib.lib().rlb_load_weights(self._h, arr, len(ptrs), version, ctypes.byref(stats)))
@@ -123,10 +130,7 @@ class RolloutInstance:
     def pull_shadow(self, hf_weights, version: int) -> None:
         """Start pulling `version` into the shadow arena (fused re-layout on the
         copy stream); returns at once while the active weights keep serving."""
-        if isinstance(hf_weights, dict):
-            ptrs = [int(hf_weights[name].data_ptr()) for name, _ in hf_manifest(self.shape)]
-        else:
-            ptrs = [int(p) for p in hf_weights]
+        ptrs = self._source_ptrs(hf_weights)
         arr = (ctypes.c_void_p * len(ptrs))(*ptrs)
         check(_lib.lib().rlb_load_shadow(self._h, arr, len(ptrs), version))
 

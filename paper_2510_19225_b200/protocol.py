@@ -205,8 +205,10 @@ class InstanceAdapter:
         if kind == "pull_weights":
             if self._open_endpoint is None:
                 raise ProtocolError("no weight source resolver configured")
-            src = self._open_endpoint(message["agent_endpoint"])
+            src = self._open_endpoint(message["agent_endpoint"], message["version"])
             self.instance.pull_weights(src, message["version"])
+            if hasattr(src, "close"):
+                src.close()
             return [self.status()]
         raise ProtocolError(f"{kind} is not a manager->instance message")
 

@@ -1,0 +1,75 @@
+"""Live mode on CPU: the manager server and instance processes (threads here,
+fake instances) over TCP with the reference wire protocol; a connection drop
+is a preemption and the displaced requests resume elsewhere; weights pulled
+over W/D frames from an agent server."""
+import threading
+
+import pytest
+
+from oracle.audit import assert_token_conservation, assert_version_gating
+from paper_2510_19225_b200.events import EventLog
+from paper_2510_19225_b200.live import AgentServer, ManagerServer, serve_instance
+from paper_2510_19225_b200.manager import RolloutManager
+from paper_2510_19225_b200.protocol import ProtocolError, read_frames, write_pull_request
+from tests.fakes import FakeInstance, reference_continuation
+
+
+def _prompts(n):
+    import random
+    rng = random.Random(11)
+    return [[rng.randrange(997) for _ in range(rng.randint(2, 9))] for _ in range(n)]
+
+
+@pytest.mark.parametrize("die", [None, 40])
+def test_live_rollout_over_tcp(die):
+    m = RolloutManager(theta=3, log=EventLog())
+    m.n_prem_cap = 3
+    m.begin_step(1, 0.0)
+    srv = ManagerServer(m, version=1, endpoint_for=lambda iid: f"fake://{iid}", max_inflight=4)
+    prompts = _prompts(18)
+    for k, p in enumerate(prompts):
+        m.create_request(f"r{k}", len(p), 12 + k % 5, "g", 0.0, prompt_tokens=p)
+    stop = threading.Event()
+    threads = []
+    for k in range(3):
+        inst = FakeInstance(vocab=997, max_slots=4)
+        kw = {"die_after_tokens": die} if (die and k == 1) else {}
+        t = threading.Thread(target=serve_instance, args=(srv.address, inst, f"i{k}"),
+                             kwargs=dict(open_endpoint=lambda ep, v: ep, n_steps=3, stop=stop, **kw),
+                             daemon=True)
+        t.start()
+        threads.append(t)
+    srv.run_until_done(timeout=60)
+    stop.set()
+    srv.close()
+    recs = m.log.records
+    assert assert_token_conservation(recs) == 18
+    assert assert_version_gating(recs) > 0
+    probe = FakeInstance(vocab=997)
+    for k, p in enumerate(prompts):
+        assert m.requests[f"r{k}"].generated == reference_continuation(probe, p, 12 + k % 5)
+    preempts = [r for r in recs if r["type"] == "preempt"]
+    if die:
+        assert len(preempts) == 1 and preempts[0]["instance_id"] == "i1"
+        assert preempts[0]["displaced"] > 0       # they resumed on i0 / i2 (checked above)
+    else:
+        assert not preempts
+
+
+def test_agent_pull_frames():
+    agent = AgentServer(shard_bytes=1000)
+    blob = bytes(range(256)) * 30
+    agent.stage(3, blob)
+    import socket
+    host, port = agent.address
+    with socket.create_connection((host, port)) as s, s.makefile("rwb") as f:
+        write_pull_request(f, 3)
+        f.flush()
+        frames = list(read_frames(f))
+    assert [k for k, _ in frames] == [b"W"] * 8 + [b"D"]
+    assert b"".join(p for k, p in frames if k == b"W") == blob
+    with socket.create_connection((host, port)) as s, s.makefile("rwb") as f:
+        write_pull_request(f, 4)                  # not staged: EOF, no frames
+        f.flush()
+        assert list(read_frames(f)) == []
+    agent.close()

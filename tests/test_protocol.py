@@ -80,7 +80,7 @@ def test_cuda_ipc_endpoint_round_trip():
 
 def test_instance_adapter_serves_the_messages():
     inst = FakeInstance(vocab=50, max_slots=4)
-    ad = InstanceAdapter(inst, "i0", open_endpoint=lambda ep: ep)
+    ad = InstanceAdapter(inst, "i0", open_endpoint=lambda ep, version: ep)
     assert protocol.decode_line(protocol.encode_message(ad.register()))["instance_id"] == "i0"
     out = ad.handle(protocol.msg_pull_weights(2, "cuda-ipc://x"))
     assert out[0]["weight_version"] == 2
