@@ -177,8 +177,7 @@ def main():
     ws, rank, local = dist_env()
     torch.cuda.set_device(local)
     if ws > 1:
-        os.environ.setdefault("NCCL_DEBUG", "ERROR")   # keep stdout to the one JSON line
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        multi.init_nccl_quiet(dist, torch, local)        # stdout stays one JSON line
     shape = QWEN25_1_5B
     n_prompts, new = args.prompts, args.new_tokens
     w = synth_hf_weights(shape, seed=0, device=f"cuda:{local}")

@@ -52,3 +52,22 @@ def broadcast_object(obj, src: int = 0):
 def weak_scaling_value(tokens_per_rank: list[float], seconds_per_rank: list[float]) -> float:
     """Whole-job throughput: tokens of all ranks / slowest rank's time."""
     return sum(tokens_per_rank) / max(seconds_per_rank)
+
+
+def init_nccl_quiet(dist, torch, local_rank: int) -> None:
+    """init_process_group("nccl") + one barrier with the process's stdout
+    pointed at stderr, so NCCL's own start-up lines (printed with C stdio,
+    e.g. "NCCL version ...") never reach the bench's one-JSON-line stdout."""
+    import os
+    import sys
+    sys.stdout.flush()
+    saved = os.dup(1)
+    os.dup2(2, 1)
+    try:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        dist.barrier()
+        torch.cuda.synchronize()
+    finally:
+        sys.stdout.flush()
+        os.dup2(saved, 1)
+        os.close(saved)
