@@ -454,7 +454,13 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     tc_fence_after();
     const uint32_t tbase = tmem + half * BN + (static_cast<uint32_t>(q * 32) << 16);
     if constexpr (EPI == EPI_SWIGLU) {
-      bf16* out = reinterpret_cast<bf16*>(p.out);
+      // act = silu(gate) * up, staged as bf16 rows in the (now free) pipeline
+      // smem, then written as full rows: a warp store covers 512 contiguous
+      // bytes instead of 32 rows x 16 bytes.
+      constexpr int OC = BN / 2;                       // output columns per row
+      constexpr int PITCH = OC * 2 + 16;               // bytes; 16 B pad spreads banks
+      uint8_t* stage = smem;
+      const int row = half * HM + q * 32 + lane;       // row within the CTA tile
 #pragma unroll 1
       for (int g = 0; g < (warp_dead ? 0 : BN / 128); ++g) {
 #pragma unroll 1
@@ -463,21 +469,32 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           tmem_ld32(tbase + g * 128 + jc, rg);
           tmem_ld32(tbase + g * 128 + 64 + jc, ru);
           tmem_ld_wait();
-          const int col = n_blk * (BN / 2) + g * 64 + jc;
-          if (live && col < p.N / 2) {
-            uint32_t pk[16];
+          uint32_t pk[16];
 #pragma unroll
-            for (int i = 0; i < 16; ++i) {
-              const float a0 = silu_f(__uint_as_float(rg[2 * i])) * __uint_as_float(ru[2 * i]);
-              const float a1 =
-                  silu_f(__uint_as_float(rg[2 * i + 1])) * __uint_as_float(ru[2 * i + 1]);
-              pk[i] = pack_bf2(a0, a1);
-            }
-            uint4* dst = reinterpret_cast<uint4*>(out + static_cast<size_t>(m) * p.ldo + col);
-#pragma unroll
-            for (int i = 0; i < 4; ++i) dst[i] = make_uint4(pk[4 * i], pk[4 * i + 1], pk[4 * i + 2], pk[4 * i + 3]);
+          for (int i = 0; i < 16; ++i) {
+            const float a0 = silu_f(__uint_as_float(rg[2 * i])) * __uint_as_float(ru[2 * i]);
+            const float a1 = silu_f(__uint_as_float(rg[2 * i + 1])) * __uint_as_float(ru[2 * i + 1]);
+            pk[i] = pack_bf2(a0, a1);
           }
+          uint4* d = reinterpret_cast<uint4*>(stage + row * PITCH + (g * 64 + jc) * 2);
+#pragma unroll
+          for (int i = 0; i < 4; ++i) d[i] = make_uint4(pk[4 * i], pk[4 * i + 1], pk[4 * i + 2], pk[4 * i + 3]);
         }
+      }
+      if (NACC == 2) asm volatile("bar.sync 1, 256;" ::: "memory");
+      else asm volatile("bar.sync 1, 128;" ::: "memory");
+      bf16* out = reinterpret_cast<bf16*>(p.out);
+      constexpr int LPR = OC * 2 / 16;                 // lanes per row (16 B each)
+      constexpr int RPW = 32 / LPR;                    // rows per warp instruction
+      const int ew = warp - 4;
+      const int sub = lane / LPR, cl = lane % LPR;
+      const int col = n_blk * OC + cl * 8;
+#pragma unroll 2
+      for (int rr = ew * RPW + sub; rr < BMT; rr += NEW * RPW) {
+        const int mm = m_blk * BMT + rr;
+        if (mm >= p.M || col >= p.N / 2) continue;
+        *reinterpret_cast<uint4*>(out + static_cast<size_t>(mm) * p.ldo + col) =
+            *reinterpret_cast<const uint4*>(stage + rr * PITCH + cl * 16);
       }
     } else if constexpr (EPI == EPI_ARGMAX) {
       // greedy head: per (row, N-tile) max and its lowest column index; the
