@@ -94,6 +94,22 @@ constexpr int RING_ROWS = 512;
 // O projection stops at half the SMs: each extra split adds an fp32 partial
 // that the row consumer must read (measured: 100.4k vs 98.7k tok/s for O /
 // down splits 3/5 vs 6/5 on config 2).
+// Small-batch floor on the split: at one 128-row tile a CTA streams
+// N x K x 2 / (N-tiles x S) weight bytes; above ~512 KB per CTA the decode of
+// a few rows is bound by too few CTAs (7B o / down / qkv).  Raise S (a divisor
+// of the K blocks, <= 8, >= 4 K blocks per split) until it fits.
+static int small_batch_splits(int N, int K, int bn, int s0) {
+  const int nk = K / 64;
+  const double per_tile = 2.0 * N * K / ((N + bn - 1) / bn);
+  int s = s0;
+  for (int d = s0; d <= 8 && d <= nk / 4; ++d) {
+    if (nk % d) continue;
+    s = d;
+    if (per_tile / d <= 512.0 * 1024) break;
+  }
+  return std::max(s, s0);
+}
+
 static int pick_splits(int N, int K, int bn, int max_ctas) {
   const int nk = K / 64;
   const int tiles = ((N + bn - 1) / bn) * 2;
@@ -330,9 +346,9 @@ int rlb_instance::init() {
   prefill_rows = std::max(prefill_rows, 128);
   max_rows = std::max(prefill_rows, max_slots);
   max_rows = (max_rows + 255) / 256 * 256;
-  sp_qkv = 1;   // 128-row tiles give QKV its parallelism
-  sp_o = pick_splits(H, NQ * D, BN_O, 74);
-  sp_down = pick_splits(H, F, BN_DOWN, 148);
+  sp_qkv = small_batch_splits(QKV, H, BN_QKV, 1);   // 128-row tiles give QKV its parallelism
+  sp_o = small_batch_splits(H, NQ * D, BN_O, pick_splits(H, NQ * D, BN_O, 74));
+  sp_down = small_batch_splits(H, F, BN_DOWN, pick_splits(H, F, BN_DOWN, 148));
   if (const char* ov = std::getenv("RLB_SPLITS")) {   // "qkv,o,down" (tuning; process-wide)
     int a = 0, b = 0, c = 0;
     if (std::sscanf(ov, "%d,%d,%d", &a, &b, &c) == 3) {

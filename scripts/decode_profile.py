@@ -11,7 +11,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
 from paper_2510_19225_b200.instance import RolloutInstance
 from paper_2510_19225_b200.profile import estimate_plateau, measured_profile_table
-from paper_2510_19225_b200.shapes import QWEN25_1_5B
+from paper_2510_19225_b200.shapes import SHAPES
 from paper_2510_19225_b200.synth import synth_hf_weights, synth_prompts
 
 BATCHES = [1, 2, 4, 8, 16, 32, 64, 128, 192, 256, 384, 512]
@@ -19,13 +19,20 @@ NEW = 96
 
 
 def main():
-    out = sys.argv[1] if len(sys.argv) > 1 else None
-    w = synth_hf_weights(QWEN25_1_5B, seed=0, device="cuda:0")
-    inst = RolloutInstance(QWEN25_1_5B, 0, max_slots=512, max_seq_len=512, graph_steps=16)
+    import argparse
+    ap = argparse.ArgumentParser()
+    ap.add_argument("out", nargs="?")
+    ap.add_argument("--shape", default="qwen2.5-1.5b")
+    ap.add_argument("--batches", default=",".join(map(str, BATCHES)))
+    args = ap.parse_args()
+    out = args.out
+    shape = SHAPES[args.shape]
+    w = synth_hf_weights(shape, seed=0, device="cuda:0")
+    inst = RolloutInstance(shape, 0, max_slots=512, max_seq_len=512, graph_steps=16)
     inst.load_weights(w, version=1)
     points = []
-    for b in BATCHES:
-        prompts = synth_prompts(b, QWEN25_1_5B.vocab, 128, 384, seed=b)
+    for b in map(int, args.batches.split(",")):
+        prompts = synth_prompts(b, shape.vocab, 128, 384, seed=b)
         for rep in range(2):      # first pass captures the graphs
             inst.decode_profile(reset=True)
             for i, p in enumerate(prompts):
@@ -37,7 +44,7 @@ def main():
         print(f"b={b:4d} steps={s:4d} {1e3 * sec / s:7.3f} ms/step {b * s / sec:10.0f} tok/s",
               flush=True)
     t = measured_profile_table(points)
-    res = {"shape": "qwen2.5-1.5b", "new_tokens": NEW, "prompt_len": "U[128,384]",
+    res = {"shape": shape.name, "new_tokens": NEW, "prompt_len": "U[128,384]",
            "context_calibration": t.context_calibration,
            "entries": [{"batch_size": e.batch_size, "decode_tokens_per_s": e.decode_throughput}
                        for e in t.entries],
