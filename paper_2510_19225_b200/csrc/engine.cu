@@ -85,6 +85,7 @@ constexpr int SMALL_ROWS = 256;
 // tiles.  None of these choices changes a bit of any row's result.
 struct TilePlan {
   int bm_qkv, bm_o, bn_gu, bm_gu, bm_down;
+  bool cl_down;   // down: cluster residual add (else fp32 partials + RMSNorm sum)
 };
 constexpr int RING_ROWS = 512;
 
@@ -253,11 +254,15 @@ struct rlb_instance {
   // others share each weight stage between two 128-row accumulators
   int bm_qkv = 128, bm_o = 256, bm_gu = 256, bm_down = 256;   // decode batch (> 256 rows)
   TilePlan plan(int R) const {
-    if (R <= 128) return {128, 128, BN_SMALL, 128, 128};
-    if (R <= SMALL_ROWS) return {128, 128, BN_SMALL, 256, 128};
-    if (R > 512) return {256, bm_o, BN_GU, bm_gu, bm_down};
-    return {bm_qkv, bm_o, BN_GU, bm_gu, bm_down};
+    if (R <= 128) return {128, 128, BN_SMALL, 128, 128, cl_down};
+    if (R <= SMALL_ROWS) return {128, 128, BN_SMALL, 256, 128, cl_down};
+    // prefill chunks: the DSMEM reduction of thousands of split tiles costs
+    // more than writing the partials (both sum the splits in the same order)
+    if (R > 512) return {256, bm_o, BN_GU, bm_gu, bm_down, cl_down_large};
+    return {bm_qkv, bm_o, BN_GU, bm_gu, bm_down, cl_down};
   }
+  bool cl_down_large = false;
+  bool last_cl_down = true;   // mode of the last forward (its head sums the partials)
   // split-K O / down: sum the splits inside a cluster and add into h in the
   // GEMM epilogue (true), or write fp32 partials that the following RMSNorm
   // kernel sums in split order (false)
@@ -362,12 +367,14 @@ int rlb_instance::init() {
     }
   }
 
-  if (const char* ov = std::getenv("RLB_CLUSTER")) {   // "o,down" 0/1 (tuning; process-wide)
-    int a = 0, b = 0;
-    if (std::sscanf(ov, "%d,%d", &a, &b) == 2) {
+  if (const char* ov = std::getenv("RLB_CLUSTER")) {   // "o,down[,down_large]" 0/1 (tuning)
+    int a = 0, b = 0, c = 0;
+    const int n = std::sscanf(ov, "%d,%d,%d", &a, &b, &c);
+    if (n >= 2) {
       cl_o = a != 0;
       cl_down = b != 0;
     }
+    if (n == 3) cl_down_large = c != 0;
   }
   if (const char* ov = std::getenv("RLB_BM")) {   // "qkv,o,gate_up,down" (tuning; process-wide)
     int a = 0, b = 0, c = 0, d = 0;
@@ -547,7 +554,7 @@ int rlb_instance::forward_layers(int R) {
                    R, 2 * F, H, nullptr, d_act, F, tp.bm_gu)))
       return rc;
     const bool last = l + 1 == m.layers;
-    if (cl_down) {
+    if (tp.cl_down) {
       if ((rc = proj(m_act, w.m_down, BN_DOWN, sp_down, EPI_RESADD, R, H, F, nullptr, d_h, H,
                      tp.bm_down)))
         return rc;
@@ -565,6 +572,7 @@ int rlb_instance::forward_layers(int R) {
     }
   }
   pending_rows = R;
+  last_cl_down = tp.cl_down;
   return RLB_OK;
 }
 
@@ -580,7 +588,8 @@ int rlb_instance::proj(const CUtensorMap& a, const CUtensorMap& b, int bn, int s
 int rlb_instance::head(int Lrows, bool append) {
   if (Lrows <= 0) return RLB_OK;
   int rc;
-  if ((rc = resid_norm_launch(d_h, cl_down ? nullptr : d_part, cl_down ? 0 : sp_down, pending_rows,
+  if ((rc = resid_norm_launch(d_h, last_cl_down ? nullptr : d_part, last_cl_down ? 0 : sp_down,
+                              pending_rows,
                               d_logit_src, Lrows, norm, H, m.rms_eps, d_xn, false, st)))
     return rc;
   if (!append) return proj(m_xn, m_lm, BN_LM, 1, EPI_F32, Lrows, V, H, nullptr, d_logits, V);
