@@ -216,3 +216,20 @@ def test_decode_profile_measured(tiny):
     assert t.distinct_batch_sizes() == len(prof)
     assert 1 <= estimate_plateau(t, t.context_calibration) <= 32
     assert inst.decode_profile(reset=True) == prof and inst.decode_profile() == []
+
+
+def test_qwen25_1_5b_full_depth_teacher_forced(cuda):
+    """The config-2 model itself (28 layers, 151,936 vocab): greedy rollout on
+    the B200 against the fp32 oracle, teacher-forced (bf16 tolerance 2e-2)."""
+    from paper_2510_19225_b200.shapes import QWEN25_1_5B
+    w = synth_hf_weights(QWEN25_1_5B, seed=0, device="cuda")
+    prompts = synth_prompts(3, QWEN25_1_5B.vocab, 48, 96, seed=8)
+    inst = _instance(QWEN25_1_5B, w, max_slots=8, max_seq_len=256)
+    gen = _rollout(inst, prompts, 24)
+    inst.close()
+    oracle = Qwen2Fp32(QWEN25_1_5B, w)
+    del w
+    rep = teacher_forced_compare(oracle, prompts, gen, TOL_BF16)
+    print(f"qwen2.5-1.5b 28L: {rep.steps} steps, exemption rate {rep.exemption_rate:.4f}")
+    assert rep.ok, rep.failures[:5]
+    assert rep.exemption_rate < 0.1
