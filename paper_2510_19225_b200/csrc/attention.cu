@@ -62,8 +62,11 @@ __device__ __forceinline__ void mma_bf16(float (&d)[4], uint32_t a0, uint32_t a2
 
 }  // namespace
 
+#ifndef ATTN_MINB
+#define ATTN_MINB 2   // resident CTAs per SM the register budget is cut for
+#endif
 template <int D>
-__global__ void __launch_bounds__(WARPS * 32, 2) attn_mma_kernel(AttnArgs a) {
+__global__ void __launch_bounds__(WARPS * 32, ATTN_MINB) attn_mma_kernel(AttnArgs a) {
   constexpr int ROWB = D * 2;            // bytes per token row
   constexpr int CPR = ROWB / 16;         // 16-byte chunks per row
   constexpr int KSTEPS = D / 16;
