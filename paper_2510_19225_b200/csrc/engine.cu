@@ -262,6 +262,7 @@ struct rlb_instance {
     return {bm_qkv, bm_o, BN_GU, bm_gu, bm_down, cl_down};
   }
   bool cl_down_large = false;
+  int mc_gu = 1;   // gate_up A-multicast pairs at > 256 rows (RLB_GU_MC=2)
   bool last_cl_down = true;   // mode of the last forward (its head sums the partials)
   // split-K O / down: sum the splits inside a cluster and add into h in the
   // GEMM epilogue (true), or write fp32 partials that the following RMSNorm
@@ -376,6 +377,7 @@ int rlb_instance::init() {
     }
     if (n == 3) cl_down_large = c != 0;
   }
+  if (const char* ov = std::getenv("RLB_GU_MC")) mc_gu = std::atoi(ov) == 2 ? 2 : 1;
   if (const char* ov = std::getenv("RLB_BM")) {   // "qkv,o,gate_up,down" (tuning; process-wide)
     int a = 0, b = 0, c = 0, d = 0;
     if (std::sscanf(ov, "%d,%d,%d,%d", &a, &b, &c, &d) == 4) {
@@ -550,9 +552,14 @@ int rlb_instance::forward_layers(int R) {
                                   st)))
         return rc;
     }
-    if ((rc = proj(m_xn, tp.bn_gu == BN_SMALL ? w.m_gu_small : w.m_gu, tp.bn_gu, 1, EPI_SWIGLU,
-                   R, 2 * F, H, nullptr, d_act, F, tp.bm_gu)))
-      return rc;
+    {
+      GemmParams pg{R, 2 * F, H, nullptr, d_act, F, 1, d_part};
+      const bool mc = mc_gu == 2 && tp.bn_gu == BN_GU && tp.bm_gu == 256 &&
+                      ((2 * F) / BN_GU) % 2 == 0;
+      if ((rc = gemm_launch(m_xn, tp.bn_gu == BN_SMALL ? w.m_gu_small : w.m_gu, tp.bn_gu,
+                            EPI_SWIGLU, pg, st, tp.bm_gu, mc ? 2 : 1)))
+        return rc;
+    }
     const bool last = l + 1 == m.layers;
     if (tp.cl_down) {
       if ((rc = proj(m_act, w.m_down, BN_DOWN, sp_down, EPI_RESADD, R, H, F, nullptr, d_h, H,

@@ -323,7 +323,12 @@ __device__ __forceinline__ void rope_direct(const GemmParams& p, uint32_t tbase,
   }
 }
 
-template <int BN, int EPI, int NACC>
+// MC = 2: the CTAs of two neighbouring N tiles form a (1,2,1) cluster and
+// share the A (activation) tile: each loads one 128-row half and multicasts
+// it to both, halving the A traffic from L2; both MMA warps release a stage
+// on both CTAs (multicast commit), so neither refills it before the other
+// has consumed it.
+template <int BN, int EPI, int NACC, int MC = 1>
 __global__ void __launch_bounds__(GEMM_THREADS, 1)
     gemm_bf16_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                  GemmParams p) {
@@ -361,7 +366,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   const bool via_cluster = kClusterEpi && p.splits > 1;
   // accumulators with at least one live row (a small-M tile skips the
   // loads, MMAs and TMEM reads of the empty one)
-  const int live_acc = (NACC == 2 && p.M - m_blk * BMT > HM) ? 2 : 1;
+  const int live_acc = MC > 1 ? NACC : ((NACC == 2 && p.M - m_blk * BMT > HM) ? 2 : 1);
   const uint32_t stage_tx = static_cast<uint32_t>(live_acc * C::A_BYTES + C::B_BYTES);
 
   if (warp == 0 && lane == 0) {
@@ -369,7 +374,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     tma_prefetch(&tmB);
     for (int s = 0; s < C::STAGES; ++s) {
       mbar_init(smem_u32(&full[s]), 1);
-      mbar_init(smem_u32(&empty[s]), 1);
+      mbar_init(smem_u32(&empty[s]), MC);
     }
     mbar_init(smem_u32(tfull), 1);
     fence_mbar_init();
@@ -377,6 +382,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   if (warp == 2) tmem_alloc(smem_u32(tmem_slot), C::TMEM_COLS);
   tc_fence_before();
   __syncthreads();
+  if constexpr (MC > 1) cluster_sync();      // peers' barriers initialised before any multicast
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   if (stamp && threadIdx.x == 0) p.dbg[1] = gtime();
@@ -410,11 +416,18 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           mbar_expect_tx(smem_u32(&full[s]), stage_tx);
           tma_load_2d(smem_u32(st + NACC * C::A_BYTES), &tmB, smem_u32(&full[s]), kx, n_blk * BN);
         }
+        if constexpr (MC > 1) {
+          static_assert(MC == NACC, "one A half per cluster CTA");
+          const int a = static_cast<int>(cluster_rank());
+          tma_load_2d_mc(smem_u32(st + a * C::A_BYTES), &tmA, smem_u32(&full[s]), kx,
+                         m_blk * BMT + a * HM, static_cast<uint16_t>((1u << MC) - 1));
+        } else {
 #pragma unroll
-        for (int a = 0; a < NACC; ++a)
-          if (a < live_acc)
-            tma_load_2d(smem_u32(st + a * C::A_BYTES), &tmA, smem_u32(&full[s]), kx,
-                        m_blk * BMT + a * HM);
+          for (int a = 0; a < NACC; ++a)
+            if (a < live_acc)
+              tma_load_2d(smem_u32(st + a * C::A_BYTES), &tmA, smem_u32(&full[s]), kx,
+                          m_blk * BMT + a * HM);
+        }
       }
     }
   } else if (warp == 1) {
@@ -436,7 +449,10 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
               umma_bf16(tmem + a * BN, umma_desc_sw128(st + a * C::A_BYTES) + 2 * k, bd + 2 * k,
                         idesc, (kb | k) != 0);
         }
-        umma_commit(smem_u32(&empty[s]));
+        if constexpr (MC > 1)
+          umma_commit_mc(smem_u32(&empty[s]), static_cast<uint16_t>((1u << MC) - 1));
+        else
+          umma_commit(smem_u32(&empty[s]));
       }
       umma_commit(smem_u32(tfull));
       if (stamp) p.dbg[3] = gtime();
@@ -650,6 +666,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     }
   }
   if (stamp && threadIdx.x == 128) p.dbg[6] = gtime();
+  if constexpr (MC > 1) cluster_sync();      // no peer arrives on this CTA's barriers any more
   tc_fence_before();
   __syncthreads();
   if (warp == 2) {
@@ -695,9 +712,9 @@ int make_kmajor_map(CUtensorMap* map, const void* ptr, int64_t rows, int64_t k, 
   return RLB_OK;
 }
 
-template <int BN, int EPI, int NACC>
+template <int BN, int EPI, int NACC, int MC = 1>
 static int set_attr() {
-  RLB_CUDA(cudaFuncSetAttribute(gemm_bf16_tc<BN, EPI, NACC>,
+  RLB_CUDA(cudaFuncSetAttribute(gemm_bf16_tc<BN, EPI, NACC, MC>,
                                 cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 GemmCfg<BN, NACC>::SMEM));
   return RLB_OK;
@@ -723,20 +740,23 @@ int gemm_prepare() {
   if (done[dev & 63]) return RLB_OK;
   int rc;
   if ((rc = set_attr_bn<128, 2>()) || (rc = set_attr_bn<256, 2>()) || (rc = set_attr_bn<128, 1>()) ||
-      (rc = set_attr_bn<256, 1>()))
+      (rc = set_attr_bn<256, 1>()) || (rc = set_attr<256, EPI_SWIGLU, 2, 2>()))
     return rc;
   done[dev & 63] = true;
   return RLB_OK;
 }
 
-template <int BN, int EPI, int NACC>
+template <int BN, int EPI, int NACC, int MC = 1>
 static int launch_one(const CUtensorMap& a, const CUtensorMap& b, const GemmParams& p,
                       cudaStream_t st) {
   using C = GemmCfg<BN, NACC>;
   RLB_CHECK((p.N + BN - 1) / BN <= 65535, RLB_ERR_ARG, "too many N tiles");
   dim3 grid((p.M + C::BMT - 1) / C::BMT, (p.N + BN - 1) / BN, p.splits);
-  if (cluster_epi(EPI) && BN == 128 && p.splits > 1) {
-    // the split CTAs of a tile form one cluster (DSMEM reduction)
+  const bool split_cluster = cluster_epi(EPI) && BN == 128 && p.splits > 1;
+  if (split_cluster || MC > 1) {
+    // split-K CTAs of a tile (DSMEM reduction) or A-sharing N-tile pairs
+    RLB_CHECK(MC == 1 || (grid.y % MC == 0 && p.splits == 1), RLB_ERR_ARG,
+              "A multicast needs an even number of N tiles and no split");
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = grid;
     cfg.blockDim = dim3(GEMM_THREADS);
@@ -745,16 +765,17 @@ static int launch_one(const CUtensorMap& a, const CUtensorMap& b, const GemmPara
     cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeClusterDimension;
     attr[0].val.clusterDim.x = 1;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = static_cast<unsigned>(p.splits);
+    attr[0].val.clusterDim.y = MC;
+    attr[0].val.clusterDim.z = split_cluster ? static_cast<unsigned>(p.splits) : 1u;
     attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = pdl_enabled(RLB_PDL_CLASS) ? 2 : 1;
-    RLB_CUDA(cudaLaunchKernelEx(&cfg, gemm_bf16_tc<BN, EPI, NACC>, a, b, p));
+    RLB_CUDA(cudaLaunchKernelEx(&cfg, gemm_bf16_tc<BN, EPI, NACC, MC>, a, b, p));
     return RLB_OK;
   }
-  RLB_CUDA(launch_k(gemm_bf16_tc<BN, EPI, NACC>, grid, dim3(GEMM_THREADS), C::SMEM, st, a, b, p));
+  if constexpr (MC == 1)
+    RLB_CUDA(launch_k(gemm_bf16_tc<BN, EPI, NACC>, grid, dim3(GEMM_THREADS), C::SMEM, st, a, b, p));
   return RLB_OK;
 }
 
@@ -777,8 +798,13 @@ static int launch_bn(const CUtensorMap& a, const CUtensorMap& b, int epi, const 
 }
 
 int gemm_launch(const CUtensorMap& a, const CUtensorMap& b, int block_n, int epi,
-                const GemmParams& p, cudaStream_t st, int block_m) {
+                const GemmParams& p, cudaStream_t st, int block_m, int a_multicast) {
   if (p.M <= 0) return RLB_OK;
+  if (a_multicast == 2) {
+    RLB_CHECK(block_n == 256 && block_m == 256 && epi == EPI_SWIGLU, RLB_ERR_ARG,
+              "A multicast is built for the 256x256 SwiGLU projection");
+    return launch_one<256, EPI_SWIGLU, 2, 2>(a, b, p, st);
+  }
   RLB_CHECK(p.K % BK == 0 && p.N % 16 == 0, RLB_ERR_ARG, "GEMM shape not tileable");
   RLB_CHECK(p.splits >= 1 && (p.K / BK) % p.splits == 0, RLB_ERR_ARG,
             "split-K must divide the K blocks");
@@ -830,9 +856,10 @@ extern "C" int rlb_bench_gemm(int device, int32_t M, int32_t N, int32_t K, int32
   cudaEvent_t e0, e1;
   RLB_CUDA(cudaEventCreate(&e0));
   RLB_CUDA(cudaEventCreate(&e1));
-  if ((rc = gemm_launch(ma, mb, block_n, epi, p, 0, block_m))) return rc;
+  const int mc = std::getenv("RLB_GEMM_MC") ? 2 : 1;   // A multicast pairs (SwiGLU 256x256)
+  if ((rc = gemm_launch(ma, mb, block_n, epi, p, 0, block_m, mc))) return rc;
   RLB_CUDA(cudaEventRecord(e0, 0));
-  for (int i = 0; i < iters && !rc; ++i) rc = gemm_launch(ma, mb, block_n, epi, p, 0, block_m);
+  for (int i = 0; i < iters && !rc; ++i) rc = gemm_launch(ma, mb, block_n, epi, p, 0, block_m, mc);
   RLB_CUDA(cudaEventRecord(e1, 0));
   RLB_CUDA(cudaEventSynchronize(e1));
   float ms = 0.f;
@@ -844,7 +871,7 @@ extern "C" int rlb_bench_gemm(int device, int32_t M, int32_t N, int32_t K, int32
     RLB_CUDA(cudaMalloc(&d, sizeof(h)));
     RLB_CUDA(cudaMemset(d, 0, sizeof(h)));
     p.dbg = d;
-    rc = gemm_launch(ma, mb, block_n, epi, p, 0, block_m);
+    rc = gemm_launch(ma, mb, block_n, epi, p, 0, block_m, mc);
     RLB_CUDA(cudaMemcpy(h, d, sizeof(h), cudaMemcpyDeviceToHost));
     std::fprintf(stderr, "gemm dbg (ns from CTA start): setup %lld wait %lld mma_done %lld "
                  "epi_start %lld epi_end %lld dealloc %lld\n",
@@ -881,7 +908,9 @@ extern "C" int rlb_gemm(int device, int32_t M, int32_t N, int32_t K, const void*
   p.ldo = epilogue == EPI_SWIGLU ? N / 2 : N;
   p.splits = splits < 1 ? 1 : splits;
   if (p.splits == 1 || (epilogue == EPI_RESADD && block_n == 128)) {
-    rc = gemm_launch(ma, mb, block_n, epilogue, p, 0, block_m);   // RESADD: cluster split-K
+    // RESADD: cluster split-K; RLB_GEMM_MC: A-multicast pairs (SwiGLU 256x256)
+    rc = gemm_launch(ma, mb, block_n, epilogue, p, 0, block_m,
+                     std::getenv("RLB_GEMM_MC") ? 2 : 1);
   } else {
     RLB_CUDA(cudaMalloc(&p.ws, sizeof(float) * static_cast<size_t>(p.splits) * M * N));
     rc = gemm_launch(ma, mb, block_n, EPI_PARTIAL, p, 0, block_m);

@@ -104,3 +104,16 @@ def test_resadd_cluster_batch_invariant(dev, sp, bm):
     big[idx], h[idx] = rows, h_rows
     out = gemm(dev, big, B, out=h, epilogue=1, block_n=128, splits=sp, block_m=bm)
     assert torch.equal(out[idx], small)
+
+
+def test_gemm_swiglu_a_multicast_pairs(dev, monkeypatch):
+    """(1,2,1) clusters sharing the A tile by TMA multicast: same bits as the
+    unclustered kernel."""
+    from paper_2510_19225_b200.instance import gemm
+    M, F, K = 512, 8960, 1536
+    A = _rand((M, K), 1.0, 21)
+    wgu = _rand((2 * F, K), 0.05, 22)
+    ref = gemm(dev, A, wgu, epilogue=2, block_n=256)
+    monkeypatch.setenv("RLB_GEMM_MC", "1")
+    out = gemm(dev, A, wgu, epilogue=2, block_n=256)
+    assert torch.equal(out, ref)
