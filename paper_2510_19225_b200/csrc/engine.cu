@@ -245,6 +245,7 @@ struct rlb_instance {
   }
   rlb_stats stats{};
   int last_R = 0;  // rows of the last decode step (for rlb_profile_kernel)
+  unsigned long long* d_dbg = nullptr;   // RLB_GEMM_DBG: CTA-0 timestamps of profiled GEMMs
   // split-K factors of the small-N projections: a property of the model
   // shape only (never of M or of the engine config), so every instance of
   // the same model reduces every row identically.
@@ -586,6 +587,7 @@ int rlb_instance::forward_layers(int R) {
 int rlb_instance::proj(const CUtensorMap& a, const CUtensorMap& b, int bn, int splits, int epi,
                        int R, int N, int K, const bf16* bias, void* out, int ldo, int bm) {
   GemmParams p{R, N, K, bias, out, ldo, splits < 1 ? 1 : splits, d_part};
+  p.dbg = d_dbg;   // null outside rlb_profile_kernel's RLB_GEMM_DBG breakdown
   return gemm_launch(a, b, bn, epi, p, st, bm);
 }
 
@@ -1230,6 +1232,7 @@ int rlb_profile_kernel(rlb_instance* h, int32_t which, int32_t iters, double* av
         GemmParams pq{R, h->QKV, H, w.bqkv, nullptr, 0, h->sp_qkv, nullptr};
         pq.rope = RopeDst{h->d_row_slot, h->d_row_pos, h->d_rope, h->d_q, NQ * D, h->kv_scratch(),
                           h->d_bt, h->pps, NQ, h->NKV, D};
+        pq.dbg = h->d_dbg;
         return gemm_launch(h->m_xn, w.m_qkv, BN_QKV, EPI_ROPE, pq, h->st, tp.bm_qkv);
       }
       case 4: return h->proj(h->m_attn, w.m_o, BN_O, h->sp_o, h->cl_o ? EPI_RESADD : EPI_PARTIAL,
@@ -1262,6 +1265,20 @@ int rlb_profile_kernel(rlb_instance* h, int32_t which, int32_t iters, double* av
   }
   int rc = launch();  // warm
   if (rc) return rc;
+  if (std::getenv("RLB_GEMM_DBG") && which >= 1 && which <= 5) {   // latency breakdown, 1 launch
+    if (!h->d_dbg) RLB_CUDA(cudaMalloc(&h->d_dbg, 8 * sizeof(unsigned long long)));
+    RLB_CUDA(cudaMemsetAsync(h->d_dbg, 0, 8 * sizeof(unsigned long long), h->st));
+    if ((rc = launch())) return rc;
+    unsigned long long t[8];
+    RLB_CUDA(cudaMemcpyAsync(t, h->d_dbg, sizeof(t), cudaMemcpyDeviceToHost, h->st));
+    RLB_CUDA(cudaStreamSynchronize(h->st));
+    std::fprintf(stderr, "kernel %d dbg (ns from CTA start): setup %lld wait %lld mma_done %lld "
+                 "epi_start %lld epi_end %lld dealloc %lld\n", which,
+                 (long long)(t[1] - t[0]), (long long)(t[2] - t[0]), (long long)(t[3] - t[0]),
+                 (long long)(t[4] - t[0]), (long long)(t[6] - t[0]), (long long)(t[5] - t[0]));
+    RLB_CUDA(cudaFree(h->d_dbg));
+    h->d_dbg = nullptr;
+  }
   RLB_CUDA(cudaEventRecord(h->ev0, h->st));
   for (int i = 0; i < iters; ++i)
     if ((rc = launch())) return rc;

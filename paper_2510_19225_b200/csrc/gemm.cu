@@ -249,21 +249,42 @@ __device__ __forceinline__ void cluster_epilogue(const GemmParams& p, uint32_t s
 // EPI_ROPE without split-K, straight from TMEM: the thread owns row m (its
 // TMEM lane) and the tile's 128 columns (one head of D=128, two of D=64).
 // Rotation partners c and c + D/2 are loaded as two 32-column chunks.
-__device__ __forceinline__ void rope_direct(const GemmParams& p, uint32_t tbase, int m, bool live,
-                                            int n_blk) {
+// Row metadata of the direct RoPE epilogue, loaded by the epilogue thread
+// while the mainloop runs: position, its K/V slot, and an L1 prefetch of the
+// (cos, sin) rows the thread's column pairs will read.
+struct RopeRow {
+  int pos = 0;
+  bf16* kv_page = nullptr;
+};
+__device__ __forceinline__ RopeRow rope_row_prefetch(const GemmParams& p, int m, bool live,
+                                                     int n_blk, int cp0, int cp1) {
+  RopeRow rr;
+  if (!live) return rr;
   const RopeDst& d = p.rope;
   const int hd = d.d / 2;
   const size_t head_stride = static_cast<size_t>(2) * PAGE * d.d;
-  int pos = 0;
-  bf16* kv_page = nullptr;
-  if (live) {
-    pos = d.row_pos[m];
-    const int page = d.block_table[static_cast<size_t>(d.row_slot[m]) * d.bt_stride + pos / PAGE];
-    kv_page = d.kv + static_cast<size_t>(page) * head_stride * d.nkv +
-              static_cast<size_t>(pos % PAGE) * d.d;
+  rr.pos = d.row_pos[m];
+  const int page = d.block_table[static_cast<size_t>(d.row_slot[m]) * d.bt_stride + rr.pos / PAGE];
+  rr.kv_page = d.kv + static_cast<size_t>(page) * head_stride * d.nkv +
+               static_cast<size_t>(rr.pos % PAGE) * d.d;
+  for (int cp = cp0; cp < cp1; ++cp) {
+    const int j0 = (n_blk * 128 + (cp * 32 / hd) * d.d + (cp * 32) % hd) % d.d;
+    const char* c = reinterpret_cast<const char*>(d.rope + static_cast<size_t>(rr.pos) * hd + j0);
+    asm volatile("prefetch.global.L1 [%0];" ::"l"(c));
+    asm volatile("prefetch.global.L1 [%0];" ::"l"(c + 128));
   }
+  return rr;
+}
+
+__device__ __forceinline__ void rope_direct(const GemmParams& p, uint32_t tbase, int m, bool live,
+                                            int n_blk, int cp0, int cp1, const RopeRow& rr) {
+  const RopeDst& d = p.rope;
+  const int hd = d.d / 2;
+  const size_t head_stride = static_cast<size_t>(2) * PAGE * d.d;
+  const int pos = rr.pos;
+  bf16* kv_page = rr.kv_page;
 #pragma unroll 1
-  for (int cp = 0; cp < 2; ++cp) {
+  for (int cp = cp0; cp < cp1; ++cp) {
     const int a = (cp * 32 / hd) * d.d + (cp * 32) % hd;   // first column of the chunk
     uint32_t r1[32], r2[32];
     tmem_ld32(tbase + a, r1);
@@ -335,6 +356,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   using C = GemmCfg<BN, NACC>;
   constexpr int BMT = C::BMT;
   constexpr int NEW = 4 * NACC;                 // epilogue warps with an accumulator
+  // epilogue warps that run (direct RoPE with one accumulator splits columns)
+  constexpr int NEW_ALL = (EPI == EPI_ROPE && NACC == 1) ? 8 : NEW;
   constexpr bool kClusterEpi = cluster_epi(EPI) && BN == 128;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -457,14 +480,21 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       umma_commit(smem_u32(tfull));
       if (stamp) p.dbg[3] = gtime();
     }
-  } else if (warp >= 4 && warp < 4 + NEW) {
-    const int half = (warp - 4) >> 2;          // accumulator
+  } else if (warp >= 4 && warp < 4 + NEW_ALL) {
+    // with one accumulator the RoPE epilogue uses all 8 epilogue warps: warps
+    // 8-11 read the same TMEM lanes as 4-7 and take the second column pair
+    const int half = NACC == 2 ? (warp - 4) >> 2 : 0;   // accumulator
     const int q = warp & 3;                    // TMEM lane quadrant
     const int m = m_blk * BMT + half * HM + q * 32 + lane;
     const bool live = m < p.M;
     // warp-uniform: no row of this warp exists -> no TMEM reads (tcgen05.ld is
     // warp-collective, so the skip is per warp)
     const bool warp_dead = m_blk * BMT + half * HM + q * 32 >= p.M;
+    const int rcp0 = NACC == 1 ? (warp - 4) >> 2 : 0, rcp1 = NACC == 1 ? rcp0 + 1 : 2;
+    RopeRow rrow;
+    if constexpr (EPI == EPI_ROPE) {
+      if (!via_cluster) rrow = rope_row_prefetch(p, m, live, n_blk, rcp0, rcp1);   // overlaps the mainloop
+    }
     mbar_wait(smem_u32(tfull), 0);
     if (stamp && threadIdx.x == 128) p.dbg[4] = gtime();
     tc_fence_after();
@@ -538,11 +568,11 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       }
     } else if constexpr (EPI == EPI_ROPE) {
       if (via_cluster) {
-        // stage this split's fp32 tile for the cluster reduction
+        // stage this split's fp32 tile for the cluster reduction (warps 4..)
         float* stage = reinterpret_cast<float*>(smem);
         const int row = half * HM + q * 32 + lane;
 #pragma unroll 1
-        for (int c = 0; c < (warp_dead ? 0 : BN); c += 32) {
+        for (int c = 0; c < (warp_dead || warp >= 4 + NEW ? 0 : BN); c += 32) {
           uint32_t r[32];
           tmem_ld32(tbase + c, r);
           tmem_ld_wait();
@@ -553,7 +583,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
                                 __uint_as_float(r[4 * i + 2]), __uint_as_float(r[4 * i + 3]));
         }
       } else if (!warp_dead) {
-        rope_direct(p, tbase, m, live, n_blk);
+        rope_direct(p, tbase, m, live, n_blk, rcp0, rcp1, rrow);
       }
     } else if constexpr ((EPI == EPI_PARTIAL || EPI == EPI_F32) && BN == 128) {
       // fp32 tile out through shared memory so every global store is a full
