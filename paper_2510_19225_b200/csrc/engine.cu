@@ -253,7 +253,7 @@ struct rlb_instance {
   // rows per GEMM CTA: QKV uses 128-row tiles instead of split-K (twice the
   // CTAs, and its RoPE / KV-append epilogue runs straight from TMEM); the
   // others share each weight stage between two 128-row accumulators
-  int bm_qkv = 128, bm_o = 256, bm_gu = 256, bm_down = 256;   // decode batch (> 256 rows)
+  int bm_qkv = 128, bm_o = 128, bm_gu = 256, bm_down = 256;   // decode batch (> 256 rows)
   TilePlan plan(int R) const {
     if (R <= 128) return {128, 128, BN_SMALL, 128, 128, cl_down};
     if (R <= SMALL_ROWS) return {128, 128, BN_SMALL, 256, 128, cl_down};
