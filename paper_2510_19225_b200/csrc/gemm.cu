@@ -102,6 +102,13 @@ __global__ void __launch_bounds__(256) splitk_reduce_kernel(GemmParams p) {
 
 constexpr int EPI_LDS = 128 + 4;   // padded fp32 row of a staged 128-column tile
 
+// Engine QKV layout (pull.cu relayout_segments): within a head, each 64-row
+// block holds 32 rows of the first rotation half and their partners, i.e.
+// physical column c of a head (block t = c / 64, b = c % 64) is head column
+// t*32 + b for b < 32 and t*32 + (b - 32) + D/2 otherwise.  The head column
+// of the first half of the block holding physical column gcol:
+__device__ __forceinline__ int rope_j0(int gcol, int D) { return ((gcol % D) / 64) * 32; }
+
 // Split-K reduction of one BMT x 128 tile inside its cluster: this CTA (rank
 // z of S) owns tile rows [z*BMT/S, (z+1)*BMT/S); epilogue warp ew (of NW)
 // takes every NW-th of them (<= 32 rows, so lane k can hold row k's
@@ -179,13 +186,13 @@ __device__ __forceinline__ void cluster_epilogue(const GemmParams& p, uint32_t s
     float b1[2], b2[2];
 #pragma unroll
     for (int t = 0; t < 2; ++t) {
-      const int pi = lane + 32 * t;
-      jv[t] = pi % hd;
-      c1v[t] = (pi / hd) * d.d + jv[t];
+      // pair lane + 32 t: physical column 64 t + lane and its partner (+32)
+      c1v[t] = 64 * t + lane;
       const int col1 = n_blk * 128 + c1v[t];
+      jv[t] = rope_j0(col1, d.d) + lane;
       headv[t] = col1 / d.d;
       b1[t] = __bfloat162float(p.bias[col1]);
-      b2[t] = __bfloat162float(p.bias[col1 + hd]);
+      b2[t] = __bfloat162float(p.bias[col1 + 32]);
     }
 #pragma unroll 1
     for (int k0 = 0; k0 < nrows; k0 += G) {
@@ -199,7 +206,7 @@ __device__ __forceinline__ void cluster_epilogue(const GemmParams& p, uint32_t s
 #pragma unroll
           for (int t = 0; t < 2; ++t) {
             const uint32_t o1 = static_cast<uint32_t>((rr * EPI_LDS + c1v[t]) * 4);
-            const uint32_t o2 = o1 + static_cast<uint32_t>(hd * 4);
+            const uint32_t o2 = o1 + 32u * 4u;                 // the partner column
             float a1 = dsmem_ld(base[0] + o1), a2 = dsmem_ld(base[0] + o2);
 #pragma unroll
             for (int i = 1; i < 8; ++i) {
@@ -256,8 +263,14 @@ struct RopeRow {
   int pos = 0;
   bf16* kv_page = nullptr;
 };
+// Engine QKV layout (pull.cu relayout_segments): within a head, each 64-row
+// block holds 32 rows of the first rotation half and their partners, i.e.
+// physical column c of a head (block t = c / 64, b = c % 64) is head column
+// t*32 + b for b < 32 and t*32 + (b - 32) + D/2 otherwise.  Chunk pair cp of a
+// tile = physical columns [64 cp, 64 cp + 32) and their partners (+32).
+
 __device__ __forceinline__ RopeRow rope_row_prefetch(const GemmParams& p, int m, bool live,
-                                                     int n_blk, int cp0, int cp1) {
+                                                     int col0, int cp0, int cp1) {
   RopeRow rr;
   if (!live) return rr;
   const RopeDst& d = p.rope;
@@ -268,7 +281,7 @@ __device__ __forceinline__ RopeRow rope_row_prefetch(const GemmParams& p, int m,
   rr.kv_page = d.kv + static_cast<size_t>(page) * head_stride * d.nkv +
                static_cast<size_t>(rr.pos % PAGE) * d.d;
   for (int cp = cp0; cp < cp1; ++cp) {
-    const int j0 = (n_blk * 128 + (cp * 32 / hd) * d.d + (cp * 32) % hd) % d.d;
+    const int j0 = rope_j0(col0 + cp * 64, d.d);
     const char* c = reinterpret_cast<const char*>(d.rope + static_cast<size_t>(rr.pos) * hd + j0);
     asm volatile("prefetch.global.L1 [%0];" ::"l"(c));
     asm volatile("prefetch.global.L1 [%0];" ::"l"(c + 128));
@@ -277,7 +290,7 @@ __device__ __forceinline__ RopeRow rope_row_prefetch(const GemmParams& p, int m,
 }
 
 __device__ __forceinline__ void rope_direct(const GemmParams& p, uint32_t tbase, int m, bool live,
-                                            int n_blk, int cp0, int cp1, const RopeRow& rr) {
+                                            int col0, int cp0, int cp1, const RopeRow& rr) {
   const RopeDst& d = p.rope;
   const int hd = d.d / 2;
   const size_t head_stride = static_cast<size_t>(2) * PAGE * d.d;
@@ -285,17 +298,17 @@ __device__ __forceinline__ void rope_direct(const GemmParams& p, uint32_t tbase,
   bf16* kv_page = rr.kv_page;
 #pragma unroll 1
   for (int cp = cp0; cp < cp1; ++cp) {
-    const int a = (cp * 32 / hd) * d.d + (cp * 32) % hd;   // first column of the chunk
+    const int a = cp * 64;                                   // physical column of the chunk
     uint32_t r1[32], r2[32];
     tmem_ld32(tbase + a, r1);
-    tmem_ld32(tbase + a + hd, r2);
+    tmem_ld32(tbase + a + 32, r2);                           // the partners
     tmem_ld_wait();
     if (!live) continue;
-    const int col1 = n_blk * 128 + a;
+    const int col1 = col0 + a;                               // physical output column
     const int head = col1 / d.d;
-    const int j0 = col1 % d.d;                               // < hd
+    const int j0 = rope_j0(col1, d.d);                       // head column (< hd)
     const uint4* bb1 = reinterpret_cast<const uint4*>(p.bias + col1);
-    const uint4* bb2 = reinterpret_cast<const uint4*>(p.bias + col1 + hd);
+    const uint4* bb2 = reinterpret_cast<const uint4*>(p.bias + col1 + 32);
     float v1[32], v2[32];
 #pragma unroll
     for (int h4 = 0; h4 < 4; ++h4) {
@@ -357,7 +370,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   constexpr int BMT = C::BMT;
   constexpr int NEW = 4 * NACC;                 // epilogue warps with an accumulator
   // epilogue warps that run (direct RoPE with one accumulator splits columns)
-  constexpr int NEW_ALL = (EPI == EPI_ROPE && NACC == 1) ? 8 : NEW;
+  constexpr int NEW_ALL = (EPI == EPI_ROPE && NACC == 1 && BN == 128) ? 8 : NEW;
   constexpr bool kClusterEpi = cluster_epi(EPI) && BN == 128;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -490,10 +503,12 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     // warp-uniform: no row of this warp exists -> no TMEM reads (tcgen05.ld is
     // warp-collective, so the skip is per warp)
     const bool warp_dead = m_blk * BMT + half * HM + q * 32 >= p.M;
-    const int rcp0 = NACC == 1 ? (warp - 4) >> 2 : 0, rcp1 = NACC == 1 ? rcp0 + 1 : 2;
+    // RoPE chunk pairs (64 physical columns each) of this thread
+    const int rcp0 = NEW_ALL > NEW ? (warp - 4) >> 2 : 0;
+    const int rcp1 = NEW_ALL > NEW ? rcp0 + 1 : BN / 64;
     RopeRow rrow;
     if constexpr (EPI == EPI_ROPE) {
-      if (!via_cluster) rrow = rope_row_prefetch(p, m, live, n_blk, rcp0, rcp1);   // overlaps the mainloop
+      if (!via_cluster) rrow = rope_row_prefetch(p, m, live, n_blk * BN, rcp0, rcp1);   // overlaps the mainloop
     }
     mbar_wait(smem_u32(tfull), 0);
     if (stamp && threadIdx.x == 128) p.dbg[4] = gtime();
@@ -583,7 +598,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
                                 __uint_as_float(r[4 * i + 2]), __uint_as_float(r[4 * i + 3]));
         }
       } else if (!warp_dead) {
-        rope_direct(p, tbase, m, live, n_blk, rcp0, rcp1, rrow);
+        rope_direct(p, tbase, m, live, n_blk * BN, rcp0, rcp1, rrow);
       }
     } else if constexpr ((EPI == EPI_PARTIAL || EPI == EPI_F32) && BN == 128) {
       // fp32 tile out through shared memory so every global store is a full

@@ -70,12 +70,24 @@ void relayout_segments(const rlb_model_cfg& m, std::vector<Segment>* out) {
                   wo = c.put(H * QD), ln2 = c.put(H), wgu = c.put(2 * F * H), wd = c.put(H * F);
     const int32_t base = hf;  // ln1 q qb k kb v vb o ln2 gate up down
     seg(base + 0, 0, ln1, 2 * H);
-    seg(base + 1, 0, wqkv, 2 * QD * H);
-    seg(base + 2, 0, bqkv, 2 * QD);
-    seg(base + 3, 0, wqkv + 2 * QD * H, 2 * KD * H);
-    seg(base + 4, 0, bqkv + 2 * QD, 2 * KD);
-    seg(base + 5, 0, wqkv + 2 * (QD + KD) * H, 2 * KD * H);
-    seg(base + 6, 0, bqkv + 2 * (QD + KD), 2 * KD);
+    // q / k / v heads in 32-row pieces: each 64-row block = 32 rows of the
+    // first rotation half + their partners (row + D/2), so a 64-column GEMM
+    // tile holds whole RoPE pairs (identity for D = 64)
+    const int64_t D = m.head_dim, hd = D / 2, P = 32;
+    int64_t row0 = 0;
+    const int heads[3] = {m.n_q_heads, m.n_kv_heads, m.n_kv_heads};
+    for (int pj = 0; pj < 3; ++pj) {
+      const int32_t wi = base + 1 + 2 * pj, bi = base + 2 + 2 * pj;
+      for (int64_t hh = 0; hh < heads[pj]; ++hh)
+        for (int64_t t = 0; t < hd / P; ++t)
+          for (int half = 0; half < 2; ++half) {
+            const int64_t r_src = hh * D + half * hd + t * P;
+            const int64_t r_dst = row0 + hh * D + (2 * t + half) * P;
+            seg(wi, 2 * r_src * H, wqkv + 2 * r_dst * H, 2 * P * H);
+            seg(bi, 2 * r_src, bqkv + 2 * r_dst, 2 * P);
+          }
+      row0 += heads[pj] * D;
+    }
     seg(base + 7, 0, wo, 2 * H * QD);
     seg(base + 8, 0, ln2, 2 * H);
     const int64_t blk = 2 * GU * H;

@@ -176,6 +176,22 @@ def engine_layout(m: ModelShape) -> tuple[list[EngineTensor], int]:
     return tensors, off
 
 
+ROPE_PIECE = 32   # rows per rotation-half piece in the engine QKV layout
+
+
+def rope_pieces(head_dim: int) -> list[tuple[int, int]]:
+    """(src_row, dst_row) of the 32-row pieces of one q / k / v head in the
+    engine layout: every 64-row block holds 32 rows of the first rotation half
+    and their 32 partners (+head_dim/2), so a 64-column GEMM tile owns whole
+    RoPE pairs.  Identity for head_dim 64."""
+    hd = head_dim // 2
+    out = []
+    for t in range(hd // ROPE_PIECE):
+        out.append((t * ROPE_PIECE, 2 * t * ROPE_PIECE))
+        out.append((hd + t * ROPE_PIECE, (2 * t + 1) * ROPE_PIECE))
+    return out
+
+
 def relayout_segments(m: ModelShape) -> list[tuple[int, int, int, int]]:
     """(hf_tensor_index, src_byte_offset, dst_arena_offset, nbytes) copies that
     turn the HF tensors into the engine arena.  Every engine byte is written
@@ -193,14 +209,17 @@ def relayout_segments(m: ModelShape) -> list[tuple[int, int, int, int]]:
     for i in range(m.layers):
         p, e = f"model.layers.{i}.", f"layers.{i}."
         whole(p + "input_layernorm.weight", eng[e + "ln1"].offset, 2 * H)
-        o = eng[e + "wqkv"].offset
-        whole(p + "self_attn.q_proj.weight", o, 2 * m.q_dim * H)
-        whole(p + "self_attn.k_proj.weight", o + 2 * m.q_dim * H, 2 * m.kv_dim * H)
-        whole(p + "self_attn.v_proj.weight", o + 2 * (m.q_dim + m.kv_dim) * H, 2 * m.kv_dim * H)
-        o = eng[e + "bqkv"].offset
-        whole(p + "self_attn.q_proj.bias", o, 2 * m.q_dim)
-        whole(p + "self_attn.k_proj.bias", o + 2 * m.q_dim, 2 * m.kv_dim)
-        whole(p + "self_attn.v_proj.bias", o + 2 * (m.q_dim + m.kv_dim), 2 * m.kv_dim)
+        D, pieces = m.head_dim, rope_pieces(m.head_dim)
+        ow, ob = eng[e + "wqkv"].offset, eng[e + "bqkv"].offset
+        row0 = 0                                  # first engine row of the projection
+        for proj, heads in (("q", m.n_q_heads), ("k", m.n_kv_heads), ("v", m.n_kv_heads)):
+            wi, bi = idx[p + f"self_attn.{proj}_proj.weight"], idx[p + f"self_attn.{proj}_proj.bias"]
+            for hh in range(heads):
+                for src, dst in pieces:
+                    r_src, r_dst = hh * D + src, row0 + hh * D + dst
+                    segs.append((wi, 2 * r_src * H, ow + 2 * r_dst * H, 2 * ROPE_PIECE * H))
+                    segs.append((bi, 2 * r_src, ob + 2 * r_dst, 2 * ROPE_PIECE))
+            row0 += heads * D
         whole(p + "self_attn.o_proj.weight", eng[e + "wo"].offset, 2 * H * m.q_dim)
         whole(p + "post_attention_layernorm.weight", eng[e + "ln2"].offset, 2 * H)
         o = eng[e + "wgu"].offset
