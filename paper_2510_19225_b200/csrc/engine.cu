@@ -66,7 +66,7 @@ struct Req {
 
 struct LayerW {
   bf16 *ln1, *wqkv, *bqkv, *wo, *ln2, *wgu, *wdown;
-  CUtensorMap m_qkv, m_o, m_gu, m_gu_small, m_down;
+  CUtensorMap m_qkv, m_qkv64, m_o, m_gu, m_gu_small, m_down;
 };
 
 // GEMM tile widths per projection (N-tile of the 128 x BN UMMA tile).  A
@@ -86,6 +86,7 @@ constexpr int SMALL_ROWS = 256;
 struct TilePlan {
   int bm_qkv, bm_o, bn_gu, bm_gu, bm_down;
   bool cl_down;   // down: cluster residual add (else fp32 partials + RMSNorm sum)
+  int bn_qkv;     // 64 (twice the CTAs, whole RoPE pairs per tile) or 128
 };
 constexpr int RING_ROWS = 512;
 
@@ -255,13 +256,15 @@ struct rlb_instance {
   // others share each weight stage between two 128-row accumulators
   int bm_qkv = 128, bm_o = 128, bm_gu = 256, bm_down = 256;   // decode batch (> 256 rows)
   TilePlan plan(int R) const {
-    if (R <= 128) return {128, 128, BN_SMALL, 128, 128, cl_down};
-    if (R <= SMALL_ROWS) return {128, 128, BN_SMALL, 256, 128, cl_down};
+    const int bnq = sp_qkv == 1 ? bn_qkv_decode : BN_QKV;
+    if (R <= 128) return {128, 128, BN_SMALL, 128, 128, cl_down, bnq};
+    if (R <= SMALL_ROWS) return {128, 128, BN_SMALL, 256, 128, cl_down, bnq};
     // prefill chunks: the DSMEM reduction of thousands of split tiles costs
     // more than writing the partials (both sum the splits in the same order)
-    if (R > 512) return {256, bm_o, BN_GU, bm_gu, bm_down, cl_down_large};
-    return {bm_qkv, bm_o, BN_GU, bm_gu, bm_down, cl_down};
+    if (R > 512) return {256, bm_o, BN_GU, bm_gu, bm_down, cl_down_large, BN_QKV};
+    return {bm_qkv, bm_o, BN_GU, bm_gu, bm_down, cl_down, bm_qkv == 128 ? bnq : BN_QKV};
   }
+  int bn_qkv_decode = 64;   // RLB_QKV_BN=128 restores 128-column QKV tiles
   bool cl_down_large = false;
   int mc_gu = 1;   // gate_up A-multicast pairs at > 256 rows (RLB_GU_MC=2)
   bool last_cl_down = true;   // mode of the last forward (its head sums the partials)
@@ -379,6 +382,7 @@ int rlb_instance::init() {
     if (n == 3) cl_down_large = c != 0;
   }
   if (const char* ov = std::getenv("RLB_GU_MC")) mc_gu = std::atoi(ov) == 2 ? 2 : 1;
+  if (const char* ov = std::getenv("RLB_QKV_BN")) bn_qkv_decode = std::atoi(ov) == 128 ? 128 : 64;
   if (const char* ov = std::getenv("RLB_BM")) {   // "qkv,o,gate_up,down" (tuning; process-wide)
     int a = 0, b = 0, c = 0, d = 0;
     if (std::sscanf(ov, "%d,%d,%d,%d", &a, &b, &c, &d) == 4) {
@@ -484,6 +488,7 @@ int rlb_instance::bind_arena() {
     w.wgu = put(static_cast<int64_t>(2) * F * H);
     w.wdown = put(static_cast<int64_t>(H) * F);
     if ((rc = make_kmajor_map(&w.m_qkv, w.wqkv, QKV, H, BN_QKV))) return rc;
+    if ((rc = make_kmajor_map(&w.m_qkv64, w.wqkv, QKV, H, 64))) return rc;
     if ((rc = make_kmajor_map(&w.m_o, w.wo, H, NQ * D, BN_O))) return rc;
     if ((rc = make_kmajor_map(&w.m_gu, w.wgu, 2 * F, H, BN_GU))) return rc;
     if ((rc = make_kmajor_map(&w.m_gu_small, w.wgu, 2 * F, H, BN_SMALL))) return rc;
@@ -536,7 +541,9 @@ int rlb_instance::forward_layers(int R) {
     bf16* kv_l = kv + layer_stride * l;
     GemmParams pq{R, QKV, H, w.bqkv, nullptr, 0, sp_qkv, nullptr};
     pq.rope = RopeDst{d_row_slot, d_row_pos, d_rope, d_q, NQ * D, kv_l, d_bt, pps, NQ, NKV, D};
-    if ((rc = gemm_launch(m_xn, w.m_qkv, BN_QKV, EPI_ROPE, pq, st, tp.bm_qkv))) return rc;
+    if ((rc = gemm_launch(m_xn, tp.bn_qkv == 64 ? w.m_qkv64 : w.m_qkv, tp.bn_qkv, EPI_ROPE, pq, st,
+                          tp.bm_qkv)))
+      return rc;
     AttnArgs a{d_q, NQ * D, kv_l, d_bt, pps, d_row_slot, d_row_pos, R, NQ, NKV, D, max_splits,
                d_ws, d_attn, NQ * D};
     if ((rc = attention_launch(a, st))) return rc;
@@ -1233,7 +1240,8 @@ int rlb_profile_kernel(rlb_instance* h, int32_t which, int32_t iters, double* av
         pq.rope = RopeDst{h->d_row_slot, h->d_row_pos, h->d_rope, h->d_q, NQ * D, h->kv_scratch(),
                           h->d_bt, h->pps, NQ, h->NKV, D};
         pq.dbg = h->d_dbg;
-        return gemm_launch(h->m_xn, w.m_qkv, BN_QKV, EPI_ROPE, pq, h->st, tp.bm_qkv);
+        return gemm_launch(h->m_xn, tp.bn_qkv == 64 ? w.m_qkv64 : w.m_qkv, tp.bn_qkv, EPI_ROPE,
+                           pq, h->st, tp.bm_qkv);
       }
       case 4: return h->proj(h->m_attn, w.m_o, BN_O, h->sp_o, h->cl_o ? EPI_RESADD : EPI_PARTIAL,
                              R, H, NQ * D, nullptr, h->d_part, H, tp.bm_o);

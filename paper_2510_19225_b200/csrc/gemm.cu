@@ -50,7 +50,7 @@ struct GemmCfg {
   static constexpr int A_BYTES = HM * BK * 2;          // one accumulator's rows
   static constexpr int B_BYTES = BN * BK * 2;
   static constexpr int STAGE_BYTES = NACC * A_BYTES + B_BYTES;
-  static constexpr int STAGES = BN == 256 ? 3 : (NACC == 2 ? 4 : 6);
+  static constexpr int STAGES = BN == 256 ? 3 : (NACC == 2 ? 4 : (BN == 64 ? 8 : 6));
   static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 256;
   static constexpr uint32_t TMEM_COLS = NACC * BN;
 };
@@ -785,7 +785,8 @@ int gemm_prepare() {
   if (done[dev & 63]) return RLB_OK;
   int rc;
   if ((rc = set_attr_bn<128, 2>()) || (rc = set_attr_bn<256, 2>()) || (rc = set_attr_bn<128, 1>()) ||
-      (rc = set_attr_bn<256, 1>()) || (rc = set_attr<256, EPI_SWIGLU, 2, 2>()))
+      (rc = set_attr_bn<256, 1>()) || (rc = set_attr<256, EPI_SWIGLU, 2, 2>()) ||
+      (rc = set_attr<64, EPI_ROPE, 1>()))
     return rc;
   done[dev & 63] = true;
   return RLB_OK;
@@ -857,9 +858,14 @@ int gemm_launch(const CUtensorMap& a, const CUtensorMap& b, int block_n, int epi
                 (cluster_epi(epi) && block_n == 128 && p.splits <= 8),
             RLB_ERR_ARG,
             "split-K needs EPI_PARTIAL (workspace) or a cluster epilogue (BN=128, <= 8 splits)");
-  RLB_CHECK(epi != EPI_ROPE || (block_n == 128 && p.bias != nullptr && p.N % 128 == 0 &&
-                                128 % p.rope.d == 0),
-            RLB_ERR_ARG, "EPI_ROPE needs 128-column head tiles and a bias");
+  RLB_CHECK(epi != EPI_ROPE || ((block_n == 128 || block_n == 64) && p.bias != nullptr &&
+                                p.N % block_n == 0 && (p.rope.d == 64 || p.rope.d == 128)),
+            RLB_ERR_ARG, "EPI_ROPE needs 64/128-column tiles, head_dim 64/128 and a bias");
+  if (block_n == 64) {   // the narrow tile exists for single-split RoPE (decode QKV)
+    RLB_CHECK(epi == EPI_ROPE && block_m == 128 && p.splits == 1, RLB_ERR_ARG,
+              "64-column tiles: RoPE epilogue, 128-row tiles, no split");
+    return launch_one<64, EPI_ROPE, 1>(a, b, p, st);
+  }
   RLB_CHECK(epi != EPI_SWIGLU || (block_n % 128 == 0 && p.N % 128 == 0), RLB_ERR_ARG,
             "SwiGLU GEMM needs 128-column gate/up tiles");
   RLB_CHECK(block_m == 128 || block_m == 256, RLB_ERR_ARG, "block_m must be 128 or 256");
