@@ -43,6 +43,8 @@ int make_kmajor_map(CUtensorMap* map, const void* ptr, int64_t rows, int64_t k, 
 int gemm_prepare();  // set smem attributes of every GEMM variant on the current device
 int gemm_launch(const CUtensorMap& a, const CUtensorMap& b, int block_n, int epi,
                 const GemmParams& p, cudaStream_t st, int block_m = 256, int a_multicast = 1);
+int gemm_launch_pair(const CUtensorMap& a, const CUtensorMap& b128, int epi, const GemmParams& p,
+                     cudaStream_t st);
 
 // ---- elementwise / attention launchers (kernels.cu) ----
 struct AttnArgs {

@@ -117,3 +117,17 @@ def test_gemm_swiglu_a_multicast_pairs(dev, monkeypatch):
     monkeypatch.setenv("RLB_GEMM_MC", "1")
     out = gemm(dev, A, wgu, epilogue=2, block_n=256)
     assert torch.equal(out, ref)
+
+
+@pytest.mark.parametrize("M", [512, 300, 1024, 77])
+def test_gemm_swiglu_pair_tiles(dev, monkeypatch, M):
+    """2-SM pair tiles (cta_group::2, 512 x 256 per cluster): same bits as
+    the single-SM kernel."""
+    from paper_2510_19225_b200.instance import gemm
+    F, K = 8960, 1536
+    A = _rand((M, K), 1.0, 23)
+    wgu = _rand((2 * F, K), 0.05, 24)
+    ref = gemm(dev, A, wgu, epilogue=2, block_n=256)
+    monkeypatch.setenv("RLB_GEMM_PAIR", "1")
+    out = gemm(dev, A, wgu, epilogue=2, block_n=256)
+    assert torch.equal(out, ref)
