@@ -363,9 +363,9 @@ int rlb_instance::init() {
     int a = 0, b = 0, c = 0;
     if (std::sscanf(ov, "%d,%d,%d", &a, &b, &c) == 3) {
       const int kq = H / 64, ko = NQ * D / 64, kd = F / 64;
-      RLB_CHECK(a >= 1 && a <= 8 && kq % a == 0 && b >= 1 && b <= 8 && ko % b == 0 && c >= 1 &&
-                    c <= 8 && kd % c == 0,
-                RLB_ERR_ARG, "RLB_SPLITS must divide the K blocks (<= 8)");
+      RLB_CHECK(a >= 1 && a <= 8 && kq >= 4 * a && b >= 1 && b <= 8 && ko >= 4 * b && c >= 1 &&
+                    c <= 8 && kd >= 4 * c,
+                RLB_ERR_ARG, "RLB_SPLITS: 1..8 splits of >= 4 K blocks");
       sp_qkv = a;
       sp_o = b;
       sp_down = c;

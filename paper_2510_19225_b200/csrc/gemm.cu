@@ -396,8 +396,10 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   };
   if (stamp && threadIdx.x == 0) p.dbg[0] = gtime();
   const int nk_total = p.K / BK;
-  const int nk = nk_total / p.splits;          // k-blocks of this split
-  const int kb0 = blockIdx.z * nk;
+  // split z covers K blocks [z*nk/S, (z+1)*nk/S): a fixed partition of the
+  // weight's K range (uneven when S does not divide it)
+  const int kb0 = static_cast<int>(blockIdx.z) * nk_total / p.splits;
+  const int nk = (static_cast<int>(blockIdx.z) + 1) * nk_total / p.splits - kb0;
   // split-K cluster epilogue (S > 1) or direct from TMEM (S == 1)
   const bool via_cluster = kClusterEpi && p.splits > 1;
   // accumulators with at least one live row (a small-M tile skips the
@@ -1061,8 +1063,8 @@ int gemm_launch(const CUtensorMap& a, const CUtensorMap& b, int block_n, int epi
     return launch_one<256, EPI_SWIGLU, 2, 2>(a, b, p, st);
   }
   RLB_CHECK(p.K % BK == 0 && p.N % 16 == 0, RLB_ERR_ARG, "GEMM shape not tileable");
-  RLB_CHECK(p.splits >= 1 && (p.K / BK) % p.splits == 0, RLB_ERR_ARG,
-            "split-K must divide the K blocks");
+  RLB_CHECK(p.splits >= 1 && p.K / BK >= p.splits, RLB_ERR_ARG,
+            "split-K needs at least one K block per split");
   RLB_CHECK(p.splits == 1 || (epi == EPI_PARTIAL && p.ws != nullptr) ||
                 (cluster_epi(epi) && block_n == 128 && p.splits <= 8),
             RLB_ERR_ARG,

@@ -37,7 +37,8 @@ def test_gemm_bf16_bias(dev, M, N, K, bn, sp, bm):
 @pytest.mark.parametrize("M,N,K,bn,sp,bm", [(512, 1536, 8960, 128, 5, 256), (130, 256, 1024, 128, 1, 256),
                                             (64, 1536, 1536, 128, 6, 256), (700, 3584, 18944, 128, 2, 256),
                                             (512, 1536, 1536, 128, 1, 128), (300, 1536, 8960, 128, 4, 128),
-                                            (1, 1536, 8960, 128, 7, 128), (200, 512, 1024, 256, 1, 256)])
+                                            (1, 1536, 8960, 128, 7, 128), (200, 512, 1024, 256, 1, 256),
+                                            (512, 1536, 8960, 128, 6, 256), (300, 1536, 8960, 128, 8, 256)])
 def test_gemm_residual_add(dev, M, N, K, bn, sp, bm):
     """fp32 h += A.B^T; split-K (block_n 128) reduces its splits in a cluster."""
     from paper_2510_19225_b200.instance import gemm
