@@ -2,9 +2,13 @@
 //
 //   C[M, N] = A[M, K] . B[N, K]^T      (A = activations, B = weights; both K-major bf16)
 //
-// One CTA computes a 256 x BN tile as two 128 x BN UMMA accumulators in TMEM
-// that share every B stage (the B tile is read from L2 once per 256 rows, so
-// a decode step at M=512 reads each weight tile twice, not four times).
+// One CTA computes a (128 * NACC) x BN tile: NACC = 2 gives two 128 x BN UMMA
+// accumulators in TMEM that share every B stage (a weight tile is read once
+// per 256 rows); NACC = 1 gives twice the CTAs for the short projections,
+// which are bound by how fast one SM's shared memory can be fed.  BN is 256,
+// 128 or (RoPE only) 64.  Experiments kept off by default: A-tile multicast
+// across N-tile pairs (MC = 2) and 2-SM pair tiles (gemm_pair_tc); see
+// DESIGN.md §9 for their measurements.
 // Warp roles (384 threads):
 //   warp 0      one elected lane issues TMA loads: A rows [m, m+128), A rows
 //               [m+128, m+256) and B rows [n, n+BN), 64-element (128 B) K

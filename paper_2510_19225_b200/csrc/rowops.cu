@@ -1,7 +1,8 @@
 // K3 row kernel: residual stream -> RMSNorm -> bf16 input of the next GEMM.
-// The projections add their (cluster-reduced) split-K sums into h in their
-// epilogues, so the engine runs this with S = 0; S > 0 reduces fp32 partials
-// [S][M][N] in split order first (kept for partial-producing callers).
+// S > 0: first sum the S fp32 split-K partials [S][M][N] of the projection
+// that precedes it in split order and add them to h (the O projection at
+// decode, the down projection in prefill chunks); S = 0 when the projection
+// already added its (cluster-reduced) sum into h in its epilogue.
 #define RLB_PDL_CLASS 4
 #include "internal.h"
 
