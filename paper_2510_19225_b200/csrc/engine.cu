@@ -261,7 +261,7 @@ struct rlb_instance {
     if (R <= SMALL_ROWS) return {128, 128, BN_SMALL, 256, 128, cl_down, bnq};
     // prefill chunks: the DSMEM reduction of thousands of split tiles costs
     // more than writing the partials (both sum the splits in the same order)
-    if (R > 512) return {256, bm_o, BN_GU, bm_gu, bm_down, cl_down_large, BN_QKV};
+    if (R > 512) return {256, 256, BN_GU, bm_gu, bm_down, cl_down_large, BN_QKV};
     return {bm_qkv, bm_o, BN_GU, bm_gu, bm_down, cl_down, bm_qkv == 128 ? bnq : BN_QKV};
   }
   int bn_qkv_decode = 64;   // RLB_QKV_BN=128 restores 128-column QKV tiles
