@@ -115,3 +115,38 @@ def test_swap_refused_with_requests_in_flight():
     inst.generate("r", [1, 2, 3], target_len=4)
     with pytest.raises(RlbStateError):
         inst.swap_weights()
+
+
+def test_seeding_handoff_to_remotes():
+    """Local engines serve first (ungated); when the remotes are Active,
+    end_seeding hands every local request to them with its prefix, and each
+    completes exactly like an uninterrupted continuation."""
+    m = RolloutManager(theta=6, m_b=4, log=EventLog())
+    m.n_prem_cap = 2
+    pool = TransferPool(build_agents(1, 2, 900e9))
+    run = RolloutRunner(m, pool, flush_steps=4, max_inflight=6)
+    m.begin_step(1, run.now())
+    pool.stage(1, source={"weights": "v1"}, now=run.now())
+    for k in range(2):
+        run.add_local_engine(f"local{k:02d}", FakeInstance(vocab=997, max_slots=6))
+    ps = prompts(20, seed=9)
+    for k, p in enumerate(ps):
+        run.submit(f"r{k}", p, target_len=25)
+    for _ in range(3):                      # seeding: only the local engines serve
+        run.pump()
+        run.advance()
+    assert all(m.owner[r].startswith("local") for r in m.owner)
+    for k in range(2):
+        assert run.add_instance(f"i{k}", FakeInstance(vocab=997, max_slots=6))
+    handed = run.end_seeding()
+    assert handed > 0 and not m.local_ids
+    run.run()
+    recs = m.log.records
+    assert any(r["type"] == "seeding_end" and r["handed_off"] == handed for r in recs)
+    assert sum(1 for r in recs if r["type"] == "migrate_out" and r["reason"] == "seed_handoff") == handed
+    assert assert_token_conservation(recs) == 20
+    assert assert_version_gating(recs) > 0
+    probe = FakeInstance(vocab=997)
+    for k, p in enumerate(ps):
+        assert m.requests[f"r{k}"].generated == reference_continuation(probe, p, 25)
+    run.close()
