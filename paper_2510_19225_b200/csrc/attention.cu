@@ -262,6 +262,248 @@ __global__ void __launch_bounds__(WARPS * 32, ATTN_MINB) attn_mma_kernel(AttnArg
   }
 }
 
+// Prefill variant: one CTA serves two consecutive token rows (2p, 2p+1) of
+// the same sequence, the second row's GQA group in MMA rows 8..15 (zero in
+// the decode kernel), so every K/V chunk is loaded once for both.  Each row
+// keeps its own online-softmax state and skips the chunks that hold none of
+// its positions -- so it goes through exactly the chunk sequence, masking,
+// warp split and merge order of the decode kernel and gets the same bits
+// (the varlen-resume invariant).  Rows of different sequences (a pair that
+// straddles a sequence boundary) run as two single-row passes.
+__device__ __forceinline__ void mma_bf16_full(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2,
+                                              uint32_t a3, uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%0,%1,%2,%3};"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+
+template <int D>
+__global__ void __launch_bounds__(WARPS * 32, 2) attn_pair_kernel(AttnArgs a) {
+  constexpr int ROWB = D * 2;
+  constexpr int CPR = ROWB / 16;
+  constexpr int KSTEPS = D / 16;
+  constexpr int NT = D / 8;
+  constexpr int STAGE_BYTES = 2 * CHUNK * ROWB;
+  constexpr int WARP_SMEM = STAGES * STAGE_BYTES;
+  extern __shared__ __align__(128) uint8_t smem[];
+
+  const int ws_idx = blockIdx.x, kvh = blockIdx.y;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int G = a.NQ / a.NKV;
+  pdl_trigger();
+  pdl_wait();
+  const int rA = 2 * blockIdx.z;
+  const bool hasB = rA + 1 < a.R;
+  const bool shared = hasB && a.row_slot[rA] == a.row_slot[rA + 1];
+  const float scale = rsqrtf(static_cast<float>(D)) * 1.4426950408889634f;
+  const int w0 = ws_idx * SUPER;
+  const int h = lane >> 2;
+
+  // pass 0: rows A (and B when it shares A's sequence); pass 1: row B alone
+  for (int pass = 0; pass < (hasB && !shared ? 2 : 1); ++pass) {
+    const int r0 = rA + pass;                              // MMA rows 0..7
+    const bool two = pass == 0 && shared;                  // MMA rows 8..15 = row rA + 1
+    const int n0 = a.row_pos[r0] + 1;
+    const int n1 = two ? a.row_pos[rA + 1] + 1 : 0;
+    const int wn0 = min(SUPER, n0 - w0), wn1 = two ? min(SUPER, n1 - w0) : 0;
+    const int wn = max(wn0, wn1);
+    if (wn <= 0) continue;
+
+    uint32_t qa[KSTEPS][4];
+    {
+      const bf16* q0 = a.q + static_cast<size_t>(r0) * a.ldq + static_cast<size_t>(kvh * G + h) * D;
+      const bf16* q1 = a.q + static_cast<size_t>(rA + 1) * a.ldq + static_cast<size_t>(kvh * G + h) * D;
+#pragma unroll
+      for (int kk = 0; kk < KSTEPS; ++kk) {
+        const int c = kk * 16 + 2 * (lane & 3);
+        qa[kk][0] = h < G && wn0 > 0 ? *reinterpret_cast<const uint32_t*>(q0 + c) : 0u;
+        qa[kk][2] = h < G && wn0 > 0 ? *reinterpret_cast<const uint32_t*>(q0 + c + 8) : 0u;
+        qa[kk][1] = h < G && wn1 > 0 ? *reinterpret_cast<const uint32_t*>(q1 + c) : 0u;
+        qa[kk][3] = h < G && wn1 > 0 ? *reinterpret_cast<const uint32_t*>(q1 + c + 8) : 0u;
+      }
+    }
+    const int npages = (wn + PAGE - 1) / PAGE;
+    const int nseg = npages > warp ? (npages - warp + WARPS - 1) / WARPS : 0;
+    int my_page = 0;
+    if (lane < nseg) {
+      const int pg = w0 / PAGE + warp + lane * WARPS;
+      my_page = a.block_table[static_cast<size_t>(a.row_slot[r0]) * a.bt_stride + pg];
+    }
+    const int last_seg_tokens = nseg > 0 ? min(PAGE, wn - (warp + (nseg - 1) * WARPS) * PAGE) : 0;
+    const int nchunks = nseg > 0 ? (nseg - 1) * (PAGE / CHUNK) + (last_seg_tokens + CHUNK - 1) / CHUNK : 0;
+    uint8_t* wsm = smem + warp * WARP_SMEM;
+    const uint32_t wsm_u32 = smem_u32(wsm);
+    const size_t head_off = static_cast<size_t>(kvh) * (2 * PAGE * D);
+    const size_t page_stride = static_cast<size_t>(a.NKV) * (2 * PAGE * D);
+    auto issue = [&](int c) {
+      const int seg = c >> 2;
+      const int page = __shfl_sync(0xffffffffu, my_page, seg);
+      const int seg_tok = min(PAGE, wn - (warp + seg * WARPS) * PAGE);
+      const bf16* kp = a.kv + static_cast<size_t>(page) * page_stride + head_off;
+      const uint32_t st = wsm_u32 + (c % STAGES) * STAGE_BYTES;
+#pragma unroll
+      for (int i = 0; i < (CHUNK * CPR) / 32; ++i) {
+        const int idx = i * 32 + lane;
+        const int row = idx / CPR, ch = idx % CPR;
+        const int tok = (c & 3) * CHUNK + row;
+        const bool ok = tok < seg_tok;
+        const bf16* src = kp + static_cast<size_t>(ok ? tok : 0) * D + ch * 8;
+        const uint32_t off = row * ROWB + ((ch ^ (row & 7)) << 4);
+        cp_async16(st + off, src, ok);
+        cp_async16(st + CHUNK * ROWB + off, src + PAGE * D, ok);
+      }
+    };
+
+    float o[NT][4];
+#pragma unroll
+    for (int t = 0; t < NT; ++t) o[t][0] = o[t][1] = o[t][2] = o[t][3] = 0.f;
+    float m_run[2] = {-INFINITY, -INFINITY}, l_run[2] = {0.f, 0.f};
+#pragma unroll
+    for (int c = 0; c < STAGES - 1; ++c) {
+      if (c < nchunks) issue(c);
+      cp_commit();
+    }
+    for (int c = 0; c < nchunks; ++c) {
+      if (c + STAGES - 1 < nchunks) issue(c + STAGES - 1);
+      cp_commit();
+      cp_wait<STAGES - 1>();
+      __syncwarp();
+      const uint32_t ks = wsm_u32 + (c % STAGES) * STAGE_BYTES;
+      const uint32_t vs = ks + CHUNK * ROWB;
+      const int pstart = (warp + (c >> 2) * WARPS) * PAGE;   // window position of the page
+      const int tok0 = (c & 3) * CHUNK;
+      float s[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
+      {
+        const int mi = lane >> 3, ri = lane & 7;
+        const int row = (mi >> 1) * 8 + ri;
+#pragma unroll
+        for (int kk = 0; kk < KSTEPS; ++kk) {
+          const int ch = 2 * kk + (mi & 1);
+          uint32_t b[4];
+          ldsm_x4(ks + row * ROWB + ((ch ^ (row & 7)) << 4), b);
+          mma_bf16_full(s[0], qa[kk][0], qa[kk][1], qa[kk][2], qa[kk][3], b[0], b[1]);
+          mma_bf16_full(s[1], qa[kk][0], qa[kk][1], qa[kk][2], qa[kk][3], b[2], b[3]);
+        }
+      }
+      // per row x (0: MMA rows 0-7, 1: rows 8-15): online softmax over the
+      // chunk exactly as the decode kernel does, or no update at all when the
+      // chunk holds none of the row's positions
+      uint32_t pa[2][2];
+      float corr[2];
+#pragma unroll
+      for (int x = 0; x < 2; ++x) {
+        const int wnx = x == 0 ? wn0 : wn1;
+        const int seg_tok = min(PAGE, wnx - pstart);
+        const bool active = pstart + tok0 < wnx;             // a valid position in the chunk
+        float mx = -INFINITY;
+#pragma unroll
+        for (int j = 0; j < 2; ++j)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int tok = tok0 + 8 * j + 2 * (lane & 3) + e;
+            s[j][2 * x + e] = tok < seg_tok ? s[j][2 * x + e] * scale : -INFINITY;
+            mx = fmaxf(mx, s[j][2 * x + e]);
+          }
+        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
+        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
+        float p[2][2] = {{0.f, 0.f}, {0.f, 0.f}};
+        corr[x] = 1.f;
+        if (active) {
+          const float m_new = fmaxf(m_run[x], mx);
+          corr[x] = exp2f(m_run[x] - m_new);
+          float rs = 0.f;
+#pragma unroll
+          for (int j = 0; j < 2; ++j)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+              p[j][e] = exp2f(s[j][2 * x + e] - m_new);
+              rs += p[j][e];
+            }
+          rs += __shfl_xor_sync(0xffffffffu, rs, 1);
+          rs += __shfl_xor_sync(0xffffffffu, rs, 2);
+          l_run[x] = __fmaf_rn(l_run[x], corr[x], rs);
+          m_run[x] = m_new;
+        }
+        pa[x][0] = pack_bf2(p[0][0], p[0][1]);
+        pa[x][1] = pack_bf2(p[1][0], p[1][1]);
+      }
+#pragma unroll
+      for (int t = 0; t < NT; ++t) {
+        o[t][0] *= corr[0];
+        o[t][1] *= corr[0];
+        o[t][2] *= corr[1];
+        o[t][3] *= corr[1];
+      }
+      {
+        const int mi = lane >> 3, ri = lane & 7;
+        const int row = (mi & 1) * 8 + ri;
+#pragma unroll
+        for (int dt = 0; dt < NT / 2; ++dt) {
+          const int ch = 2 * dt + (mi >> 1);
+          uint32_t b[4];
+          ldsm_x4_t(vs + row * ROWB + ((ch ^ (row & 7)) << 4), b);
+          mma_bf16_full(o[2 * dt], pa[0][0], pa[1][0], pa[0][1], pa[1][1], b[0], b[1]);
+          mma_bf16_full(o[2 * dt + 1], pa[0][0], pa[1][0], pa[0][1], pa[1][1], b[2], b[3]);
+        }
+      }
+      __syncwarp();
+    }
+    cp_wait<0>();
+    __syncthreads();
+
+    // merge the 4 warp partials of each row in warp order
+    float* red = reinterpret_cast<float*>(smem);                 // [WARPS][16][D]
+    float* mls = red + WARPS * 16 * D;                             // [WARPS][16][2]
+    {
+#pragma unroll
+      for (int t = 0; t < NT; ++t) {
+        const int col = t * 8 + 2 * (lane & 3);
+        *reinterpret_cast<float2*>(&red[(warp * 16 + h) * D + col]) = make_float2(o[t][0], o[t][1]);
+        *reinterpret_cast<float2*>(&red[(warp * 16 + 8 + h) * D + col]) = make_float2(o[t][2], o[t][3]);
+      }
+      if ((lane & 3) == 0) {
+        mls[(warp * 16 + h) * 2] = m_run[0];
+        mls[(warp * 16 + h) * 2 + 1] = l_run[0];
+        mls[(warp * 16 + 8 + h) * 2] = m_run[1];
+        mls[(warp * 16 + 8 + h) * 2 + 1] = l_run[1];
+      }
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < 2 * G * D; i += WARPS * 32) {
+      const int x = i / (G * D), g = (i / D) % G, d = i % D;
+      if (x == 1 && !two) break;
+      const int rr = x == 0 ? r0 : rA + 1;
+      const int n = x == 0 ? n0 : n1;
+      if (w0 >= n) continue;                                   // no positions in this window
+      const int slot = x * 8 + g;
+      float M = -INFINITY;
+#pragma unroll
+      for (int w = 0; w < WARPS; ++w) M = fmaxf(M, mls[(w * 16 + slot) * 2]);
+      float L = 0.f, O = 0.f;
+#pragma unroll
+      for (int w = 0; w < WARPS; ++w) {
+        const float cw = exp2f(mls[(w * 16 + slot) * 2] - M);
+        L = __fmaf_rn(cw, mls[(w * 16 + slot) * 2 + 1], L);
+        O = __fmaf_rn(cw, red[(w * 16 + slot) * D + d], O);
+      }
+      const int qh = kvh * G + g;
+      if (n <= SUPER) {
+        a.out[static_cast<size_t>(rr) * a.ldo + qh * D + d] = __float2bfloat16_rn(O / L);
+      } else {
+        float* wsp = a.ws + ((static_cast<size_t>(rr) * a.NQ + qh) * a.max_splits + ws_idx) * (D + 2);
+        wsp[d] = O;
+        if (d == 0) {
+          wsp[D] = M;
+          wsp[D + 1] = L;
+        }
+      }
+    }
+    __syncthreads();                                           // smem reused by the next pass
+  }
+}
+
 // Merge the per-window partials of rows longer than one window, in order.
 __global__ void attn_combine_kernel(AttnArgs a) {
   pdl_trigger();
@@ -286,30 +528,39 @@ __global__ void attn_combine_kernel(AttnArgs a) {
 int attention_windows(int max_seq) { return (max_seq + SUPER - 1) / SUPER; }
 
 template <int D>
-static int launch_attn(const AttnArgs& a, cudaStream_t st) {
+static int launch_attn(const AttnArgs& a, cudaStream_t st, bool pairs) {
   constexpr int smem_pipe = WARPS * STAGES * 2 * CHUNK * D * 2;
   constexpr int smem_red = WARPS * 8 * D * 4 + WARPS * 8 * 2 * 4;
   constexpr int smem = smem_pipe > smem_red ? smem_pipe : smem_red;
+  constexpr int smem_red2 = WARPS * 16 * D * 4 + WARPS * 16 * 2 * 4;
+  constexpr int smem2 = smem_pipe > smem_red2 ? smem_pipe : smem_red2;
   static bool attr[64] = {false};
   int dev = 0;
   RLB_CUDA(cudaGetDevice(&dev));
   if (!attr[dev & 63]) {
     RLB_CUDA(cudaFuncSetAttribute(attn_mma_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    RLB_CUDA(cudaFuncSetAttribute(attn_pair_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  smem2));
     attr[dev & 63] = true;
   }
-  RLB_CUDA(launch_k(attn_mma_kernel<D>, dim3(a.max_splits, a.NKV, a.R), dim3(WARPS * 32), smem,
-                    st, a));
+  if (pairs) {
+    RLB_CUDA(launch_k(attn_pair_kernel<D>, dim3(a.max_splits, a.NKV, (a.R + 1) / 2),
+                      dim3(WARPS * 32), smem2, st, a));
+  } else {
+    RLB_CUDA(launch_k(attn_mma_kernel<D>, dim3(a.max_splits, a.NKV, a.R), dim3(WARPS * 32), smem,
+                      st, a));
+  }
   return RLB_OK;
 }
 
-int attention_launch(const AttnArgs& a, cudaStream_t st) {
+int attention_launch(const AttnArgs& a, cudaStream_t st, bool row_pairs) {
   if (a.R <= 0) return RLB_OK;
   RLB_CHECK(a.NQ % a.NKV == 0 && a.NQ / a.NKV <= 8, RLB_ERR_ARG, "GQA group must be <= 8");
   int rc;
   if (a.D == 128)
-    rc = launch_attn<128>(a, st);
+    rc = launch_attn<128>(a, st, row_pairs);
   else if (a.D == 64)
-    rc = launch_attn<64>(a, st);
+    rc = launch_attn<64>(a, st, row_pairs);
   else
     RLB_CHECK(false, RLB_ERR_ARG, "head_dim must be 64 or 128");
   if (rc) return rc;

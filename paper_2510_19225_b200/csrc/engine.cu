@@ -265,6 +265,7 @@ struct rlb_instance {
     return {bm_qkv, bm_o, BN_GU, bm_gu, bm_down, cl_down, bm_qkv == 128 ? bnq : BN_QKV};
   }
   int bn_qkv_decode = 64;   // RLB_QKV_BN=128 restores 128-column QKV tiles
+  bool attn_pairs = true;   // prefill attention on row pairs (RLB_ATTN_PAIRS=0: one row per CTA)
   bool cl_down_large = false;
   int mc_gu = 1;   // gate_up A-multicast pairs at > 256 rows (RLB_GU_MC=2)
   bool last_cl_down = true;   // mode of the last forward (its head sums the partials)
@@ -292,7 +293,8 @@ struct rlb_instance {
   ~rlb_instance();
   int init();
   int bind_arena();
-  int forward_layers(int R);
+  // prefill: rows come grouped by sequence (attention serves row pairs)
+  int forward_layers(int R, bool prefill = false);
   int head(int Lrows, bool append);
   int decode_step_launch(int R);
   int admit_and_prefill(int* rows_run);
@@ -383,6 +385,7 @@ int rlb_instance::init() {
   }
   if (const char* ov = std::getenv("RLB_GU_MC")) mc_gu = std::atoi(ov) == 2 ? 2 : 1;
   if (const char* ov = std::getenv("RLB_QKV_BN")) bn_qkv_decode = std::atoi(ov) == 128 ? 128 : 64;
+  if (const char* ov = std::getenv("RLB_ATTN_PAIRS")) attn_pairs = std::atoi(ov) != 0;
   if (const char* ov = std::getenv("RLB_BM")) {   // "qkv,o,gate_up,down" (tuning; process-wide)
     int a = 0, b = 0, c = 0, d = 0;
     if (std::sscanf(ov, "%d,%d,%d,%d", &a, &b, &c, &d) == 4) {
@@ -520,7 +523,7 @@ int rlb_instance::ensure_shadow() {
   return rc;
 }
 
-int rlb_instance::forward_layers(int R) {
+int rlb_instance::forward_layers(int R, bool prefill) {
   // Per layer:
   //   qkv  GEMM -> [sum + bias + RoPE -> q, K/V into the paged cache] in its
   //               epilogue (EPI_ROPE; splits reduced in a cluster if split)
@@ -546,7 +549,7 @@ int rlb_instance::forward_layers(int R) {
       return rc;
     AttnArgs a{d_q, NQ * D, kv_l, d_bt, pps, d_row_slot, d_row_pos, R, NQ, NKV, D, max_splits,
                d_ws, d_attn, NQ * D};
-    if ((rc = attention_launch(a, st))) return rc;
+    if ((rc = attention_launch(a, st, prefill && attn_pairs))) return rc;
     if (cl_o) {
       if ((rc = proj(m_attn, w.m_o, BN_O, sp_o, EPI_RESADD, R, H, NQ * D, nullptr, d_h, H,
                      tp.bm_o)) ||
@@ -739,7 +742,7 @@ int rlb_instance::admit_and_prefill(int* rows_run) {
     if ((rc = seed_tokens_launch(d_row_tok, d_row_pos, d_row_slot, static_cast<int>(n), d_seq_tokens,
                                  max_seq, st)))
       return rc;
-    if ((rc = forward_layers(static_cast<int>(n)))) return rc;
+    if ((rc = forward_layers(static_cast<int>(n), true))) return rc;
     if ((rc = head(nl, true))) return rc;
     stats.h2d_bytes += static_cast<int64_t>(n) * 12 + static_cast<int64_t>(nl) * 8;
     stats.kernel_launches += 1 + launches_per_forward(nl);
@@ -1334,7 +1337,7 @@ int rlb_score(rlb_instance* h, const int32_t* tokens, int32_t n, float* out_logi
     RLB_CUDA(cudaMemcpyAsync(h->d_row_tok, tok + beg, cnt * 4, cudaMemcpyHostToDevice, h->st));
     RLB_CUDA(cudaMemcpyAsync(h->d_row_pos, pos + beg, cnt * 4, cudaMemcpyHostToDevice, h->st));
     RLB_CUDA(cudaMemcpyAsync(h->d_row_slot, slot + beg, cnt * 4, cudaMemcpyHostToDevice, h->st));
-    if ((rc = h->forward_layers(cnt))) break;
+    if ((rc = h->forward_layers(cnt, true))) break;
     for (int lb = 0; lb < cnt; lb += h->max_slots) {
       const int ln = std::min(h->max_slots, cnt - lb);
       for (int i = 0; i < ln; ++i) lsrc[i] = lb + i;

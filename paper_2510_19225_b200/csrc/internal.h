@@ -56,7 +56,7 @@ struct AttnArgs {
   float* ws;                        // [R][NQ][max_splits][D+2]
   bf16* out; int ldo;
 };
-int attention_launch(const AttnArgs& a, cudaStream_t st);
+int attention_launch(const AttnArgs& a, cudaStream_t st, bool row_pairs = false);
 int attention_windows(int max_seq);   // CTA windows per row (AttnArgs.max_splits)
 
 int embed_launch(const bf16* embed, int H, const int* tok, int R, float* h, cudaStream_t st);
