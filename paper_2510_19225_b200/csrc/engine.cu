@@ -266,6 +266,13 @@ struct rlb_instance {
   }
   int bn_qkv_decode = 64;   // RLB_QKV_BN=128 restores 128-column QKV tiles
   bool attn_pairs = true;   // prefill attention on row pairs (RLB_ATTN_PAIRS=0: one row per CTA)
+  // persistent 2-SM tiles (double-buffered TMEM): bit 1 gate_up, bit 2
+  // lm_head (RLB_PAIRP).  Default: lm_head (1188 tiles: the epilogues hide
+  // behind the next tile's MMAs, 165 -> 121 us) and gate_up in prefill
+  // chunks; at a 512-row decode gate_up has ~2 tiles per cluster and gains
+  // nothing.  Same bits as the single-SM kernels.
+  int pairp = 2;
+  bool pairp_prefill = true;
   bool cl_down_large = false;
   int mc_gu = 1;   // gate_up A-multicast pairs at > 256 rows (RLB_GU_MC=2)
   bool last_cl_down = true;   // mode of the last forward (its head sums the partials)
@@ -386,6 +393,8 @@ int rlb_instance::init() {
   if (const char* ov = std::getenv("RLB_GU_MC")) mc_gu = std::atoi(ov) == 2 ? 2 : 1;
   if (const char* ov = std::getenv("RLB_QKV_BN")) bn_qkv_decode = std::atoi(ov) == 128 ? 128 : 64;
   if (const char* ov = std::getenv("RLB_ATTN_PAIRS")) attn_pairs = std::atoi(ov) != 0;
+  if (const char* ov = std::getenv("RLB_PAIRP")) pairp = std::atoi(ov);
+  if (const char* ov = std::getenv("RLB_PAIRP_PREFILL")) pairp_prefill = std::atoi(ov) != 0;
   if (const char* ov = std::getenv("RLB_BM")) {   // "qkv,o,gate_up,down" (tuning; process-wide)
     int a = 0, b = 0, c = 0, d = 0;
     if (std::sscanf(ov, "%d,%d,%d,%d", &a, &b, &c, &d) == 4) {
@@ -567,9 +576,12 @@ int rlb_instance::forward_layers(int R, bool prefill) {
       GemmParams pg{R, 2 * F, H, nullptr, d_act, F, 1, d_part};
       const bool mc = mc_gu == 2 && tp.bn_gu == BN_GU && tp.bm_gu == 256 &&
                       ((2 * F) / BN_GU) % 2 == 0;
-      if ((rc = gemm_launch(m_xn, tp.bn_gu == BN_SMALL ? w.m_gu_small : w.m_gu, tp.bn_gu,
-                            EPI_SWIGLU, pg, st, tp.bm_gu, mc ? 2 : 1)))
+      if (((pairp & 1) || (R > 512 && pairp_prefill)) && tp.bn_gu == BN_GU && tp.bm_gu == 256) {
+        if ((rc = gemm_launch_pairp(m_xn, w.m_gu_small, EPI_SWIGLU, pg, st))) return rc;
+      } else if ((rc = gemm_launch(m_xn, tp.bn_gu == BN_SMALL ? w.m_gu_small : w.m_gu, tp.bn_gu,
+                                   EPI_SWIGLU, pg, st, tp.bm_gu, mc ? 2 : 1))) {
         return rc;
+      }
     }
     const bool last = l + 1 == m.layers;
     if (tp.cl_down) {
@@ -616,9 +628,13 @@ int rlb_instance::head(int Lrows, bool append) {
   const bool small = Lrows > 32 && Lrows <= 128;
   const int bn = small ? BN_SMALL : BN_LM;
   const int ntiles = (V + bn - 1) / bn;
-  if ((rc = proj(m_xn, small ? m_lm_small : m_lm, bn, 1, EPI_ARGMAX, Lrows, V, H, nullptr, d_logits,
-                 ntiles, small ? 128 : 256)))
+  if ((pairp & 2) && Lrows > 128) {
+    GemmParams pl{Lrows, V, H, nullptr, d_logits, ntiles, 1, d_part};
+    if ((rc = gemm_launch_pairp(m_xn, m_lm_small, EPI_ARGMAX, pl, st))) return rc;
+  } else if ((rc = proj(m_xn, small ? m_lm_small : m_lm, bn, 1, EPI_ARGMAX, Lrows, V, H, nullptr,
+                        d_logits, ntiles, small ? 128 : 256))) {
     return rc;
+  }
   return argmax_append_launch(reinterpret_cast<const float2*>(d_logits), ntiles, Lrows,
                               d_logit_slot, d_seq_tokens, d_seq_len, d_seq_target, max_seq, d_ring,
                               d_ring_cur, max_slots, st);
@@ -1248,8 +1264,14 @@ int rlb_profile_kernel(rlb_instance* h, int32_t which, int32_t iters, double* av
       }
       case 4: return h->proj(h->m_attn, w.m_o, BN_O, h->sp_o, h->cl_o ? EPI_RESADD : EPI_PARTIAL,
                              R, H, NQ * D, nullptr, h->d_part, H, tp.bm_o);
-      case 5: return h->proj(h->m_xn, h->m_lm, BN_LM, 1, EPI_ARGMAX, R, h->V, H, nullptr,
-                             h->d_logits, (h->V + BN_LM - 1) / BN_LM);
+      case 5: {
+        if ((h->pairp & 2) && R > 128) {
+          GemmParams pl{R, h->V, H, nullptr, h->d_logits, (h->V + BN_LM - 1) / BN_LM, 1, h->d_part};
+          return gemm_launch_pairp(h->m_xn, h->m_lm_small, EPI_ARGMAX, pl, h->st);
+        }
+        return h->proj(h->m_xn, h->m_lm, BN_LM, 1, EPI_ARGMAX, R, h->V, H, nullptr, h->d_logits,
+                       (h->V + BN_LM - 1) / BN_LM);
+      }
       case 6: return resid_norm_launch(h->d_h, h->cl_down ? nullptr : h->d_part,
                                        h->cl_down ? 0 : h->sp_down, R, nullptr, R, w.ln2, H,
                                        h->m.rms_eps, h->d_xn, false, h->st);

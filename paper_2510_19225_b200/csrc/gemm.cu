@@ -932,6 +932,196 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   }
 }
 
+// Persistent 2-SM GEMM: every (2,1,1) cluster loops over 256 x 256 pair tiles
+// (CTA r: rows m*256 + r*128 + [0,128) and B rows n*256 + r*128 + [0,128)).
+// A tile's accumulator (128 x 256 per SM) lives in one of two TMEM buffers,
+// so the epilogue of tile i drains buffer i&1 while the MMAs of tile i+1 fill
+// the other -- the TMEM epilogue leaves the critical path.  The leader's MMA
+// thread waits for both CTAs' epilogue warps to release a buffer (16
+// arrivals, the peer's through the cluster) before reusing it.
+struct PairPCfg {
+  static constexpr int A_BYTES = HM * BK * 2;
+  static constexpr int B_BYTES = 128 * BK * 2;
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int STAGES = 6;
+  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 2048;   // + barriers, argmax exchange
+  static constexpr uint32_t TMEM_COLS = 512;
+};
+
+template <int EPI>
+__global__ void __launch_bounds__(GEMM_THREADS, 1)
+    gemm_pairp_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                  GemmParams p) {
+  using C = PairPCfg;
+  constexpr int BN = 256;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~static_cast<uintptr_t>(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE_BYTES);
+  uint64_t* full = bars;
+  uint64_t* empty = bars + C::STAGES;
+  uint64_t* tfull = bars + 2 * C::STAGES;          // [2]
+  uint64_t* tempty = bars + 2 * C::STAGES + 2;     // [2] (leader's copy is used)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * C::STAGES + 4);
+  float2* xchg = reinterpret_cast<float2*>(bars + 2 * C::STAGES + 6);   // [128] argmax halves
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int r = static_cast<int>(cluster_rank());
+  const int cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
+  const int m_tiles = (p.M + 255) / 256, n_tiles = (p.N + BN - 1) / BN;
+  const int ntiles = m_tiles * n_tiles;
+  const int nk = p.K / BK;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tmA);
+    tma_prefetch(&tmB);
+    for (int s = 0; s < C::STAGES; ++s) {
+      mbar_init(smem_u32(&full[s]), 1);
+      mbar_init(smem_u32(&empty[s]), 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(smem_u32(&tfull[b]), 1);
+      mbar_init(smem_u32(&tempty[b]), 16);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 2) tmem_alloc_pair(smem_u32(tmem_slot), C::TMEM_COLS);
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  pdl_trigger();
+  pdl_wait();
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int g = 0;
+      for (int t = cid; t < ntiles; t += ncl) {
+        const int mt = t % m_tiles, nt = t / m_tiles;
+        for (int kb = 0; kb < nk; ++kb, ++g) {
+          const int s = g % C::STAGES;
+          const uint32_t ph = (g / C::STAGES) & 1;
+          uint8_t* st = smem + s * C::STAGE_BYTES;
+          mbar_wait(smem_u32(&empty[s]), ph ^ 1);
+          if (r == 0) mbar_expect_tx(smem_u32(&full[s]), 2 * C::STAGE_BYTES);
+          tma_load_2d_pair(smem_u32(st + C::A_BYTES), &tmB, smem_u32(&full[s]), kb * BK,
+                           nt * BN + r * 128);
+          tma_load_2d_pair(smem_u32(st), &tmA, smem_u32(&full[s]), kb * BK, mt * 256 + r * HM);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && r == 0) {
+      constexpr uint32_t idesc = umma_idesc_bf16(256, BN);
+      int g = 0, i = 0;
+      for (int t = cid; t < ntiles; t += ncl, ++i) {
+        const int b = i & 1;
+        mbar_wait_cluster(smem_u32(&tempty[b]), ((i >> 1) & 1) ^ 1);
+        tc_fence_after();
+        for (int kb = 0; kb < nk; ++kb, ++g) {
+          const int s = g % C::STAGES;
+          const uint32_t ph = (g / C::STAGES) & 1;
+          const uint32_t st = smem_u32(smem + s * C::STAGE_BYTES);
+          mbar_wait(smem_u32(&full[s]), ph);
+          tc_fence_after();
+          const uint64_t ad = umma_desc_sw128(st), bd = umma_desc_sw128(st + C::A_BYTES);
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k)
+            umma_bf16_pair(tmem + b * BN, ad + 2 * k, bd + 2 * k, idesc, (kb | k) != 0);
+          umma_commit_pair(smem_u32(&empty[s]), 0x3);
+        }
+        umma_commit_pair(smem_u32(&tfull[b]), 0x3);
+      }
+    }
+  } else if (warp >= 4) {
+    const int q = warp & 3;                    // TMEM lane quadrant (rows)
+    const int ch = (warp - 4) >> 2;            // column half of the 256-column tile
+    const uint32_t leader_tempty = dsmem_addr(smem_u32(&tempty[0]), 0);
+    int i = 0;
+    for (int t = cid; t < ntiles; t += ncl, ++i) {
+      const int b = i & 1;
+      const int mt = t % m_tiles, nt = t / m_tiles;
+      const int m = mt * 256 + r * HM + q * 32 + lane;
+      const bool live = m < p.M;
+      const bool warp_dead = mt * 256 + r * HM + q * 32 >= p.M;
+      mbar_wait(smem_u32(&tfull[b]), (i >> 1) & 1);
+      tc_fence_after();
+      const uint32_t tbase = tmem + b * BN + ch * 128 + (static_cast<uint32_t>(q * 32) << 16);
+      if constexpr (EPI == EPI_SWIGLU) {
+        bf16* out = reinterpret_cast<bf16*>(p.out);
+#pragma unroll 1
+        for (int jc = 0; jc < (warp_dead ? 0 : 64); jc += 32) {
+          uint32_t rg[32], ru[32];
+          tmem_ld32(tbase + jc, rg);
+          tmem_ld32(tbase + 64 + jc, ru);
+          tmem_ld_wait();
+          const int col = nt * (BN / 2) + ch * 64 + jc;
+          if (live && col < p.N / 2) {
+            uint32_t pk[16];
+#pragma unroll
+            for (int e = 0; e < 16; ++e) {
+              const float a0 = silu_f(__uint_as_float(rg[2 * e])) * __uint_as_float(ru[2 * e]);
+              const float a1 = silu_f(__uint_as_float(rg[2 * e + 1])) * __uint_as_float(ru[2 * e + 1]);
+              pk[e] = pack_bf2(a0, a1);
+            }
+            uint4* dst = reinterpret_cast<uint4*>(out + static_cast<size_t>(m) * p.ldo + col);
+#pragma unroll
+            for (int e = 0; e < 4; ++e) dst[e] = make_uint4(pk[4 * e], pk[4 * e + 1], pk[4 * e + 2], pk[4 * e + 3]);
+          }
+        }
+      } else if constexpr (EPI == EPI_ARGMAX) {
+        float best = -INFINITY;
+        int bidx = 0x7fffffff;
+#pragma unroll 1
+        for (int c = 0; c < (warp_dead ? 0 : 128); c += 32) {
+          uint32_t rv[32];
+          tmem_ld32(tbase + c, rv);
+          tmem_ld_wait();
+          const int n = nt * BN + ch * 128 + c;
+#pragma unroll
+          for (int e = 0; e < 32; ++e) {
+            const float v = __uint_as_float(rv[e]);
+            if (n + e < p.N && v > best) {
+              best = v;
+              bidx = n + e;
+            }
+          }
+        }
+        // the two column halves of a row meet in shared memory: the lower
+        // half wins ties (first maximum in column order, as one pass would)
+        const int xi = q * 32 + lane;
+        if (ch == 1) xchg[xi] = make_float2(best, __int_as_float(bidx));
+        asm volatile("bar.sync %0, 64;" ::"r"(1 + q) : "memory");
+        if (ch == 0 && live) {
+          const float2 o = xchg[xi];
+          if (o.x > best) {
+            best = o.x;
+            bidx = __float_as_int(o.y);
+          }
+          float2* part = reinterpret_cast<float2*>(p.out) + static_cast<size_t>(m) * p.ldo + nt;
+          *part = make_float2(best, __int_as_float(bidx));
+        }
+        asm volatile("bar.sync %0, 64;" ::"r"(1 + q) : "memory");   // xchg reusable
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) {
+        if (r == 0) mbar_arrive(smem_u32(&tempty[b]));
+        else mbar_arrive_cluster(leader_tempty + b * 8);
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc_pair(tmem, C::TMEM_COLS);
+  }
+}
+
 // ------------------------------------------------------------------ host --
 
 typedef CUresult (*PFN_encodeTiled_t)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
@@ -1003,6 +1193,10 @@ int gemm_prepare() {
                                 PairCfg::SMEM));
   RLB_CUDA(cudaFuncSetAttribute(gemm_pair_tc<EPI_ARGMAX>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 PairCfg::SMEM));
+  RLB_CUDA(cudaFuncSetAttribute(gemm_pairp_tc<EPI_SWIGLU>,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize, PairPCfg::SMEM));
+  RLB_CUDA(cudaFuncSetAttribute(gemm_pairp_tc<EPI_ARGMAX>,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize, PairPCfg::SMEM));
   done[dev & 63] = true;
   return RLB_OK;
 }
@@ -1121,6 +1315,41 @@ int gemm_launch_pair(const CUtensorMap& a, const CUtensorMap& b128, int epi, con
   return RLB_OK;
 }
 
+// Persistent 2-SM pair tiles (256 x 256 per cluster, double-buffered TMEM).
+int gemm_launch_pairp(const CUtensorMap& a, const CUtensorMap& b128, int epi, const GemmParams& p,
+                      cudaStream_t st) {
+  if (p.M <= 0) return RLB_OK;
+  RLB_CHECK(p.K % BK == 0 && p.splits == 1, RLB_ERR_ARG, "pair GEMM: K multiple of 64, no split");
+  RLB_CHECK(epi == EPI_SWIGLU || epi == EPI_ARGMAX, RLB_ERR_ARG,
+            "pair GEMM epilogues: SwiGLU, argmax");
+  RLB_CHECK(epi != EPI_SWIGLU || p.N % 256 == 0, RLB_ERR_ARG, "SwiGLU pair tiles are 256 wide");
+  static int n_sm = 0;
+  if (!n_sm) {
+    int dev = 0;
+    RLB_CUDA(cudaGetDevice(&dev));
+    RLB_CUDA(cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev));
+  }
+  const int ntiles = ((p.M + 255) / 256) * ((p.N + 255) / 256);
+  const int clusters = std::min(ntiles, n_sm / 2);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(2 * clusters, 1, 1);
+  cfg.blockDim = dim3(GEMM_THREADS);
+  cfg.dynamicSmemBytes = PairPCfg::SMEM;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled(RLB_PDL_CLASS) ? 2 : 1;
+  if (epi == EPI_SWIGLU) RLB_CUDA(cudaLaunchKernelEx(&cfg, gemm_pairp_tc<EPI_SWIGLU>, a, b128, p));
+  else RLB_CUDA(cudaLaunchKernelEx(&cfg, gemm_pairp_tc<EPI_ARGMAX>, a, b128, p));
+  return RLB_OK;
+}
+
 }  // namespace rlb
 
 // Microbenchmark: `iters` back-to-back launches of one GEMM configuration on
@@ -1155,6 +1384,8 @@ extern "C" int rlb_bench_gemm(int device, int32_t M, int32_t N, int32_t K, int32
   CUtensorMap mb128;
   if (pair && (rc = make_kmajor_map(&mb128, B, N, K, 128))) return rc;
   auto go = [&]() {
+    if (pair && std::atoi(std::getenv("RLB_GEMM_PAIR")) == 2)
+      return gemm_launch_pairp(ma, mb128, epi, p, 0);
     return pair ? gemm_launch_pair(ma, mb128, epi, p, 0)
                 : gemm_launch(ma, mb, block_n, epi, p, 0, block_m, mc);
   };
@@ -1211,7 +1442,9 @@ extern "C" int rlb_gemm(int device, int32_t M, int32_t N, int32_t K, const void*
   if (std::getenv("RLB_GEMM_PAIR") && p.splits == 1) {   // 2-SM pair tiles
     CUtensorMap mb128;
     rc = make_kmajor_map(&mb128, B, N, K, 128);
-    if (!rc) rc = gemm_launch_pair(ma, mb128, epilogue, p, 0);
+    if (!rc)
+      rc = std::atoi(std::getenv("RLB_GEMM_PAIR")) == 2 ? gemm_launch_pairp(ma, mb128, epilogue, p, 0)
+                                                        : gemm_launch_pair(ma, mb128, epilogue, p, 0);
   } else if (p.splits == 1 || (epilogue == EPI_RESADD && block_n == 128)) {
     // RESADD: cluster split-K; RLB_GEMM_MC: A-multicast pairs (SwiGLU 256x256)
     rc = gemm_launch(ma, mb, block_n, epilogue, p, 0, block_m,

@@ -45,6 +45,8 @@ int gemm_launch(const CUtensorMap& a, const CUtensorMap& b, int block_n, int epi
                 const GemmParams& p, cudaStream_t st, int block_m = 256, int a_multicast = 1);
 int gemm_launch_pair(const CUtensorMap& a, const CUtensorMap& b128, int epi, const GemmParams& p,
                      cudaStream_t st);
+int gemm_launch_pairp(const CUtensorMap& a, const CUtensorMap& b128, int epi, const GemmParams& p,
+                      cudaStream_t st);
 
 // ---- elementwise / attention launchers (kernels.cu) ----
 struct AttnArgs {
