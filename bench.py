@@ -56,6 +56,9 @@ def parse():
     ap.add_argument("--flush-steps", type=int, default=64, help="decode steps per rlb_step call")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--prefill-rows", type=int, default=16384, help="token rows per prefill chunk")
+    ap.add_argument("--strong", action="store_true",
+                    help="strong scaling: --prompts in total, split over the ranks (default: weak, "
+                         "--prompts per rank)")
     return ap.parse_args()
 
 
@@ -180,6 +183,8 @@ def main():
         multi.init_nccl_quiet(dist, torch, local)        # stdout stays one JSON line
     shape = QWEN25_1_5B
     n_prompts, new = args.prompts, args.new_tokens
+    if args.strong:                       # fixed total work: this rank's share of the prompts
+        n_prompts = args.prompts // ws + (1 if rank < args.prompts % ws else 0)
     w = synth_hf_weights(shape, seed=0, device=f"cuda:{local}")
     inst = RolloutInstance(shape, local, max_slots=n_prompts, max_seq_len=MAX_SEQ,
                            max_prefill_rows=args.prefill_rows, graph_steps=16)
@@ -258,7 +263,8 @@ def main():
             "metric": "rollout tokens/s", "value": total_tokens / dev_max, "unit": "tokens/s",
             "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": 1000.0 * dev_max / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+            "scaling": "strong" if args.strong else "weak", "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic",
             "config": {"workload": "config2: qwen2.5-1.5b-shape random-init greedy rollout, "
                                    f"{n_prompts} prompts x {new} tokens per instance, one instance per GPU",
                        "model": "qwen2.5-1.5b-shape (random init)", "prompts_per_gpu": n_prompts,
