@@ -365,9 +365,21 @@ int rlb_instance::init() {
   prefill_rows = std::max(prefill_rows, 128);
   max_rows = std::max(prefill_rows, max_slots);
   max_rows = (max_rows + 255) / 256 * 256;
-  sp_qkv = small_batch_splits(QKV, H, BN_QKV, 1);   // 128-row tiles give QKV its parallelism
+  // QKV is never split: 64-wide RoPE tiles give it its CTAs.  O / down:
+  // measured on B200 for the two shapes the configs use (scripts/sweep_bm.sh,
+  // scripts/decode_profile.py --shape; splits of 5+ CTAs per cluster stop
+  // packing into the GPCs once there are more than ~24 clusters), the
+  // rule-based pick for any other shape.
+  sp_qkv = 1;
   sp_o = small_batch_splits(H, NQ * D, BN_O, pick_splits(H, NQ * D, BN_O, 74));
   sp_down = small_batch_splits(H, F, BN_DOWN, pick_splits(H, F, BN_DOWN, 148));
+  if (H == 1536 && NQ * D == 1536 && F == 8960) {          // Qwen2.5-1.5B
+    sp_o = 3;
+    sp_down = 5;
+  } else if (H == 3584 && NQ * D == 3584 && F == 18944) {  // Qwen2.5-7B
+    sp_o = 4;
+    sp_down = 4;
+  }
   if (const char* ov = std::getenv("RLB_SPLITS")) {   // "qkv,o,down" (tuning; process-wide)
     int a = 0, b = 0, c = 0;
     if (std::sscanf(ov, "%d,%d,%d", &a, &b, &c) == 3) {
