@@ -266,3 +266,26 @@ def test_seeding_handoff_bit_exact(tiny):
     got = [m.requests[f"r{k}"].generated for k in range(len(prompts))]
     run.close()
     assert got == want
+
+
+def test_qwen7b_width_rollout_and_migration(cuda):
+    """7B widths (GQA group 7, 28 q / 4 kv heads, hidden 3584, ffn 18944, untied
+    lm_head) at 2 layers: teacher-forced parity with the oracle and bit-exact
+    migration resume -- the config 4 / 5 shape family."""
+    from paper_2510_19225_b200.shapes import ModelShape
+    shape = ModelShape("qwen2.5-7b-2L-v8192", vocab=8192, hidden=3584, layers=2, n_q_heads=28,
+                       n_kv_heads=4, head_dim=128, ffn=18_944, tied=False)
+    w = synth_hf_weights(shape, seed=3, device="cuda")
+    prompts = synth_prompts(6, shape.vocab, 64, 200, seed=13)
+    ref = _rollout(_instance(shape, w, max_slots=8, max_seq_len=512), prompts, 48)
+    oracle = Qwen2Fp32(shape, w)
+    rep = teacher_forced_compare(oracle, prompts, ref, TOL_BF16)
+    print(f"7B-width 2L: {rep.steps} steps, exemption rate {rep.exemption_rate:.4f}")
+    assert rep.ok, rep.failures[:5]
+    src = _instance(shape, w, max_slots=8, max_seq_len=512)
+    for i, p in enumerate(prompts):
+        src.generate(f"r{i}", p, target_len=48)
+    src.step(19)
+    exported = src.export_partials([f"r{i}" for i in range(len(prompts))])
+    dst = _instance(shape, w, max_slots=3, max_seq_len=512, max_prefill_rows=512)
+    assert _rollout(dst, prompts, 48, prefix=[g for _, g in exported]) == ref
