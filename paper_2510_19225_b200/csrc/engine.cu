@@ -197,6 +197,10 @@ struct rlb_instance {
   float* d_ws = nullptr;
   CUtensorMap m_xn, m_attn, m_act;
   int32_t *d_ring = nullptr, *d_ring_ctr = nullptr, *d_ring_cur = nullptr, *h_ring = nullptr;
+  // K5 export scratch (rlb_export_partials)
+  int* d_exp_slots = nullptr;
+  int64_t* d_exp_cu = nullptr;
+  int32_t* d_exp_out = nullptr;
   float2* d_rope = nullptr;
   // requests
   std::deque<Req*> pending;
@@ -318,7 +322,7 @@ rlb_instance::~rlb_instance() {
   void* bufs[] = {arena, kv, d_bt, d_seq_tokens, d_seq_len, d_seq_target, d_row_tok, d_row_pos,
                   d_row_slot, d_logit_src, d_logit_slot, d_dec_slots, d_h, d_xn, d_qkv, d_q,
                   d_attn, d_act, d_logits, d_ws, d_ring, d_ring_ctr, d_ring_cur, d_rope,
-                  d_part};
+                  d_part, d_exp_slots, d_exp_cu, d_exp_out};
   for (void* b : bufs)
     if (b) cudaFree(b);
   if (shadow.arena) cudaFree(shadow.arena);
@@ -463,6 +467,9 @@ int rlb_instance::init() {
   const size_t part = std::max({static_cast<size_t>(sp_o) * H, static_cast<size_t>(sp_down) * H});
   if ((rc = dalloc(&d_part, part * R))) return rc;
   if ((rc = dalloc(&d_ring, static_cast<size_t>(RING_ROWS) * max_slots))) return rc;
+  if ((rc = dalloc(&d_exp_slots, max_slots)) || (rc = dalloc(&d_exp_cu, max_slots + 1)) ||
+      (rc = dalloc(&d_exp_out, static_cast<size_t>(max_slots) * max_seq)))
+    return rc;
   if ((rc = dalloc(&d_ring_ctr, 1)) || (rc = dalloc(&d_ring_cur, 1))) return rc;
   RLB_CUDA(cudaMemset(d_ring, 0xff, sizeof(int32_t) * RING_ROWS * max_slots));
   RLB_CUDA(cudaMemset(d_ring_ctr, 0, sizeof(int32_t)));
@@ -1200,26 +1207,23 @@ int rlb_export_partials(rlb_instance* h, int32_t n, const uint64_t* keys, int32_
     }
   }
   if (!dslots.empty()) {
-    int* d_slots = nullptr;
-    int64_t* d_cu = nullptr;
-    int32_t* d_out = nullptr;
+    // persistent device scratch + the pinned staging buffer: no allocation on
+    // the migration path
     const int nd = static_cast<int>(dslots.size());
-    RLB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&d_slots), nd * sizeof(int), h->st));
-    RLB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&d_cu), (nd + 1) * sizeof(int64_t), h->st));
-    RLB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&d_out), std::max<int64_t>(dcu.back(), 1) * 4, h->st));
-    RLB_CUDA(cudaMemcpyAsync(d_slots, dslots.data(), nd * sizeof(int), cudaMemcpyHostToDevice, h->st));
-    RLB_CUDA(cudaMemcpyAsync(d_cu, dcu.data(), (nd + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, h->st));
-    int rc = gather_seqs_launch(d_slots, d_cu, nd, h->d_seq_tokens, h->max_seq, d_out, h->st);
+    RLB_CHECK(dcu.back() <= static_cast<int64_t>(h->stage_cap), RLB_ERR_CAPACITY,
+              "export exceeds the staging buffer");
+    RLB_CUDA(cudaMemcpyAsync(h->d_exp_slots, dslots.data(), nd * sizeof(int), cudaMemcpyHostToDevice,
+                             h->st));
+    RLB_CUDA(cudaMemcpyAsync(h->d_exp_cu, dcu.data(), (nd + 1) * sizeof(int64_t),
+                             cudaMemcpyHostToDevice, h->st));
+    int rc = gather_seqs_launch(h->d_exp_slots, h->d_exp_cu, nd, h->d_seq_tokens, h->max_seq,
+                                h->d_exp_out, h->st);
     if (rc) return rc;
-    std::vector<int32_t> buf(dcu.back());
-    RLB_CUDA(cudaMemcpyAsync(buf.data(), d_out, dcu.back() * 4, cudaMemcpyDeviceToHost, h->st));
-    RLB_CUDA(cudaFreeAsync(d_slots, h->st));
-    RLB_CUDA(cudaFreeAsync(d_cu, h->st));
-    RLB_CUDA(cudaFreeAsync(d_out, h->st));
+    RLB_CUDA(cudaMemcpyAsync(h->h_stage, h->d_exp_out, dcu.back() * 4, cudaMemcpyDeviceToHost, h->st));
     RLB_CUDA(cudaStreamSynchronize(h->st));
     for (int k = 0; k < nd; ++k) {
       const int i = didx[k];
-      std::memcpy(out_tokens + cu[i], buf.data() + dcu[k], sizeof(int32_t) * (dcu[k + 1] - dcu[k]));
+      std::memcpy(out_tokens + cu[i], h->h_stage + dcu[k], sizeof(int32_t) * (dcu[k + 1] - dcu[k]));
     }
   }
   return RLB_OK;
