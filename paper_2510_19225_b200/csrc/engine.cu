@@ -424,6 +424,14 @@ int rlb_instance::init() {
 
   RLB_CUDA(cudaSetDevice(device));
   RLB_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  {
+    // stream-ordered allocations (the pull's chunk lists) keep their memory in
+    // the pool instead of returning it to the driver at every synchronize
+    cudaMemPool_t pool;
+    RLB_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
+    uint64_t keep = ~0ull;
+    RLB_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
+  }
   RLB_CUDA(cudaEventCreate(&ev0));
   RLB_CUDA(cudaEventCreate(&ev1));
   RLB_CUDA(cudaEventCreate(&evA));
