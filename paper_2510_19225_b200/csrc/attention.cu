@@ -20,6 +20,9 @@
 #define RLB_PDL_CLASS 2
 #include "internal.h"
 
+#include <algorithm>
+#include <cstdlib>
+
 namespace rlb {
 
 namespace {
@@ -65,48 +68,70 @@ __device__ __forceinline__ void mma_bf16(float (&d)[4], uint32_t a0, uint32_t a2
 #ifndef ATTN_MINB
 #define ATTN_MINB 2   // resident CTAs per SM the register budget is cut for
 #endif
+
+// Everything one (window, kv head, row) item needs before its K/V stream:
+// q fragments, the row's length and this lane's page id (each lane holds
+// one page of its warp's share).  Loaded ahead of the item by the persistent
+// kernel, so the dependent chain row -> slot -> block table -> q is off the
+// critical path.
 template <int D>
-__global__ void __launch_bounds__(WARPS * 32, ATTN_MINB) attn_mma_kernel(AttnArgs a) {
+struct AttnItem {
+  uint32_t qa[D / 16][2];
+  int n = 0;            // context length of the row (0: nothing in this window)
+  int my_page = 0;
+};
+
+template <int D>
+__device__ __forceinline__ void attn_load_item(const AttnArgs& a, int ws_idx, int kvh, int r,
+                                               AttnItem<D>& it) {
+  constexpr int KSTEPS = D / 16;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int G = a.NQ / a.NKV;
+  const int h = lane >> 2;
+  const bf16* qrow = a.q + static_cast<size_t>(r) * a.ldq + static_cast<size_t>(kvh * G + h) * D;
+#pragma unroll
+  for (int kk = 0; kk < KSTEPS; ++kk) {
+    const int c = kk * 16 + 2 * (lane & 3);
+    it.qa[kk][0] = h < G ? *reinterpret_cast<const uint32_t*>(qrow + c) : 0u;
+    it.qa[kk][1] = h < G ? *reinterpret_cast<const uint32_t*>(qrow + c + 8) : 0u;
+  }
+  const int n = a.row_pos[r] + 1;
+  const int w0 = ws_idx * SUPER;
+  it.n = w0 >= n ? 0 : n;
+  it.my_page = 0;
+  if (it.n) {
+    const int wn = min(SUPER, n - w0);
+    const int npages = (wn + PAGE - 1) / PAGE;
+    const int nseg = npages > warp ? (npages - warp + WARPS - 1) / WARPS : 0;
+    if (lane < nseg) {
+      const int p = w0 / PAGE + warp + lane * WARPS;
+      it.my_page = a.block_table[static_cast<size_t>(a.row_slot[r]) * a.bt_stride + p];
+    }
+  }
+}
+
+// One item: stream the window's K/V pages through the warps' cp.async rings
+// (S = QK^T, online softmax, O += PV on the tensor cores), merge the four warp
+// partials in warp order, write the row's output (or the window partial).
+// Called by every thread of the CTA (it synchronises the CTA).
+template <int D>
+__device__ __forceinline__ void attn_run_item(const AttnArgs& a, int ws_idx, int kvh, int r,
+                                              const AttnItem<D>& it, uint8_t* smem) {
   constexpr int ROWB = D * 2;            // bytes per token row
   constexpr int CPR = ROWB / 16;         // 16-byte chunks per row
   constexpr int KSTEPS = D / 16;
   constexpr int NT = D / 8;              // output n-tiles
   constexpr int STAGE_BYTES = 2 * CHUNK * ROWB;      // K and V
   constexpr int WARP_SMEM = STAGES * STAGE_BYTES;
-  extern __shared__ __align__(128) uint8_t smem[];
-
-  const int ws_idx = blockIdx.x, kvh = blockIdx.y, r = blockIdx.z;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int G = a.NQ / a.NKV;
-  pdl_trigger();
-  pdl_wait();   // q and this step's K/V rows come from the previous kernel
-
-  // Q fragments first: independent of the row metadata loads below.
-  uint32_t qa[KSTEPS][2];
-  {
-    const int h = lane >> 2;
-    const bf16* qrow = a.q + static_cast<size_t>(r) * a.ldq + static_cast<size_t>(kvh * G + h) * D;
-#pragma unroll
-    for (int kk = 0; kk < KSTEPS; ++kk) {
-      const int c = kk * 16 + 2 * (lane & 3);
-      qa[kk][0] = h < G ? *reinterpret_cast<const uint32_t*>(qrow + c) : 0u;
-      qa[kk][1] = h < G ? *reinterpret_cast<const uint32_t*>(qrow + c + 8) : 0u;
-    }
-  }
-  const int n = a.row_pos[r] + 1;
+  const int n = it.n;
   const int w0 = ws_idx * SUPER;
-  if (w0 >= n) return;
   const int wn = min(SUPER, n - w0);                     // positions in this window
   const float scale = rsqrtf(static_cast<float>(D)) * 1.4426950408889634f;
-
-  // pages of this warp: window pages p = warp, warp+4, ...; prefetch their ids
   const int npages = (wn + PAGE - 1) / PAGE;
   const int nseg = npages > warp ? (npages - warp + WARPS - 1) / WARPS : 0;
-  int my_page = 0;
-  if (lane < nseg) {
-    const int p = w0 / PAGE + warp + lane * WARPS;
-    my_page = a.block_table[static_cast<size_t>(a.row_slot[r]) * a.bt_stride + p];
-  }
+  const int my_page = it.my_page;
   // chunk c of this warp: segment c/4 (window page warp + 4*(c/4)), rows 16*(c%4)..
   const int last_seg_tokens = nseg > 0 ? min(PAGE, wn - (warp + (nseg - 1) * WARPS) * PAGE) : 0;
   const int nchunks = nseg > 0 ? (nseg - 1) * (PAGE / CHUNK) + (last_seg_tokens + CHUNK - 1) / CHUNK : 0;
@@ -164,8 +189,8 @@ __global__ void __launch_bounds__(WARPS * 32, ATTN_MINB) attn_mma_kernel(AttnArg
         const int ch = 2 * kk + (mi & 1);
         uint32_t b[4];
         ldsm_x4(ks + row * ROWB + ((ch ^ (row & 7)) << 4), b);
-        mma_bf16(s[0], qa[kk][0], qa[kk][1], b[0], b[1]);
-        mma_bf16(s[1], qa[kk][0], qa[kk][1], b[2], b[3]);
+        mma_bf16(s[0], it.qa[kk][0], it.qa[kk][1], b[0], b[1]);
+        mma_bf16(s[1], it.qa[kk][0], it.qa[kk][1], b[2], b[3]);
       }
     }
     // ---- online softmax (row = lane/4, columns 2*(lane%4)+{0,1} of each n-tile)
@@ -259,6 +284,55 @@ __global__ void __launch_bounds__(WARPS * 32, ATTN_MINB) attn_mma_kernel(AttnArg
         wsp[D + 1] = L;
       }
     }
+  }
+}
+
+// One CTA per (window, kv head, row).
+template <int D>
+__global__ void __launch_bounds__(WARPS * 32, ATTN_MINB) attn_mma_kernel(AttnArgs a) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  pdl_trigger();
+  pdl_wait();   // q and this step's K/V rows come from the previous kernel
+  AttnItem<D> it;
+  attn_load_item<D>(a, blockIdx.x, blockIdx.y, blockIdx.z, it);
+  if (it.n == 0) return;
+  attn_run_item<D>(a, blockIdx.x, blockIdx.y, blockIdx.z, it, smem);
+}
+
+// Persistent variant: a grid of ~2 CTAs per SM walks the items (row-major:
+// item = (row * NKV + kv head) * windows + window); the next item's q, length
+// and page ids are loaded while the current one streams.  Same arithmetic per
+// item as attn_mma_kernel.
+template <int D>
+__global__ void __launch_bounds__(WARPS * 32, ATTN_MINB) attn_mma_persistent(AttnArgs a) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  pdl_trigger();
+  pdl_wait();
+  const int items = a.R * a.NKV * a.max_splits;
+  auto coords = [&](int i, int& ws, int& kvh, int& r) {
+    ws = i % a.max_splits;
+    kvh = (i / a.max_splits) % a.NKV;
+    r = i / (a.max_splits * a.NKV);
+  };
+  int i = blockIdx.x;
+  if (i >= items) return;
+  AttnItem<D> cur, nxt;
+  int ws, kvh, r;
+  coords(i, ws, kvh, r);
+  attn_load_item<D>(a, ws, kvh, r, cur);
+  for (; i < items; i += gridDim.x) {
+    const int in = i + gridDim.x;
+    int ws2 = 0, kvh2 = 0, r2 = 0;
+    if (in < items) {
+      coords(in, ws2, kvh2, r2);
+      attn_load_item<D>(a, ws2, kvh2, r2, nxt);     // in flight while `cur` streams
+    }
+    if (cur.n) attn_run_item<D>(a, ws, kvh, r, cur, smem);
+    __syncthreads();                                // smem free for the next item
+    cur = nxt;
+    ws = ws2;
+    kvh = kvh2;
+    r = r2;
   }
 }
 
@@ -541,11 +615,23 @@ static int launch_attn(const AttnArgs& a, cudaStream_t st, bool pairs) {
     RLB_CUDA(cudaFuncSetAttribute(attn_mma_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     RLB_CUDA(cudaFuncSetAttribute(attn_pair_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   smem2));
+    RLB_CUDA(cudaFuncSetAttribute(attn_mma_persistent<D>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     attr[dev & 63] = true;
   }
+  static int n_sm = 0;
+  if (!n_sm) RLB_CUDA(cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev));
+  static const int persist = [] {
+    const char* e = std::getenv("RLB_ATTN_PERSIST");
+    return e ? std::atoi(e) : 0;
+  }();
   if (pairs) {
     RLB_CUDA(launch_k(attn_pair_kernel<D>, dim3(a.max_splits, a.NKV, (a.R + 1) / 2),
                       dim3(WARPS * 32), smem2, st, a));
+  } else if (persist) {
+    const int items = a.R * a.NKV * a.max_splits;
+    RLB_CUDA(launch_k(attn_mma_persistent<D>, dim3(std::min(items, ATTN_MINB * n_sm)),
+                      dim3(WARPS * 32), smem, st, a));
   } else {
     RLB_CUDA(launch_k(attn_mma_kernel<D>, dim3(a.max_splits, a.NKV, a.R), dim3(WARPS * 32), smem,
                       st, a));
