@@ -259,23 +259,39 @@ struct rlb_instance {
   // CTAs, and its RoPE / KV-append epilogue runs straight from TMEM); the
   // others share each weight stage between two 128-row accumulators
   int bm_qkv = 128, bm_o = 128, bm_gu = 256, bm_down = 256;   // decode batch (> 256 rows)
+  // persistent 2-SM tiles writing split-K partials for down above the
+  // small-batch plans (bit 4) and for O in prefill chunks (bit 8): a third
+  // less operand ingress per SM than the single-SM 256 x 128 tiles, same K
+  // partition, same bits.  Measured (scripts/pair_splitk.py, 1.5B shape):
+  // down at 512 rows 22.0 us (cluster residual add) -> 14.8 us (+ ~2 us in
+  // the RMSNorm that sums the 5 partials); prefill chunk of 16k rows: down
+  // 492 -> 310 us, O 147 -> 93 us; O at 512 rows gains nothing (8.6 us).
+  bool pair_down(int R) const { return (pairp & 4) && R > SMALL_ROWS; }
+  bool pair_o(int R) const { return (pairp & 8) && R > 512; }
+  int proj_pairp(const CUtensorMap& a, const CUtensorMap& b128, int splits, int R, int N, int K) {
+    GemmParams p{R, N, K, nullptr, nullptr, 0, splits, d_part};
+    p.dbg = d_dbg;
+    return gemm_launch_pairp(a, b128, EPI_PARTIAL, p, st);
+  }
   TilePlan plan(int R) const {
     const int bnq = sp_qkv == 1 ? bn_qkv_decode : BN_QKV;
     if (R <= 128) return {128, 128, BN_SMALL, 128, 128, cl_down, bnq};
     if (R <= SMALL_ROWS) return {128, 128, BN_SMALL, 256, 128, cl_down, bnq};
     // prefill chunks: the DSMEM reduction of thousands of split tiles costs
     // more than writing the partials (both sum the splits in the same order)
-    if (R > 512) return {256, 256, BN_GU, bm_gu, bm_down, cl_down_large, BN_QKV};
-    return {bm_qkv, bm_o, BN_GU, bm_gu, bm_down, cl_down, bm_qkv == 128 ? bnq : BN_QKV};
+    if (R > 512) return {256, 256, BN_GU, bm_gu, bm_down, cl_down_large && !pair_down(R), BN_QKV};
+    return {bm_qkv, bm_o, BN_GU, bm_gu, bm_down, cl_down && !pair_down(R),
+            bm_qkv == 128 ? bnq : BN_QKV};
   }
   int bn_qkv_decode = 64;   // RLB_QKV_BN=128 restores 128-column QKV tiles
   bool attn_pairs = true;   // prefill attention on row pairs (RLB_ATTN_PAIRS=0: one row per CTA)
   // persistent 2-SM tiles (double-buffered TMEM): bit 1 gate_up, bit 2
-  // lm_head (RLB_PAIRP).  Default: lm_head (1188 tiles: the epilogues hide
-  // behind the next tile's MMAs, 165 -> 121 us) and gate_up in prefill
-  // chunks; at a 512-row decode gate_up has ~2 tiles per cluster and gains
-  // nothing.  Same bits as the single-SM kernels.
-  int pairp = 2;
+  // lm_head, bit 4 down, bit 8 O in prefill (RLB_PAIRP).  Default: lm_head
+  // (1188 tiles: the epilogues hide behind the next tile's MMAs, 165 -> 121
+  // us), down, O in prefill and gate_up in prefill chunks; at a 512-row
+  // decode gate_up has ~2 tiles per cluster and gains nothing.  Same bits as
+  // the single-SM kernels.
+  int pairp = 2 | 4 | 8;
   bool pairp_prefill = true;
   bool cl_down_large = false;
   int mc_gu = 1;   // gate_up A-multicast pairs at > 256 rows (RLB_GU_MC=2)
@@ -586,15 +602,16 @@ int rlb_instance::forward_layers(int R, bool prefill) {
     AttnArgs a{d_q, NQ * D, kv_l, d_bt, pps, d_row_slot, d_row_pos, R, NQ, NKV, D, max_splits,
                d_ws, d_attn, NQ * D};
     if ((rc = attention_launch(a, st, prefill && attn_pairs))) return rc;
-    if (cl_o) {
+    if (cl_o && !pair_o(R)) {
       if ((rc = proj(m_attn, w.m_o, BN_O, sp_o, EPI_RESADD, R, H, NQ * D, nullptr, d_h, H,
                      tp.bm_o)) ||
           (rc = resid_norm_launch(d_h, nullptr, 0, R, nullptr, R, w.ln2, H, m.rms_eps, d_xn, false,
                                   st)))
         return rc;
     } else {
-      if ((rc = proj(m_attn, w.m_o, BN_O, sp_o, EPI_PARTIAL, R, H, NQ * D, nullptr, nullptr, 0,
-                     tp.bm_o)) ||
+      if ((rc = pair_o(R) ? proj_pairp(m_attn, w.m_o, sp_o, R, H, NQ * D)
+                          : proj(m_attn, w.m_o, BN_O, sp_o, EPI_PARTIAL, R, H, NQ * D, nullptr,
+                                 nullptr, 0, tp.bm_o)) ||
           (rc = resid_norm_launch(d_h, d_part, sp_o, R, nullptr, R, w.ln2, H, m.rms_eps, d_xn, true,
                                   st)))
         return rc;
@@ -619,8 +636,9 @@ int rlb_instance::forward_layers(int R, bool prefill) {
                                            m.rms_eps, d_xn, false, st)))
         return rc;
     } else {
-      if ((rc = proj(m_act, w.m_down, BN_DOWN, sp_down, EPI_PARTIAL, R, H, F, nullptr, nullptr, 0,
-                     tp.bm_down)))
+      if ((rc = pair_down(R) ? proj_pairp(m_act, w.m_down, sp_down, R, H, F)
+                             : proj(m_act, w.m_down, BN_DOWN, sp_down, EPI_PARTIAL, R, H, F,
+                                    nullptr, nullptr, 0, tp.bm_down)))
         return rc;
       // the last layer's partials are summed by the head's norm (its rows only)
       if (!last && (rc = resid_norm_launch(d_h, d_part, sp_down, R, nullptr, R, L[l + 1].ln1, H,
@@ -1275,9 +1293,11 @@ int rlb_profile_kernel(rlb_instance* h, int32_t which, int32_t iters, double* av
       // profiled is discarded)
       case 1: return h->proj(h->m_xn, tp.bn_gu == BN_SMALL ? w.m_gu_small : w.m_gu, tp.bn_gu, 1,
                              EPI_SWIGLU, R, 2 * F, H, nullptr, h->d_act, F, tp.bm_gu);
-      case 2: return h->proj(h->m_act, w.m_down, BN_DOWN, h->sp_down,
-                             h->cl_down ? EPI_RESADD : EPI_PARTIAL, R, H, F, nullptr, h->d_part, H,
-                             tp.bm_down);
+      case 2:
+        if (h->pair_down(R)) return h->proj_pairp(h->m_act, w.m_down, h->sp_down, R, H, F);
+        return h->proj(h->m_act, w.m_down, BN_DOWN, h->sp_down,
+                       tp.cl_down ? EPI_RESADD : EPI_PARTIAL, R, H, F, nullptr, h->d_part, H,
+                       tp.bm_down);
       case 3: {
         GemmParams pq{R, h->QKV, H, w.bqkv, nullptr, 0, h->sp_qkv, nullptr};
         pq.rope = RopeDst{h->d_row_slot, h->d_row_pos, h->d_rope, h->d_q, NQ * D, h->kv_scratch(),
@@ -1286,8 +1306,10 @@ int rlb_profile_kernel(rlb_instance* h, int32_t which, int32_t iters, double* av
         return gemm_launch(h->m_xn, tp.bn_qkv == 64 ? w.m_qkv64 : w.m_qkv, tp.bn_qkv, EPI_ROPE,
                            pq, h->st, tp.bm_qkv);
       }
-      case 4: return h->proj(h->m_attn, w.m_o, BN_O, h->sp_o, h->cl_o ? EPI_RESADD : EPI_PARTIAL,
-                             R, H, NQ * D, nullptr, h->d_part, H, tp.bm_o);
+      case 4:
+        if (h->pair_o(R)) return h->proj_pairp(h->m_attn, w.m_o, h->sp_o, R, H, NQ * D);
+        return h->proj(h->m_attn, w.m_o, BN_O, h->sp_o, h->cl_o ? EPI_RESADD : EPI_PARTIAL,
+                       R, H, NQ * D, nullptr, h->d_part, H, tp.bm_o);
       case 5: {
         if ((h->pairp & 2) && R > 128) {
           GemmParams pl{R, h->V, H, nullptr, h->d_logits, (h->V + BN_LM - 1) / BN_LM, 1, h->d_part};
@@ -1296,8 +1318,8 @@ int rlb_profile_kernel(rlb_instance* h, int32_t which, int32_t iters, double* av
         return h->proj(h->m_xn, h->m_lm, BN_LM, 1, EPI_ARGMAX, R, h->V, H, nullptr, h->d_logits,
                        (h->V + BN_LM - 1) / BN_LM);
       }
-      case 6: return resid_norm_launch(h->d_h, h->cl_down ? nullptr : h->d_part,
-                                       h->cl_down ? 0 : h->sp_down, R, nullptr, R, w.ln2, H,
+      case 6: return resid_norm_launch(h->d_h, tp.cl_down ? nullptr : h->d_part,
+                                       tp.cl_down ? 0 : h->sp_down, R, nullptr, R, w.ln2, H,
                                        h->m.rms_eps, h->d_xn, false, h->st);
     }
     set_error("unknown kernel id");
@@ -1317,7 +1339,7 @@ int rlb_profile_kernel(rlb_instance* h, int32_t which, int32_t iters, double* av
     case 3: work = 2.0 * R * h->QKV * H; break;
     case 4: work = 2.0 * R * H * NQ * D; break;
     case 5: work = 2.0 * R * h->V * static_cast<double>(H); break;
-    case 6: work = R * H * (4.0 * (h->cl_down ? 1 : 1 + h->sp_down) + 2.0); break;  // bytes
+    case 6: work = R * H * (4.0 * (tp.cl_down ? 1 : 1 + h->sp_down) + 2.0); break;  // bytes
     default: RLB_CHECK(false, RLB_ERR_ARG, "unknown kernel id");
   }
   int rc = launch();  // warm

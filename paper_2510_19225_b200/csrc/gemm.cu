@@ -939,12 +939,18 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
 // the other -- the TMEM epilogue leaves the critical path.  The leader's MMA
 // thread waits for both CTAs' epilogue warps to release a buffer (16
 // arrivals, the peer's through the cluster) before reusing it.
+// EPI_PARTIAL (split-K, grid-stride over (m, n, split) tiles) gives one
+// pipeline stage to per-warp staging of the fp32 partial (32 rows x 32
+// columns at a time, written back as full 128-byte row segments).
+template <int EPI>
 struct PairPCfg {
   static constexpr int A_BYTES = HM * BK * 2;
   static constexpr int B_BYTES = 128 * BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int STAGES = 6;
-  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 2048;   // + barriers, argmax exchange
+  static constexpr int STAGES = EPI == EPI_PARTIAL ? 5 : 6;
+  static constexpr int XPITCH = 36;                                // staged fp32 row (floats)
+  static constexpr int XSTAGE = EPI == EPI_PARTIAL ? 8 * 32 * XPITCH * 4 : 0;
+  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 2048 + XSTAGE;   // + barriers, argmax exchange
   static constexpr uint32_t TMEM_COLS = 512;
 };
 
@@ -952,7 +958,7 @@ template <int EPI>
 __global__ void __launch_bounds__(GEMM_THREADS, 1)
     gemm_pairp_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                   GemmParams p) {
-  using C = PairPCfg;
+  using C = PairPCfg<EPI>;
   constexpr int BN = 256;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -970,8 +976,16 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   const int r = static_cast<int>(cluster_rank());
   const int cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
   const int m_tiles = (p.M + 255) / 256, n_tiles = (p.N + BN - 1) / BN;
-  const int ntiles = m_tiles * n_tiles;
-  const int nk = p.K / BK;
+  // split-K: split z covers K blocks [z*nkt/S, (z+1)*nkt/S) -- the single-SM
+  // kernel's partition, so every partial has the same bits
+  const int S = EPI == EPI_PARTIAL ? p.splits : 1;
+  const int ntiles = m_tiles * n_tiles * S;
+  const int nkt = p.K / BK;
+  auto krange = [&](int t, int& kb0, int& nk) {
+    const int z = t / (m_tiles * n_tiles);
+    kb0 = z * nkt / S;
+    nk = (z + 1) * nkt / S - kb0;
+  };
 
   if (warp == 0 && lane == 0) {
     tma_prefetch(&tmA);
@@ -999,16 +1013,19 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     if (lane == 0) {
       int g = 0;
       for (int t = cid; t < ntiles; t += ncl) {
-        const int mt = t % m_tiles, nt = t / m_tiles;
+        const int mt = t % m_tiles, nt = (t / m_tiles) % n_tiles;
+        int kb0, nk;
+        krange(t, kb0, nk);
         for (int kb = 0; kb < nk; ++kb, ++g) {
           const int s = g % C::STAGES;
           const uint32_t ph = (g / C::STAGES) & 1;
           uint8_t* st = smem + s * C::STAGE_BYTES;
+          const int kx = (kb0 + kb) * BK;
           mbar_wait(smem_u32(&empty[s]), ph ^ 1);
           if (r == 0) mbar_expect_tx(smem_u32(&full[s]), 2 * C::STAGE_BYTES);
-          tma_load_2d_pair(smem_u32(st + C::A_BYTES), &tmB, smem_u32(&full[s]), kb * BK,
+          tma_load_2d_pair(smem_u32(st + C::A_BYTES), &tmB, smem_u32(&full[s]), kx,
                            nt * BN + r * 128);
-          tma_load_2d_pair(smem_u32(st), &tmA, smem_u32(&full[s]), kb * BK, mt * 256 + r * HM);
+          tma_load_2d_pair(smem_u32(st), &tmA, smem_u32(&full[s]), kx, mt * 256 + r * HM);
         }
       }
     }
@@ -1020,6 +1037,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         const int b = i & 1;
         mbar_wait_cluster(smem_u32(&tempty[b]), ((i >> 1) & 1) ^ 1);
         tc_fence_after();
+        int kb0, nk;
+        krange(t, kb0, nk);
         for (int kb = 0; kb < nk; ++kb, ++g) {
           const int s = g % C::STAGES;
           const uint32_t ph = (g / C::STAGES) & 1;
@@ -1042,7 +1061,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     int i = 0;
     for (int t = cid; t < ntiles; t += ncl, ++i) {
       const int b = i & 1;
-      const int mt = t % m_tiles, nt = t / m_tiles;
+      const int mt = t % m_tiles, nt = (t / m_tiles) % n_tiles;
       const int m = mt * 256 + r * HM + q * 32 + lane;
       const bool live = m < p.M;
       const bool warp_dead = mt * 256 + r * HM + q * 32 >= p.M;
@@ -1104,6 +1123,37 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           *part = make_float2(best, __int_as_float(bidx));
         }
         asm volatile("bar.sync %0, 64;" ::"r"(1 + q) : "memory");   // xchg reusable
+      } else if constexpr (EPI == EPI_PARTIAL) {
+        // this K range's fp32 partial [z][M][N]: each 32 x 32 block goes
+        // through the warp's staging tile (row per lane in, 4 rows x 128 B
+        // per store instruction out)
+        float* xs = reinterpret_cast<float*>(smem + C::STAGES * C::STAGE_BYTES + 2048) +
+                    (warp - 4) * 32 * C::XPITCH;
+        const int z = t / (m_tiles * n_tiles);
+        float* base = p.ws + static_cast<size_t>(z) * p.M * p.N;
+        const int mrow0 = mt * 256 + r * HM + q * 32;
+#pragma unroll 1
+        for (int c = 0; c < (warp_dead ? 0 : 128); c += 32) {
+          uint32_t rv[32];
+          tmem_ld32(tbase + c, rv);
+          tmem_ld_wait();
+          float4* s4 = reinterpret_cast<float4*>(xs + lane * C::XPITCH);
+#pragma unroll
+          for (int e = 0; e < 8; ++e)
+            s4[e] = make_float4(__uint_as_float(rv[4 * e]), __uint_as_float(rv[4 * e + 1]),
+                                __uint_as_float(rv[4 * e + 2]), __uint_as_float(rv[4 * e + 3]));
+          __syncwarp();
+          const int n = nt * BN + ch * 128 + c + (lane & 7) * 4;
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            const int rr = e * 4 + (lane >> 3);
+            const int mm = mrow0 + rr;
+            if (mm < p.M && n < p.N)
+              *reinterpret_cast<float4*>(base + static_cast<size_t>(mm) * p.N + n) =
+                  *reinterpret_cast<const float4*>(xs + rr * C::XPITCH + (lane & 7) * 4);
+          }
+          __syncwarp();
+        }
       }
       tc_fence_before();
       __syncwarp();
@@ -1194,9 +1244,11 @@ int gemm_prepare() {
   RLB_CUDA(cudaFuncSetAttribute(gemm_pair_tc<EPI_ARGMAX>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 PairCfg::SMEM));
   RLB_CUDA(cudaFuncSetAttribute(gemm_pairp_tc<EPI_SWIGLU>,
-                                cudaFuncAttributeMaxDynamicSharedMemorySize, PairPCfg::SMEM));
+                                cudaFuncAttributeMaxDynamicSharedMemorySize, PairPCfg<EPI_SWIGLU>::SMEM));
   RLB_CUDA(cudaFuncSetAttribute(gemm_pairp_tc<EPI_ARGMAX>,
-                                cudaFuncAttributeMaxDynamicSharedMemorySize, PairPCfg::SMEM));
+                                cudaFuncAttributeMaxDynamicSharedMemorySize, PairPCfg<EPI_ARGMAX>::SMEM));
+  RLB_CUDA(cudaFuncSetAttribute(gemm_pairp_tc<EPI_PARTIAL>,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize, PairPCfg<EPI_PARTIAL>::SMEM));
   done[dev & 63] = true;
   return RLB_OK;
 }
@@ -1319,9 +1371,11 @@ int gemm_launch_pair(const CUtensorMap& a, const CUtensorMap& b128, int epi, con
 int gemm_launch_pairp(const CUtensorMap& a, const CUtensorMap& b128, int epi, const GemmParams& p,
                       cudaStream_t st) {
   if (p.M <= 0) return RLB_OK;
-  RLB_CHECK(p.K % BK == 0 && p.splits == 1, RLB_ERR_ARG, "pair GEMM: K multiple of 64, no split");
-  RLB_CHECK(epi == EPI_SWIGLU || epi == EPI_ARGMAX, RLB_ERR_ARG,
-            "pair GEMM epilogues: SwiGLU, argmax");
+  RLB_CHECK(p.K % BK == 0 && (p.splits == 1 || epi == EPI_PARTIAL), RLB_ERR_ARG,
+            "persistent pair GEMM: K multiple of 64, split-K only with fp32 partials");
+  RLB_CHECK(epi == EPI_SWIGLU || epi == EPI_ARGMAX || (epi == EPI_PARTIAL && p.ws != nullptr &&
+                                                       p.splits >= 1 && p.K / BK >= p.splits),
+            RLB_ERR_ARG, "persistent pair GEMM epilogues: SwiGLU, argmax, fp32 partials");
   RLB_CHECK(epi != EPI_SWIGLU || p.N % 256 == 0, RLB_ERR_ARG, "SwiGLU pair tiles are 256 wide");
   static int n_sm = 0;
   if (!n_sm) {
@@ -1329,12 +1383,12 @@ int gemm_launch_pairp(const CUtensorMap& a, const CUtensorMap& b128, int epi, co
     RLB_CUDA(cudaGetDevice(&dev));
     RLB_CUDA(cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev));
   }
-  const int ntiles = ((p.M + 255) / 256) * ((p.N + 255) / 256);
+  const int ntiles = ((p.M + 255) / 256) * ((p.N + 255) / 256) * (epi == EPI_PARTIAL ? p.splits : 1);
   const int clusters = std::min(ntiles, n_sm / 2);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(2 * clusters, 1, 1);
   cfg.blockDim = dim3(GEMM_THREADS);
-  cfg.dynamicSmemBytes = PairPCfg::SMEM;
+  cfg.dynamicSmemBytes = epi == EPI_PARTIAL ? PairPCfg<EPI_PARTIAL>::SMEM : PairPCfg<EPI_SWIGLU>::SMEM;
   cfg.stream = st;
   cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -1346,6 +1400,7 @@ int gemm_launch_pairp(const CUtensorMap& a, const CUtensorMap& b128, int epi, co
   cfg.attrs = attr;
   cfg.numAttrs = pdl_enabled(RLB_PDL_CLASS) ? 2 : 1;
   if (epi == EPI_SWIGLU) RLB_CUDA(cudaLaunchKernelEx(&cfg, gemm_pairp_tc<EPI_SWIGLU>, a, b128, p));
+  else if (epi == EPI_PARTIAL) RLB_CUDA(cudaLaunchKernelEx(&cfg, gemm_pairp_tc<EPI_PARTIAL>, a, b128, p));
   else RLB_CUDA(cudaLaunchKernelEx(&cfg, gemm_pairp_tc<EPI_ARGMAX>, a, b128, p));
   return RLB_OK;
 }
@@ -1451,7 +1506,14 @@ extern "C" int rlb_gemm(int device, int32_t M, int32_t N, int32_t K, const void*
                      std::getenv("RLB_GEMM_MC") ? 2 : 1);
   } else {
     RLB_CUDA(cudaMalloc(&p.ws, sizeof(float) * static_cast<size_t>(p.splits) * M * N));
-    rc = gemm_launch(ma, mb, block_n, EPI_PARTIAL, p, 0, block_m);
+    const char* pe = std::getenv("RLB_GEMM_PAIR");
+    if (pe && std::atoi(pe) == 2) {   // persistent 2-SM tiles, split-K partials
+      CUtensorMap mb128;
+      rc = make_kmajor_map(&mb128, B, N, K, 128);
+      if (!rc) rc = gemm_launch_pairp(ma, mb128, EPI_PARTIAL, p, 0);
+    } else {
+      rc = gemm_launch(ma, mb, block_n, EPI_PARTIAL, p, 0, block_m);
+    }
     if (!rc) {
       switch (epilogue) {
         case EPI_BF16: splitk_reduce_kernel<EPI_BF16><<<M, 256>>>(p); break;

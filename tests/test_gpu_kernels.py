@@ -134,3 +134,18 @@ def test_gemm_swiglu_pair_tiles(dev, monkeypatch, M, mode):
     monkeypatch.setenv("RLB_GEMM_PAIR", mode)
     out = gemm(dev, A, wgu, epilogue=2, block_n=256)
     assert torch.equal(out, ref)
+
+
+@pytest.mark.parametrize("M,N,K,sp", [(512, 1536, 8960, 5), (300, 1536, 8960, 6), (2048, 1536, 8960, 5),
+                                      (77, 1536, 1536, 3), (1000, 3584, 18944, 4), (512, 1536, 1536, 7)])
+def test_gemm_splitk_partials_pair_tiles(dev, monkeypatch, M, N, K, sp):
+    """Persistent 2-SM tiles writing split-K fp32 partials (the down / O
+    projections above the small-batch plans): every split covers the same K
+    blocks as the single-SM kernel, so the reduced result has the same bits."""
+    from paper_2510_19225_b200.instance import gemm
+    A, B = _rand((M, K), 1.0, 31), _rand((N, K), 0.02, 32)
+    ref = gemm(dev, A, B, epilogue=3, block_n=128, splits=sp)
+    monkeypatch.setenv("RLB_GEMM_PAIR", "2")
+    out = gemm(dev, A, B, epilogue=3, block_n=128, splits=sp)
+    assert torch.equal(out, ref)
+    torch.testing.assert_close(out, A.float() @ B.float().T, rtol=2e-4, atol=5e-4)
