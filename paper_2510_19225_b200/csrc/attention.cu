@@ -353,8 +353,15 @@ __device__ __forceinline__ void mma_bf16_full(float (&d)[4], uint32_t a0, uint32
       : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
 }
 
+#ifndef ATTN_PAIR_STAGES
+#define ATTN_PAIR_STAGES 2     // prefill rows: a shallower ring, more resident CTAs
+#endif
+#ifndef ATTN_PAIR_MINB
+#define ATTN_PAIR_MINB 3
+#endif
 template <int D>
-__global__ void __launch_bounds__(WARPS * 32, 2) attn_pair_kernel(AttnArgs a) {
+__global__ void __launch_bounds__(WARPS * 32, ATTN_PAIR_MINB) attn_pair_kernel(AttnArgs a) {
+  constexpr int STAGES = ATTN_PAIR_STAGES;   // pipeline depth only: no effect on the bits
   constexpr int ROWB = D * 2;
   constexpr int CPR = ROWB / 16;
   constexpr int KSTEPS = D / 16;
@@ -544,6 +551,26 @@ __global__ void __launch_bounds__(WARPS * 32, 2) attn_pair_kernel(AttnArgs a) {
         mls[(warp * 16 + 8 + h) * 2 + 1] = l_run[1];
       }
     }
+    // per (row, head) slot: the running max over the warps, each warp's
+    // rescale factor and the merged denominator, once per slot instead of
+    // once per output element (same operations, same order, same bits)
+    float* cws = mls + WARPS * 16 * 2;                             // [16][WARPS + 2]
+    __syncthreads();
+    if (threadIdx.x < 16) {
+      const int slot = threadIdx.x;
+      float M = -INFINITY;
+#pragma unroll
+      for (int w = 0; w < WARPS; ++w) M = fmaxf(M, mls[(w * 16 + slot) * 2]);
+      float L = 0.f;
+#pragma unroll
+      for (int w = 0; w < WARPS; ++w) {
+        const float cw = exp2f(mls[(w * 16 + slot) * 2] - M);
+        L = __fmaf_rn(cw, mls[(w * 16 + slot) * 2 + 1], L);
+        cws[slot * (WARPS + 2) + w] = cw;
+      }
+      cws[slot * (WARPS + 2) + WARPS] = M;
+      cws[slot * (WARPS + 2) + WARPS + 1] = L;
+    }
     __syncthreads();
     for (int i = threadIdx.x; i < 2 * G * D; i += WARPS * 32) {
       const int x = i / (G * D), g = (i / D) % G, d = i % D;
@@ -552,16 +579,11 @@ __global__ void __launch_bounds__(WARPS * 32, 2) attn_pair_kernel(AttnArgs a) {
       const int n = x == 0 ? n0 : n1;
       if (w0 >= n) continue;                                   // no positions in this window
       const int slot = x * 8 + g;
-      float M = -INFINITY;
+      const float* cs = cws + slot * (WARPS + 2);
+      const float M = cs[WARPS], L = cs[WARPS + 1];
+      float O = 0.f;
 #pragma unroll
-      for (int w = 0; w < WARPS; ++w) M = fmaxf(M, mls[(w * 16 + slot) * 2]);
-      float L = 0.f, O = 0.f;
-#pragma unroll
-      for (int w = 0; w < WARPS; ++w) {
-        const float cw = exp2f(mls[(w * 16 + slot) * 2] - M);
-        L = __fmaf_rn(cw, mls[(w * 16 + slot) * 2 + 1], L);
-        O = __fmaf_rn(cw, red[(w * 16 + slot) * D + d], O);
-      }
+      for (int w = 0; w < WARPS; ++w) O = __fmaf_rn(cs[w], red[(w * 16 + slot) * D + d], O);
       const int qh = kvh * G + g;
       if (n <= SUPER) {
         a.out[static_cast<size_t>(rr) * a.ldo + qh * D + d] = __float2bfloat16_rn(O / L);
@@ -606,8 +628,9 @@ static int launch_attn(const AttnArgs& a, cudaStream_t st, bool pairs) {
   constexpr int smem_pipe = WARPS * STAGES * 2 * CHUNK * D * 2;
   constexpr int smem_red = WARPS * 8 * D * 4 + WARPS * 8 * 2 * 4;
   constexpr int smem = smem_pipe > smem_red ? smem_pipe : smem_red;
-  constexpr int smem_red2 = WARPS * 16 * D * 4 + WARPS * 16 * 2 * 4;
-  constexpr int smem2 = smem_pipe > smem_red2 ? smem_pipe : smem_red2;
+  constexpr int smem_red2 = WARPS * 16 * D * 4 + WARPS * 16 * 2 * 4 + 16 * (WARPS + 2) * 4;
+  constexpr int smem_pipe2 = WARPS * ATTN_PAIR_STAGES * 2 * CHUNK * D * 2;
+  constexpr int smem2 = smem_pipe2 > smem_red2 ? smem_pipe2 : smem_red2;
   static bool attr[64] = {false};
   int dev = 0;
   RLB_CUDA(cudaGetDevice(&dev));
