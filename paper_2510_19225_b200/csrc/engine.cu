@@ -285,6 +285,7 @@ struct rlb_instance {
   }
   int bn_qkv_decode = 64;   // RLB_QKV_BN=128 restores 128-column QKV tiles
   bool attn_pairs = true;   // prefill attention on row pairs (RLB_ATTN_PAIRS=0: one row per CTA)
+  bool sort_rows = true;    // decode rows in descending context order (RLB_SORT_ROWS=0: slot order)
   // persistent 2-SM tiles (double-buffered TMEM): bit 1 gate_up, bit 2
   // lm_head, bit 4 down, bit 8 O in prefill (RLB_PAIRP).  Default: lm_head
   // (1188 tiles: the epilogues hide behind the next tile's MMAs, 165 -> 121
@@ -425,6 +426,7 @@ int rlb_instance::init() {
   if (const char* ov = std::getenv("RLB_GU_MC")) mc_gu = std::atoi(ov) == 2 ? 2 : 1;
   if (const char* ov = std::getenv("RLB_QKV_BN")) bn_qkv_decode = std::atoi(ov) == 128 ? 128 : 64;
   if (const char* ov = std::getenv("RLB_ATTN_PAIRS")) attn_pairs = std::atoi(ov) != 0;
+  if (const char* ov = std::getenv("RLB_SORT_ROWS")) sort_rows = std::atoi(ov) != 0;
   if (const char* ov = std::getenv("RLB_PAIRP")) pairp = std::atoi(ov);
   if (const char* ov = std::getenv("RLB_PAIRP_PREFILL")) pairp_prefill = std::atoi(ov) != 0;
   if (const char* ov = std::getenv("RLB_BM")) {   // "qkv,o,gate_up,down" (tuning; process-wide)
@@ -830,6 +832,12 @@ int rlb_instance::run_decode(int steps, int* steps_run) {
     }
     const int R = static_cast<int>(dec_list.size());
     if (R == 0) break;
+    // longest contexts first: the attention grid dispatches rows in order, so
+    // the long rows start in the first wave and the last wave is short rows
+    // (every row's arithmetic is independent of its position in the batch)
+    if (sort_rows)
+      std::stable_sort(dec_list.begin(), dec_list.end(),
+                       [&](int x, int y) { return h_seq_len[x] > h_seq_len[y]; });
     RLB_CUDA(cudaMemcpyAsync(d_dec_slots, dec_list.data(), R * sizeof(int), cudaMemcpyHostToDevice, st));
     stats.h2d_bytes += static_cast<int64_t>(R) * 4;
     last_R = R;
