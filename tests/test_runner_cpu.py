@@ -150,3 +150,28 @@ def test_seeding_handoff_to_remotes():
     for k, p in enumerate(ps):
         assert m.requests[f"r{k}"].generated == reference_continuation(probe, p, 25)
     run.close()
+
+
+def test_preempted_instance_torn_down_off_the_resume_path():
+    """A killed instance leaves the serving set at once, but its device
+    teardown waits until the run ends (a dead process frees nothing on the
+    survivors' critical path); the resume report splits out the host phases."""
+    run = make_runner()
+    victim = run.instances["i1"]
+    for k, p in enumerate(prompts(24, seed=3)):
+        run.submit(f"r{k}", p, target_len=25)
+    seen = []
+    orig = run.preempt
+
+    def preempt(iid):
+        out = orig(iid)
+        seen.append((iid not in run.instances, victim.closed))
+        return out
+
+    run.preempt = preempt
+    out = run.run(kill_at={8: ["i1"]})
+    assert seen == [(True, False)]
+    assert victim.closed
+    rep = out["resume_i1"]
+    assert rep["preempt_ms"] >= 0 and rep["route_submit_ms"] >= 0
+    run.close()
