@@ -29,7 +29,10 @@ namespace {
 
 constexpr int WARPS = 4;
 constexpr int CHUNK = 16;              // tokens per pipeline stage
-constexpr int STAGES = 3;
+#ifndef ATTN_STAGES
+#define ATTN_STAGES 3
+#endif
+constexpr int STAGES = ATTN_STAGES;    // decode ring depth (timing only, not the bits)
 constexpr int SUPER = 2048;            // positions per CTA window (8 pages per warp)
 static_assert(SUPER / PAGE / WARPS <= 32, "page ids of a warp are held one per lane");
 
