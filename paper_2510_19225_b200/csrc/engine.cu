@@ -273,15 +273,51 @@ struct rlb_instance {
     p.dbg = d_dbg;
     return gemm_launch_pairp(a, b128, EPI_PARTIAL, p, st);
   }
+  int n_sm = 148;
+  bool bm_override = false;   // RLB_BM set: the fixed decode-batch tiles below
+  // Between 129 and 512 rows each projection takes the first of its tile
+  // shapes (smallest first) whose grid fits in one wave of the SMs, else the
+  // one with the fewest waves.  Tile shapes never change a row's bits.  For
+  // the 1.5B shape this reproduces the measured plans (128 x 64 QKV, 128 x
+  // 128 O, 256 x 128 / 256 x 256 SwiGLU); for 7B at 192 rows it moves O and
+  // down to 256-row tiles and gate_up to 256 x 256 (one wave of 148 CTAs).
+  int pick_tile(int R, const int (*cand)[2], int n, int N, int S, int* bn) const {
+    int best = 0, best_w = 1 << 30;
+    for (int i = 0; i < n; ++i) {
+      const int ctas = ((R + cand[i][0] - 1) / cand[i][0]) * ((N + cand[i][1] - 1) / cand[i][1]) * S;
+      const int w = (ctas + n_sm - 1) / n_sm;
+      if (w < best_w) {
+        best = i;
+        best_w = w;
+      }
+      if (w == 1) break;
+    }
+    *bn = cand[best][1];
+    return cand[best][0];
+  }
   TilePlan plan(int R) const {
     const int bnq = sp_qkv == 1 ? bn_qkv_decode : BN_QKV;
     if (R <= 128) return {128, 128, BN_SMALL, 128, 128, cl_down, bnq};
-    if (R <= SMALL_ROWS) return {128, 128, BN_SMALL, 256, 128, cl_down, bnq};
     // prefill chunks: the DSMEM reduction of thousands of split tiles costs
     // more than writing the partials (both sum the splits in the same order)
     if (R > 512) return {256, 256, BN_GU, bm_gu, bm_down, cl_down_large && !pair_down(R), BN_QKV};
-    return {bm_qkv, bm_o, BN_GU, bm_gu, bm_down, cl_down && !pair_down(R),
-            bm_qkv == 128 ? bnq : BN_QKV};
+    if (bm_override) {
+      if (R <= SMALL_ROWS) return {128, 128, BN_SMALL, 256, 128, cl_down, bnq};
+      return {bm_qkv, bm_o, BN_GU, bm_gu, bm_down, cl_down && !pair_down(R),
+              bm_qkv == 128 ? bnq : BN_QKV};
+    }
+    const int cq[3][2] = {{128, bnq}, {128, 128}, {256, 128}};
+    const int co[2][2] = {{128, BN_O}, {256, BN_O}};
+    const int cg[3][2] = {{128, BN_SMALL}, {256, BN_SMALL}, {256, BN_GU}};
+    const int cd[2][2] = {{128, BN_DOWN}, {256, BN_DOWN}};
+    TilePlan tp{};
+    int bn = 0;
+    tp.bm_qkv = pick_tile(R, cq, 3, QKV, sp_qkv, &tp.bn_qkv);
+    tp.bm_o = pick_tile(R, co, 2, H, sp_o, &bn);
+    tp.bm_gu = pick_tile(R, cg, 3, 2 * F, 1, &tp.bn_gu);
+    tp.bm_down = pick_tile(R, cd, 2, H, sp_down, &bn);
+    tp.cl_down = cl_down && !pair_down(R);
+    return tp;
   }
   int bn_qkv_decode = 64;   // RLB_QKV_BN=128 restores 128-column QKV tiles
   bool attn_pairs = true;   // prefill attention on row pairs (RLB_ATTN_PAIRS=0: one row per CTA)
@@ -433,6 +469,7 @@ int rlb_instance::init() {
     int a = 0, b = 0, c = 0, d = 0;
     if (std::sscanf(ov, "%d,%d,%d,%d", &a, &b, &c, &d) == 4) {
       for (int v : {a, b, c, d}) RLB_CHECK(v == 128 || v == 256, RLB_ERR_ARG, "RLB_BM: 128 or 256");
+      bm_override = true;
       bm_qkv = a;
       bm_o = b;
       bm_gu = c;
@@ -441,6 +478,7 @@ int rlb_instance::init() {
   }
 
   RLB_CUDA(cudaSetDevice(device));
+  RLB_CUDA(cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, device));
   RLB_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
   {
     // stream-ordered allocations (the pull's chunk lists) keep their memory in
