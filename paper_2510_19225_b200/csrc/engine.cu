@@ -274,6 +274,7 @@ struct rlb_instance {
     return gemm_launch_pairp(a, b128, EPI_PARTIAL, p, st);
   }
   int n_sm = 148;
+  bool small_gu_wave = true;   // RLB_SMALL_GU_WAVE=0: 128-wide SwiGLU tiles at <= 128 rows
   bool bm_override = false;   // RLB_BM set: the fixed decode-batch tiles below
   // Between 129 and 512 rows each projection takes the first of its tile
   // shapes (smallest first) whose grid fits in one wave of the SMs, else the
@@ -297,7 +298,14 @@ struct rlb_instance {
   }
   TilePlan plan(int R) const {
     const int bnq = sp_qkv == 1 ? bn_qkv_decode : BN_QKV;
-    if (R <= 128) return {128, 128, BN_SMALL, 128, 128, cl_down, bnq};
+    if (R <= 128) {
+      // one row tile: SwiGLU on 128-wide tiles, or 256-wide when that is what
+      // fits one wave (7B: 296 -> 148 CTAs)
+      const int cg1[2][2] = {{128, BN_SMALL}, {128, BN_GU}};
+      int bn_gu = BN_SMALL;
+      if (!bm_override && small_gu_wave) pick_tile(R, cg1, 2, 2 * F, 1, &bn_gu);
+      return {128, 128, bn_gu, 128, 128, cl_down, bnq};
+    }
     // prefill chunks: the DSMEM reduction of thousands of split tiles costs
     // more than writing the partials (both sum the splits in the same order)
     if (R > 512) return {256, 256, BN_GU, bm_gu, bm_down, cl_down_large && !pair_down(R), BN_QKV};
@@ -462,6 +470,7 @@ int rlb_instance::init() {
   if (const char* ov = std::getenv("RLB_GU_MC")) mc_gu = std::atoi(ov) == 2 ? 2 : 1;
   if (const char* ov = std::getenv("RLB_QKV_BN")) bn_qkv_decode = std::atoi(ov) == 128 ? 128 : 64;
   if (const char* ov = std::getenv("RLB_ATTN_PAIRS")) attn_pairs = std::atoi(ov) != 0;
+  if (const char* ov = std::getenv("RLB_SMALL_GU_WAVE")) small_gu_wave = std::atoi(ov) != 0;
   if (const char* ov = std::getenv("RLB_SORT_ROWS")) sort_rows = std::atoi(ov) != 0;
   if (const char* ov = std::getenv("RLB_PAIRP")) pairp = std::atoi(ov);
   if (const char* ov = std::getenv("RLB_PAIRP_PREFILL")) pairp_prefill = std::atoi(ov) != 0;
