@@ -33,7 +33,10 @@ constexpr int CHUNK = 16;              // tokens per pipeline stage
 #define ATTN_STAGES 3
 #endif
 constexpr int STAGES = ATTN_STAGES;    // decode ring depth (timing only, not the bits)
-constexpr int SUPER = 2048;            // positions per CTA window (8 pages per warp)
+#ifndef ATTN_SUPER
+#define ATTN_SUPER 2048
+#endif
+constexpr int SUPER = ATTN_SUPER;           // positions per CTA window (8 pages per warp)
 static_assert(SUPER / PAGE / WARPS <= 32, "page ids of a warp are held one per lane");
 
 __device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, bool valid) {
