@@ -82,6 +82,17 @@ __device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* m, 
       : "memory");
 }
 
+// 3D view (64 elements, rows, K blocks): one box = `box K blocks` stacked
+// 2D tiles (each the 128B-swizzled image a 2D box would write).
+__device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap* m, uint32_t bar,
+                                            int32_t row, int32_t kblock) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(bar), "r"(0), "r"(row), "r"(kblock)
+      : "memory");
+}
+
 // The same box into the same smem offset of every CTA in `mask` (cluster
 // multicast); complete_tx lands on each destination CTA's mbarrier at `bar`.
 __device__ __forceinline__ void tma_load_2d_mc(uint32_t dst, const CUtensorMap* m, uint32_t bar,

@@ -66,7 +66,7 @@ struct Req {
 
 struct LayerW {
   bf16 *ln1, *wqkv, *bqkv, *wo, *ln2, *wgu, *wdown;
-  CUtensorMap m_qkv, m_qkv64, m_o, m_gu, m_gu_small, m_down;
+  CUtensorMap m_qkv, m_qkv64, m_qkv64x2, m_o, m_gu, m_gu_small, m_down;
 };
 
 // GEMM tile widths per projection (N-tile of the 128 x BN UMMA tile).  A
@@ -196,6 +196,14 @@ struct rlb_instance {
   float* d_logits = nullptr;
   float* d_ws = nullptr;
   CUtensorMap m_xn, m_attn, m_act;
+  CUtensorMap m_xn_x2;    // 3D view of xn: 128-row x 2-K-block boxes (64-column QKV tiles)
+  bool qkv_kps2 = true;   // RLB_QKV_KPS=1: one K block per stage
+  int qkv_launch(const TilePlan& tp, const LayerW& w, const GemmParams& pq) {
+    if (tp.bn_qkv == 64 && qkv_kps2)
+      return gemm_launch(m_xn_x2, w.m_qkv64x2, 64, EPI_ROPE, pq, st, tp.bm_qkv, 1, 2);
+    return gemm_launch(m_xn, tp.bn_qkv == 64 ? w.m_qkv64 : w.m_qkv, tp.bn_qkv, EPI_ROPE, pq, st,
+                       tp.bm_qkv);
+  }
   int32_t *d_ring = nullptr, *d_ring_ctr = nullptr, *d_ring_cur = nullptr, *h_ring = nullptr;
   // K5 export scratch (rlb_export_partials)
   int* d_exp_slots = nullptr;
@@ -470,6 +478,7 @@ int rlb_instance::init() {
   if (const char* ov = std::getenv("RLB_GU_MC")) mc_gu = std::atoi(ov) == 2 ? 2 : 1;
   if (const char* ov = std::getenv("RLB_QKV_BN")) bn_qkv_decode = std::atoi(ov) == 128 ? 128 : 64;
   if (const char* ov = std::getenv("RLB_ATTN_PAIRS")) attn_pairs = std::atoi(ov) != 0;
+  if (const char* ov = std::getenv("RLB_QKV_KPS")) qkv_kps2 = std::atoi(ov) == 2;
   if (const char* ov = std::getenv("RLB_SMALL_GU_WAVE")) small_gu_wave = std::atoi(ov) != 0;
   if (const char* ov = std::getenv("RLB_SORT_ROWS")) sort_rows = std::atoi(ov) != 0;
   if (const char* ov = std::getenv("RLB_PAIRP")) pairp = std::atoi(ov);
@@ -566,6 +575,7 @@ int rlb_instance::init() {
 
   if ((rc = gemm_prepare())) return rc;
   if ((rc = make_kmajor_map(&m_xn, d_xn, R, H, 128))) return rc;
+  if ((rc = make_kmajor_map3(&m_xn_x2, d_xn, R, H, 128, 2))) return rc;
   if ((rc = make_kmajor_map(&m_attn, d_attn, R, NQ * D, 128))) return rc;
   if ((rc = make_kmajor_map(&m_act, d_act, R, F, 128))) return rc;
   return bind_arena();
@@ -593,6 +603,7 @@ int rlb_instance::bind_arena() {
     w.wdown = put(static_cast<int64_t>(H) * F);
     if ((rc = make_kmajor_map(&w.m_qkv, w.wqkv, QKV, H, BN_QKV))) return rc;
     if ((rc = make_kmajor_map(&w.m_qkv64, w.wqkv, QKV, H, 64))) return rc;
+    if ((rc = make_kmajor_map3(&w.m_qkv64x2, w.wqkv, QKV, H, 64, 2))) return rc;
     if ((rc = make_kmajor_map(&w.m_o, w.wo, H, NQ * D, BN_O))) return rc;
     if ((rc = make_kmajor_map(&w.m_gu, w.wgu, 2 * F, H, BN_GU))) return rc;
     if ((rc = make_kmajor_map(&w.m_gu_small, w.wgu, 2 * F, H, BN_SMALL))) return rc;
@@ -645,9 +656,7 @@ int rlb_instance::forward_layers(int R, bool prefill) {
     bf16* kv_l = kv + layer_stride * l;
     GemmParams pq{R, QKV, H, w.bqkv, nullptr, 0, sp_qkv, nullptr};
     pq.rope = RopeDst{d_row_slot, d_row_pos, d_rope, d_q, NQ * D, kv_l, d_bt, pps, NQ, NKV, D};
-    if ((rc = gemm_launch(m_xn, tp.bn_qkv == 64 ? w.m_qkv64 : w.m_qkv, tp.bn_qkv, EPI_ROPE, pq, st,
-                          tp.bm_qkv)))
-      return rc;
+    if ((rc = qkv_launch(tp, w, pq))) return rc;
     AttnArgs a{d_q, NQ * D, kv_l, d_bt, pps, d_row_slot, d_row_pos, R, NQ, NKV, D, max_splits,
                d_ws, d_attn, NQ * D};
     if ((rc = attention_launch(a, st, prefill && attn_pairs))) return rc;
@@ -1358,8 +1367,7 @@ int rlb_profile_kernel(rlb_instance* h, int32_t which, int32_t iters, double* av
         pq.rope = RopeDst{h->d_row_slot, h->d_row_pos, h->d_rope, h->d_q, NQ * D, h->kv_scratch(),
                           h->d_bt, h->pps, NQ, h->NKV, D};
         pq.dbg = h->d_dbg;
-        return gemm_launch(h->m_xn, tp.bn_qkv == 64 ? w.m_qkv64 : w.m_qkv, tp.bn_qkv, EPI_ROPE,
-                           pq, h->st, tp.bm_qkv);
+        return h->qkv_launch(tp, w, pq);
       }
       case 4:
         if (h->pair_o(R)) return h->proj_pairp(h->m_attn, w.m_o, h->sp_o, R, H, NQ * D);

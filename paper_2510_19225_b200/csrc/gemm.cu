@@ -48,13 +48,18 @@ constexpr int GEMM_THREADS = 384;
 // NACC accumulators of 128 rows per CTA: 2 (256-row tiles, the B stage is
 // shared by both) or 1 (128-row tiles: twice the CTAs for short-K / small-N
 // projections that would otherwise need split-K).
-template <int BN, int NACC>
+// KPS = K blocks per pipeline stage.  KPS = 2 (the 64-column QKV tiles)
+// loads each operand tile as one 3D box of two stacked 64-wide K blocks: a
+// TMA-streaming SM's rate grows with the bytes per box (64-row weight boxes
+// stream at half the rate of 128-row ones, scripts/probe_stream.cu).
+template <int BN, int NACC, int KPS = 1>
 struct GemmCfg {
   static constexpr int BMT = HM * NACC;                // rows per CTA
-  static constexpr int A_BYTES = HM * BK * 2;          // one accumulator's rows
+  static constexpr int A_BYTES = HM * BK * 2;          // one accumulator's rows, one K block
   static constexpr int B_BYTES = BN * BK * 2;
-  static constexpr int STAGE_BYTES = NACC * A_BYTES + B_BYTES;
-  static constexpr int STAGES = BN == 256 ? 3 : (NACC == 2 ? 4 : (BN == 64 ? 8 : 6));
+  static constexpr int STAGE_BYTES = KPS * (NACC * A_BYTES + B_BYTES);
+  static constexpr int STAGES =
+      (BN == 256 ? 3 : (NACC == 2 ? 4 : (BN == 64 ? 8 : 6))) / KPS;
   static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 256;
   static constexpr uint32_t TMEM_COLS = NACC * BN;
 };
@@ -366,11 +371,12 @@ __device__ __forceinline__ void rope_direct(const GemmParams& p, uint32_t tbase,
 // it to both, halving the A traffic from L2; both MMA warps release a stage
 // on both CTAs (multicast commit), so neither refills it before the other
 // has consumed it.
-template <int BN, int EPI, int NACC, int MC = 1>
+template <int BN, int EPI, int NACC, int MC = 1, int KPS = 1>
 __global__ void __launch_bounds__(GEMM_THREADS, 1)
     gemm_bf16_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                  GemmParams p) {
-  using C = GemmCfg<BN, NACC>;
+  static_assert(KPS == 1 || MC == 1, "3D boxes: no multicast");
+  using C = GemmCfg<BN, NACC, KPS>;
   constexpr int BMT = C::BMT;
   constexpr int NEW = 4 * NACC;                 // epilogue warps with an accumulator
   // epilogue warps that run (direct RoPE with one accumulator splits columns)
@@ -434,19 +440,74 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   // the first stages' B tiles before waiting, then the A tiles after.  Every
   // other thread waits first (A, h and the outputs belong to the chain).
   const bool producer = warp == 0 && lane == 0;
-  const int pre = nk < C::STAGES ? nk : C::STAGES;
+  // stages of KPS K blocks (a partial last one still receives KPS blocks'
+  // bytes: the extra block is unused, or zero-filled past K)
+  const int ng = (nk + KPS - 1) / KPS;
+  const int pre = ng < C::STAGES ? ng : C::STAGES;
+  const uint32_t stage_txk = stage_tx * KPS;
   if (producer) {
-    for (int kb = 0; kb < pre; ++kb) {
-      uint8_t* st = smem + kb * C::STAGE_BYTES;
-      mbar_expect_tx(smem_u32(&full[kb]), stage_tx);
-      tma_load_2d(smem_u32(st + NACC * C::A_BYTES), &tmB, smem_u32(&full[kb]),
-                  (kb0 + kb) * BK, n_blk * BN);
+    for (int g = 0; g < pre; ++g) {
+      uint8_t* st = smem + g * C::STAGE_BYTES;
+      mbar_expect_tx(smem_u32(&full[g]), stage_txk);
+      if constexpr (KPS == 1)
+        tma_load_2d(smem_u32(st + NACC * C::A_BYTES), &tmB, smem_u32(&full[g]), (kb0 + g) * BK,
+                    n_blk * BN);
+      else
+        tma_load_3d(smem_u32(st + NACC * KPS * C::A_BYTES), &tmB, smem_u32(&full[g]), n_blk * BN,
+                    kb0 + g * KPS);
     }
   }
   pdl_wait();
   if (stamp && threadIdx.x == 0) p.dbg[2] = gtime();
 
-  if (warp == 0) {
+  if (warp == 0 && KPS > 1) {
+    if (producer) {
+      for (int g = 0; g < ng; ++g) {
+        const int s = g % C::STAGES;
+        const uint32_t ph = (g / C::STAGES) & 1;
+        uint8_t* st = smem + s * C::STAGE_BYTES;
+        if (g >= pre) {
+          mbar_wait(smem_u32(&empty[s]), ph ^ 1);
+          mbar_expect_tx(smem_u32(&full[s]), stage_txk);
+          tma_load_3d(smem_u32(st + NACC * KPS * C::A_BYTES), &tmB, smem_u32(&full[s]), n_blk * BN,
+                      kb0 + g * KPS);
+        }
+#pragma unroll
+        for (int a = 0; a < NACC; ++a)
+          if (a < live_acc)
+            tma_load_3d(smem_u32(st + a * KPS * C::A_BYTES), &tmA, smem_u32(&full[s]),
+                        m_blk * BMT + a * HM, kb0 + g * KPS);
+      }
+    }
+  } else if (warp == 1 && KPS > 1) {
+    if (lane == 0) {
+      constexpr uint32_t idesc = umma_idesc_bf16(HM, BN);
+      for (int g = 0; g < ng; ++g) {
+        const int s = g % C::STAGES;
+        const uint32_t ph = (g / C::STAGES) & 1;
+        const uint32_t st = smem_u32(smem + s * C::STAGE_BYTES);
+        mbar_wait(smem_u32(&full[s]), ph);
+        tc_fence_after();
+#pragma unroll
+        for (int j = 0; j < KPS; ++j) {
+          if (g * KPS + j >= nk) break;
+          const uint64_t bd = umma_desc_sw128(st + NACC * KPS * C::A_BYTES + j * C::B_BYTES);
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k) {
+#pragma unroll
+            for (int a = 0; a < NACC; ++a)
+              if (a < live_acc)
+                umma_bf16(tmem + a * BN,
+                          umma_desc_sw128(st + (a * KPS + j) * C::A_BYTES) + 2 * k, bd + 2 * k,
+                          idesc, ((g * KPS + j) | k) != 0);
+          }
+        }
+        umma_commit(smem_u32(&empty[s]));
+      }
+      umma_commit(smem_u32(tfull));
+      if (stamp) p.dbg[3] = gtime();
+    }
+  } else if (warp == 0) {
     if (producer) {
       for (int kb = 0; kb < nk; ++kb) {
         const int s = kb % C::STAGES;
@@ -1208,11 +1269,32 @@ int make_kmajor_map(CUtensorMap* map, const void* ptr, int64_t rows, int64_t k, 
   return RLB_OK;
 }
 
-template <int BN, int EPI, int NACC, int MC = 1>
+// 3D view of a K-major [rows, k] bf16 matrix: (64 elements, rows, k / 64
+// K blocks), boxes of box_rows rows x kps K blocks (gemm_bf16_tc<..., KPS>)
+int make_kmajor_map3(CUtensorMap* map, const void* ptr, int64_t rows, int64_t k, int box_rows,
+                     int kps) {
+  PFN_encodeTiled_t enc = encode_fn();
+  RLB_CHECK(enc != nullptr, RLB_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  RLB_CHECK(k % BK == 0, RLB_ERR_ARG, "GEMM K must be a multiple of 64");
+  RLB_CHECK((reinterpret_cast<uintptr_t>(ptr) & 15) == 0, RLB_ERR_ARG, "TMA base not 16B aligned");
+  cuuint64_t dims[3] = {static_cast<cuuint64_t>(BK), static_cast<cuuint64_t>(rows),
+                        static_cast<cuuint64_t>(k / BK)};
+  cuuint64_t strides[2] = {static_cast<cuuint64_t>(k * 2), static_cast<cuuint64_t>(BK * 2)};
+  cuuint32_t box[3] = {static_cast<cuuint32_t>(BK), static_cast<cuuint32_t>(box_rows),
+                       static_cast<cuuint32_t>(kps)};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(ptr), dims, strides,
+                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  RLB_CHECK(r == CUDA_SUCCESS, RLB_ERR_CUDA, "cuTensorMapEncodeTiled (3D) failed: " + std::to_string(r));
+  return RLB_OK;
+}
+
+template <int BN, int EPI, int NACC, int MC = 1, int KPS = 1>
 static int set_attr() {
-  RLB_CUDA(cudaFuncSetAttribute(gemm_bf16_tc<BN, EPI, NACC, MC>,
+  RLB_CUDA(cudaFuncSetAttribute(gemm_bf16_tc<BN, EPI, NACC, MC, KPS>,
                                 cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                GemmCfg<BN, NACC>::SMEM));
+                                GemmCfg<BN, NACC, KPS>::SMEM));
   return RLB_OK;
 }
 
@@ -1237,7 +1319,7 @@ int gemm_prepare() {
   int rc;
   if ((rc = set_attr_bn<128, 2>()) || (rc = set_attr_bn<256, 2>()) || (rc = set_attr_bn<128, 1>()) ||
       (rc = set_attr_bn<256, 1>()) || (rc = set_attr<256, EPI_SWIGLU, 2, 2>()) ||
-      (rc = set_attr<64, EPI_ROPE, 1>()))
+      (rc = set_attr<64, EPI_ROPE, 1>()) || (rc = set_attr<64, EPI_ROPE, 1, 1, 2>()))
     return rc;
   RLB_CUDA(cudaFuncSetAttribute(gemm_pair_tc<EPI_SWIGLU>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 PairCfg::SMEM));
@@ -1253,10 +1335,10 @@ int gemm_prepare() {
   return RLB_OK;
 }
 
-template <int BN, int EPI, int NACC, int MC = 1>
+template <int BN, int EPI, int NACC, int MC = 1, int KPS = 1>
 static int launch_one(const CUtensorMap& a, const CUtensorMap& b, const GemmParams& p,
                       cudaStream_t st) {
-  using C = GemmCfg<BN, NACC>;
+  using C = GemmCfg<BN, NACC, KPS>;
   RLB_CHECK((p.N + BN - 1) / BN <= 65535, RLB_ERR_ARG, "too many N tiles");
   dim3 grid((p.M + C::BMT - 1) / C::BMT, (p.N + BN - 1) / BN, p.splits);
   const bool split_cluster = cluster_epi(EPI) && BN == 128 && p.splits > 1;
@@ -1278,11 +1360,12 @@ static int launch_one(const CUtensorMap& a, const CUtensorMap& b, const GemmPara
     attr[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = pdl_enabled(RLB_PDL_CLASS) ? 2 : 1;
-    RLB_CUDA(cudaLaunchKernelEx(&cfg, gemm_bf16_tc<BN, EPI, NACC, MC>, a, b, p));
+    RLB_CUDA(cudaLaunchKernelEx(&cfg, gemm_bf16_tc<BN, EPI, NACC, MC, KPS>, a, b, p));
     return RLB_OK;
   }
   if constexpr (MC == 1)
-    RLB_CUDA(launch_k(gemm_bf16_tc<BN, EPI, NACC>, grid, dim3(GEMM_THREADS), C::SMEM, st, a, b, p));
+    RLB_CUDA(launch_k(gemm_bf16_tc<BN, EPI, NACC, 1, KPS>, grid, dim3(GEMM_THREADS), C::SMEM, st, a,
+                      b, p));
   return RLB_OK;
 }
 
@@ -1305,7 +1388,9 @@ static int launch_bn(const CUtensorMap& a, const CUtensorMap& b, int epi, const 
 }
 
 int gemm_launch(const CUtensorMap& a, const CUtensorMap& b, int block_n, int epi,
-                const GemmParams& p, cudaStream_t st, int block_m, int a_multicast) {
+                const GemmParams& p, cudaStream_t st, int block_m, int a_multicast, int kps) {
+  RLB_CHECK(kps == 1 || (block_n == 64 && a_multicast == 1), RLB_ERR_ARG,
+            "2 K blocks per stage: the 64-column RoPE tiles only");
   if (p.M <= 0) return RLB_OK;
   if (a_multicast == 2) {
     RLB_CHECK(block_n == 256 && block_m == 256 && epi == EPI_SWIGLU, RLB_ERR_ARG,
@@ -1325,6 +1410,7 @@ int gemm_launch(const CUtensorMap& a, const CUtensorMap& b, int block_n, int epi
   if (block_n == 64) {   // the narrow tile exists for single-split RoPE (decode QKV)
     RLB_CHECK(epi == EPI_ROPE && block_m == 128 && p.splits == 1, RLB_ERR_ARG,
               "64-column tiles: RoPE epilogue, 128-row tiles, no split");
+    if (kps == 2) return launch_one<64, EPI_ROPE, 1, 1, 2>(a, b, p, st);   // 3D-box maps
     return launch_one<64, EPI_ROPE, 1>(a, b, p, st);
   }
   RLB_CHECK(epi != EPI_SWIGLU || (block_n % 128 == 0 && p.N % 128 == 0), RLB_ERR_ARG,

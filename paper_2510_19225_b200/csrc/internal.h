@@ -42,7 +42,10 @@ struct GemmParams {
 int make_kmajor_map(CUtensorMap* map, const void* ptr, int64_t rows, int64_t k, int box_rows);
 int gemm_prepare();  // set smem attributes of every GEMM variant on the current device
 int gemm_launch(const CUtensorMap& a, const CUtensorMap& b, int block_n, int epi,
-                const GemmParams& p, cudaStream_t st, int block_m = 256, int a_multicast = 1);
+                const GemmParams& p, cudaStream_t st, int block_m = 256, int a_multicast = 1,
+                int kps = 1);
+int make_kmajor_map3(CUtensorMap* map, const void* ptr, int64_t rows, int64_t k, int box_rows,
+                     int kps);
 int gemm_launch_pair(const CUtensorMap& a, const CUtensorMap& b128, int epi, const GemmParams& p,
                      cudaStream_t st);
 int gemm_launch_pairp(const CUtensorMap& a, const CUtensorMap& b128, int epi, const GemmParams& p,

@@ -289,3 +289,16 @@ def test_qwen7b_width_rollout_and_migration(cuda):
     exported = src.export_partials([f"r{i}" for i in range(len(prompts))])
     dst = _instance(shape, w, max_slots=3, max_seq_len=512, max_prefill_rows=512)
     assert _rollout(dst, prompts, 48, prefix=[g for _, g in exported]) == ref
+
+
+@pytest.mark.parametrize("n_prompts", [3, 300])
+def test_qkv_two_k_blocks_per_stage_same_tokens(mid, monkeypatch, n_prompts):
+    """The 64-column QKV tiles stream two K blocks per stage through 3D TMA
+    boxes; the MMAs see the same tiles in the same K order, so the rollout's
+    tokens equal the one-block-per-stage kernel's (RLB_QKV_KPS=1)."""
+    shape, w, _ = mid
+    prompts = synth_prompts(n_prompts, shape.vocab, 128, 384, seed=17)
+    got = _rollout(_instance(shape, w, max_slots=512, max_seq_len=1024), prompts, 40)
+    monkeypatch.setenv("RLB_QKV_KPS", "1")
+    ref = _rollout(_instance(shape, w, max_slots=512, max_seq_len=1024), prompts, 40)
+    assert got == ref
