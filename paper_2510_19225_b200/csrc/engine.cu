@@ -66,7 +66,7 @@ struct Req {
 
 struct LayerW {
   bf16 *ln1, *wqkv, *bqkv, *wo, *ln2, *wgu, *wdown;
-  CUtensorMap m_qkv, m_qkv64, m_qkv64x2, m_o, m_gu, m_gu_small, m_down;
+  CUtensorMap m_qkv, m_qkv64, m_qkv64x2, m_o, m_ox2, m_gu, m_gu_small, m_down;
 };
 
 // GEMM tile widths per projection (N-tile of the 128 x BN UMMA tile).  A
@@ -197,6 +197,17 @@ struct rlb_instance {
   float* d_ws = nullptr;
   CUtensorMap m_xn, m_attn, m_act;
   CUtensorMap m_xn_x2;    // 3D view of xn: 128-row x 2-K-block boxes (64-column QKV tiles)
+  CUtensorMap m_attn_x2;  // 3D view of the attention output (O projection, 128-row tiles)
+  bool o_kps2 = true;     // RLB_O_KPS=1: one K block per stage
+  int o_partials(const TilePlan& tp, const LayerW& w, int R) {
+    if (o_kps2 && tp.bm_o == 128 && BN_O == 128) {
+      GemmParams p{R, H, NQ * D, nullptr, nullptr, 0, sp_o < 1 ? 1 : sp_o, d_part};
+      p.dbg = d_dbg;
+      return gemm_launch(m_attn_x2, w.m_ox2, BN_O, EPI_PARTIAL, p, st, 128, 1, 2);
+    }
+    return proj(m_attn, w.m_o, BN_O, sp_o, EPI_PARTIAL, R, H, NQ * D, nullptr, nullptr, 0,
+                tp.bm_o);
+  }
   bool qkv_kps2 = true;   // RLB_QKV_KPS=1: one K block per stage
   int qkv_launch(const TilePlan& tp, const LayerW& w, const GemmParams& pq) {
     if (tp.bn_qkv == 64 && qkv_kps2)
@@ -479,6 +490,7 @@ int rlb_instance::init() {
   if (const char* ov = std::getenv("RLB_QKV_BN")) bn_qkv_decode = std::atoi(ov) == 128 ? 128 : 64;
   if (const char* ov = std::getenv("RLB_ATTN_PAIRS")) attn_pairs = std::atoi(ov) != 0;
   if (const char* ov = std::getenv("RLB_QKV_KPS")) qkv_kps2 = std::atoi(ov) == 2;
+  if (const char* ov = std::getenv("RLB_O_KPS")) o_kps2 = std::atoi(ov) == 2;
   if (const char* ov = std::getenv("RLB_SMALL_GU_WAVE")) small_gu_wave = std::atoi(ov) != 0;
   if (const char* ov = std::getenv("RLB_SORT_ROWS")) sort_rows = std::atoi(ov) != 0;
   if (const char* ov = std::getenv("RLB_PAIRP")) pairp = std::atoi(ov);
@@ -576,6 +588,7 @@ int rlb_instance::init() {
   if ((rc = gemm_prepare())) return rc;
   if ((rc = make_kmajor_map(&m_xn, d_xn, R, H, 128))) return rc;
   if ((rc = make_kmajor_map3(&m_xn_x2, d_xn, R, H, 128, 2))) return rc;
+  if ((rc = make_kmajor_map3(&m_attn_x2, d_attn, R, NQ * D, 128, 2))) return rc;
   if ((rc = make_kmajor_map(&m_attn, d_attn, R, NQ * D, 128))) return rc;
   if ((rc = make_kmajor_map(&m_act, d_act, R, F, 128))) return rc;
   return bind_arena();
@@ -604,6 +617,7 @@ int rlb_instance::bind_arena() {
     if ((rc = make_kmajor_map(&w.m_qkv, w.wqkv, QKV, H, BN_QKV))) return rc;
     if ((rc = make_kmajor_map(&w.m_qkv64, w.wqkv, QKV, H, 64))) return rc;
     if ((rc = make_kmajor_map3(&w.m_qkv64x2, w.wqkv, QKV, H, 64, 2))) return rc;
+    if ((rc = make_kmajor_map3(&w.m_ox2, w.wo, H, NQ * D, BN_O, 2))) return rc;
     if ((rc = make_kmajor_map(&w.m_o, w.wo, H, NQ * D, BN_O))) return rc;
     if ((rc = make_kmajor_map(&w.m_gu, w.wgu, 2 * F, H, BN_GU))) return rc;
     if ((rc = make_kmajor_map(&w.m_gu_small, w.wgu, 2 * F, H, BN_SMALL))) return rc;
@@ -668,8 +682,7 @@ int rlb_instance::forward_layers(int R, bool prefill) {
         return rc;
     } else {
       if ((rc = pair_o(R) ? proj_pairp(m_attn, w.m_o, sp_o, R, H, NQ * D)
-                          : proj(m_attn, w.m_o, BN_O, sp_o, EPI_PARTIAL, R, H, NQ * D, nullptr,
-                                 nullptr, 0, tp.bm_o)) ||
+                          : o_partials(tp, w, R)) ||
           (rc = resid_norm_launch(d_h, d_part, sp_o, R, nullptr, R, w.ln2, H, m.rms_eps, d_xn, true,
                                   st)))
         return rc;
@@ -1371,6 +1384,7 @@ int rlb_profile_kernel(rlb_instance* h, int32_t which, int32_t iters, double* av
       }
       case 4:
         if (h->pair_o(R)) return h->proj_pairp(h->m_attn, w.m_o, h->sp_o, R, H, NQ * D);
+        if (!h->cl_o) return h->o_partials(tp, w, R);
         return h->proj(h->m_attn, w.m_o, BN_O, h->sp_o, h->cl_o ? EPI_RESADD : EPI_PARTIAL,
                        R, H, NQ * D, nullptr, h->d_part, H, tp.bm_o);
       case 5: {

@@ -1319,7 +1319,8 @@ int gemm_prepare() {
   int rc;
   if ((rc = set_attr_bn<128, 2>()) || (rc = set_attr_bn<256, 2>()) || (rc = set_attr_bn<128, 1>()) ||
       (rc = set_attr_bn<256, 1>()) || (rc = set_attr<256, EPI_SWIGLU, 2, 2>()) ||
-      (rc = set_attr<64, EPI_ROPE, 1>()) || (rc = set_attr<64, EPI_ROPE, 1, 1, 2>()))
+      (rc = set_attr<64, EPI_ROPE, 1>()) || (rc = set_attr<64, EPI_ROPE, 1, 1, 2>()) ||
+      (rc = set_attr<128, EPI_PARTIAL, 1, 1, 2>()))
     return rc;
   RLB_CUDA(cudaFuncSetAttribute(gemm_pair_tc<EPI_SWIGLU>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 PairCfg::SMEM));
@@ -1389,8 +1390,15 @@ static int launch_bn(const CUtensorMap& a, const CUtensorMap& b, int epi, const 
 
 int gemm_launch(const CUtensorMap& a, const CUtensorMap& b, int block_n, int epi,
                 const GemmParams& p, cudaStream_t st, int block_m, int a_multicast, int kps) {
-  RLB_CHECK(kps == 1 || (block_n == 64 && a_multicast == 1), RLB_ERR_ARG,
-            "2 K blocks per stage: the 64-column RoPE tiles only");
+  RLB_CHECK(kps == 1 || (a_multicast == 1 && ((block_n == 64 && epi == EPI_ROPE) ||
+                                                (block_n == 128 && block_m == 128 &&
+                                                 epi == EPI_PARTIAL))),
+            RLB_ERR_ARG, "2 K blocks per stage: 64-column RoPE or 128 x 128 partial tiles");
+  if (kps == 2 && epi == EPI_PARTIAL) {
+    RLB_CHECK(p.ws != nullptr && p.K % BK == 0 && p.K / BK >= p.splits, RLB_ERR_ARG,
+              "split-K partials need a workspace");
+    return launch_one<128, EPI_PARTIAL, 1, 1, 2>(a, b, p, st);
+  }
   if (p.M <= 0) return RLB_OK;
   if (a_multicast == 2) {
     RLB_CHECK(block_n == 256 && block_m == 256 && epi == EPI_SWIGLU, RLB_ERR_ARG,

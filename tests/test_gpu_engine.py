@@ -302,3 +302,15 @@ def test_qkv_two_k_blocks_per_stage_same_tokens(mid, monkeypatch, n_prompts):
     monkeypatch.setenv("RLB_QKV_KPS", "1")
     ref = _rollout(_instance(shape, w, max_slots=512, max_seq_len=1024), prompts, 40)
     assert got == ref
+
+
+@pytest.mark.parametrize("n_prompts", [3, 300])
+def test_o_two_k_blocks_per_stage_same_tokens(mid, monkeypatch, n_prompts):
+    """The O projection's 128 x 128 split-K tiles on two-K-block stages (3D
+    TMA boxes): the same partials, the same tokens (RLB_O_KPS=1 reference)."""
+    shape, w, _ = mid
+    prompts = synth_prompts(n_prompts, shape.vocab, 128, 384, seed=19)
+    got = _rollout(_instance(shape, w, max_slots=512, max_seq_len=1024), prompts, 40)
+    monkeypatch.setenv("RLB_O_KPS", "1")
+    ref = _rollout(_instance(shape, w, max_slots=512, max_seq_len=1024), prompts, 40)
+    assert got == ref
