@@ -377,6 +377,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
                  GemmParams p) {
   static_assert(KPS == 1 || MC == 1, "3D boxes: no multicast");
   using C = GemmCfg<BN, NACC, KPS>;
+  static_assert(KPS == 1 || (NACC == 1 && C::STAGES >= 2),
+                "two-K-block stages: one accumulator, at least two stages (the only tested form)");
   constexpr int BMT = C::BMT;
   constexpr int NEW = 4 * NACC;                 // epilogue warps with an accumulator
   // epilogue warps that run (direct RoPE with one accumulator splits columns)
