@@ -1514,6 +1514,21 @@ extern "C" int rlb_bench_gemm(int device, int32_t M, int32_t N, int32_t K, int32
   if (rc) return rc;
   bf16 *A = nullptr, *B = nullptr;
   float* C = nullptr;
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  struct Scratch {   // released on every return path
+    bf16** a;
+    bf16** b;
+    float** c;
+    cudaEvent_t* e0;
+    cudaEvent_t* e1;
+    ~Scratch() {
+      cudaFree(*a);
+      cudaFree(*b);
+      cudaFree(*c);
+      if (*e0) cudaEventDestroy(*e0);
+      if (*e1) cudaEventDestroy(*e1);
+    }
+  } scratch{&A, &B, &C, &e0, &e1};
   const int S = splits < 1 ? 1 : splits;
   RLB_CUDA(cudaMalloc(&A, sizeof(bf16) * static_cast<size_t>(M) * K));
   RLB_CUDA(cudaMalloc(&B, sizeof(bf16) * static_cast<size_t>(N) * K));
@@ -1527,7 +1542,6 @@ extern "C" int rlb_bench_gemm(int device, int32_t M, int32_t N, int32_t K, int32
   if (epilogue == EPI_ARGMAX) p.ldo = (N + block_n - 1) / block_n;
   RLB_CHECK(epilogue != EPI_ROPE, RLB_ERR_ARG, "EPI_ROPE needs an instance (rlb_profile_kernel)");
   const int epi = S > 1 && !cluster_epi(epilogue) ? static_cast<int>(EPI_PARTIAL) : epilogue;
-  cudaEvent_t e0, e1;
   RLB_CUDA(cudaEventCreate(&e0));
   RLB_CUDA(cudaEventCreate(&e1));
   const int mc = std::getenv("RLB_GEMM_MC") ? 2 : 1;   // A multicast pairs (SwiGLU 256x256)
@@ -1562,11 +1576,6 @@ extern "C" int rlb_bench_gemm(int device, int32_t M, int32_t N, int32_t K, int32
                  (long long)(h[4] - h[0]), (long long)(h[6] - h[0]), (long long)(h[5] - h[0]));
     cudaFree(d);
   }
-  cudaEventDestroy(e0);
-  cudaEventDestroy(e1);
-  cudaFree(A);
-  cudaFree(B);
-  cudaFree(C);
   return rc;
 }
 

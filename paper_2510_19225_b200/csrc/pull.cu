@@ -145,17 +145,22 @@ static int run_chunks(const std::vector<CopyChunk>& chunks, cudaStream_t st) {
   if (chunks.empty()) return RLB_OK;
   CopyChunk* d = nullptr;
   const size_t bytes = chunks.size() * sizeof(CopyChunk);
-  RLB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&d), bytes, st));
-  RLB_CUDA(cudaMemcpyAsync(d, chunks.data(), bytes, cudaMemcpyHostToDevice, st));
   int sms = 148, dev = 0;
   RLB_CUDA(cudaGetDevice(&dev));
   RLB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   int cap = sms * 4;
   if (const char* c = std::getenv("RLB_COPY_CTAS")) cap = std::max(1, std::atoi(c));
   const int grid = static_cast<int>(std::min<size_t>(chunks.size(), static_cast<size_t>(cap)));
-  chunk_copy_kernel<<<grid, COPY_THREADS, 0, st>>>(d, static_cast<int>(chunks.size()));
-  RLB_CUDA(cudaGetLastError());
-  RLB_CUDA(cudaFreeAsync(d, st));
+  RLB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&d), bytes, st));
+  // the chunk list is freed stream-ordered on every path once it is allocated
+  cudaError_t e = cudaMemcpyAsync(d, chunks.data(), bytes, cudaMemcpyHostToDevice, st);
+  if (e == cudaSuccess) {
+    chunk_copy_kernel<<<grid, COPY_THREADS, 0, st>>>(d, static_cast<int>(chunks.size()));
+    e = cudaGetLastError();
+  }
+  const cudaError_t ef = cudaFreeAsync(d, st);
+  RLB_CUDA(e);
+  RLB_CUDA(ef);
   return RLB_OK;
 }
 
