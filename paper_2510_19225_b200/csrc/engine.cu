@@ -210,6 +210,9 @@ struct rlb_instance {
   }
   bool qkv_kps2 = true;   // RLB_QKV_KPS=1: one K block per stage
   int qkv_launch(const TilePlan& tp, const LayerW& w, const GemmParams& pq) {
+    // prefill chunks: persistent 2-SM tiles with the same RoPE / KV epilogue
+    if ((pairp & 16) && pq.M > 512 && QKV % 256 == 0)
+      return gemm_launch_pairp(m_xn, w.m_qkv, EPI_ROPE, pq, st);
     if (tp.bn_qkv == 64 && qkv_kps2)
       return gemm_launch(m_xn_x2, w.m_qkv64x2, 64, EPI_ROPE, pq, st, tp.bm_qkv, 1, 2);
     return gemm_launch(m_xn, tp.bn_qkv == 64 ? w.m_qkv64 : w.m_qkv, tp.bn_qkv, EPI_ROPE, pq, st,
@@ -355,7 +358,7 @@ struct rlb_instance {
   // us), down, O in prefill and gate_up in prefill chunks; at a 512-row
   // decode gate_up has ~2 tiles per cluster and gains nothing.  Same bits as
   // the single-SM kernels.
-  int pairp = 2 | 4 | 8;
+  int pairp = 2 | 4 | 8 | 16;   // + bit 16: QKV (RoPE epilogue) in prefill chunks
   bool pairp_prefill = true;
   bool cl_down_large = false;
   int mc_gu = 1;   // gate_up A-multicast pairs at > 256 rows (RLB_GU_MC=2)

@@ -1128,10 +1128,16 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       const int m = mt * 256 + r * HM + q * 32 + lane;
       const bool live = m < p.M;
       const bool warp_dead = mt * 256 + r * HM + q * 32 >= p.M;
+      RopeRow rrow;   // EPI_ROPE: row metadata loaded while the tile's MMAs run
+      if constexpr (EPI == EPI_ROPE) rrow = rope_row_prefetch(p, m, live, nt * BN + ch * 128, 0, 2);
       mbar_wait(smem_u32(&tfull[b]), (i >> 1) & 1);
       tc_fence_after();
       const uint32_t tbase = tmem + b * BN + ch * 128 + (static_cast<uint32_t>(q * 32) << 16);
-      if constexpr (EPI == EPI_SWIGLU) {
+      if constexpr (EPI == EPI_ROPE) {
+        // bias + RoPE + q / paged K, V stores of this warp's 128 columns (two
+        // 64-column rotation blocks), the single-SM kernel's epilogue
+        if (!warp_dead) rope_direct(p, tbase, m, live, nt * BN + ch * 128, 0, 2, rrow);
+      } else if constexpr (EPI == EPI_SWIGLU) {
         bf16* out = reinterpret_cast<bf16*>(p.out);
 #pragma unroll 1
         for (int jc = 0; jc < (warp_dead ? 0 : 64); jc += 32) {
@@ -1332,6 +1338,8 @@ int gemm_prepare() {
                                 cudaFuncAttributeMaxDynamicSharedMemorySize, PairPCfg<EPI_SWIGLU>::SMEM));
   RLB_CUDA(cudaFuncSetAttribute(gemm_pairp_tc<EPI_ARGMAX>,
                                 cudaFuncAttributeMaxDynamicSharedMemorySize, PairPCfg<EPI_ARGMAX>::SMEM));
+  RLB_CUDA(cudaFuncSetAttribute(gemm_pairp_tc<EPI_ROPE>,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize, PairPCfg<EPI_ROPE>::SMEM));
   RLB_CUDA(cudaFuncSetAttribute(gemm_pairp_tc<EPI_PARTIAL>,
                                 cudaFuncAttributeMaxDynamicSharedMemorySize, PairPCfg<EPI_PARTIAL>::SMEM));
   done[dev & 63] = true;
@@ -1469,9 +1477,11 @@ int gemm_launch_pairp(const CUtensorMap& a, const CUtensorMap& b128, int epi, co
   if (p.M <= 0) return RLB_OK;
   RLB_CHECK(p.K % BK == 0 && (p.splits == 1 || epi == EPI_PARTIAL), RLB_ERR_ARG,
             "persistent pair GEMM: K multiple of 64, split-K only with fp32 partials");
-  RLB_CHECK(epi == EPI_SWIGLU || epi == EPI_ARGMAX || (epi == EPI_PARTIAL && p.ws != nullptr &&
-                                                       p.splits >= 1 && p.K / BK >= p.splits),
-            RLB_ERR_ARG, "persistent pair GEMM epilogues: SwiGLU, argmax, fp32 partials");
+  RLB_CHECK(epi == EPI_SWIGLU || epi == EPI_ARGMAX ||
+                (epi == EPI_ROPE && p.splits == 1 && p.bias != nullptr && p.N % 256 == 0 &&
+                 (p.rope.d == 64 || p.rope.d == 128)) ||
+                (epi == EPI_PARTIAL && p.ws != nullptr && p.splits >= 1 && p.K / BK >= p.splits),
+            RLB_ERR_ARG, "persistent pair GEMM epilogues: SwiGLU, argmax, RoPE, fp32 partials");
   RLB_CHECK(epi != EPI_SWIGLU || p.N % 256 == 0, RLB_ERR_ARG, "SwiGLU pair tiles are 256 wide");
   static int n_sm = 0;
   if (!n_sm) {
@@ -1497,6 +1507,7 @@ int gemm_launch_pairp(const CUtensorMap& a, const CUtensorMap& b128, int epi, co
   cfg.numAttrs = pdl_enabled(RLB_PDL_CLASS) ? 2 : 1;
   if (epi == EPI_SWIGLU) RLB_CUDA(cudaLaunchKernelEx(&cfg, gemm_pairp_tc<EPI_SWIGLU>, a, b128, p));
   else if (epi == EPI_PARTIAL) RLB_CUDA(cudaLaunchKernelEx(&cfg, gemm_pairp_tc<EPI_PARTIAL>, a, b128, p));
+  else if (epi == EPI_ROPE) RLB_CUDA(cudaLaunchKernelEx(&cfg, gemm_pairp_tc<EPI_ROPE>, a, b128, p));
   else RLB_CUDA(cudaLaunchKernelEx(&cfg, gemm_pairp_tc<EPI_ARGMAX>, a, b128, p));
   return RLB_OK;
 }
