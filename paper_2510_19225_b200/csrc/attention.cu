@@ -365,8 +365,14 @@ __device__ __forceinline__ void mma_bf16_full(float (&d)[4], uint32_t a0, uint32
 #ifndef ATTN_PAIR_MINB
 #define ATTN_PAIR_MINB 3
 #endif
-template <int D>
-__global__ void __launch_bounds__(WARPS * 32, ATTN_PAIR_MINB) attn_pair_kernel(AttnArgs a) {
+// NW = 2: the short-pair variant -- rows with <= 2 pages of context only
+// have pages in warp slots 0 and 1, so two physical warps do all the work and
+// slots 2, 3 enter the merge as the empty partials (m = -inf, l = 0, o = 0)
+// an idle warp of the 4-warp kernel contributes: the same merge, the same
+// bits, at half the CTA footprint.
+template <int D, int NW = WARPS>
+__global__ void __launch_bounds__(NW * 32, NW == WARPS ? ATTN_PAIR_MINB : 2 * ATTN_PAIR_MINB)
+    attn_pair_kernel(AttnArgs a) {
   constexpr int STAGES = ATTN_PAIR_STAGES;   // pipeline depth only: no effect on the bits
   constexpr int ROWB = D * 2;
   constexpr int CPR = ROWB / 16;
@@ -381,7 +387,8 @@ __global__ void __launch_bounds__(WARPS * 32, ATTN_PAIR_MINB) attn_pair_kernel(A
   const int G = a.NQ / a.NKV;
   pdl_trigger();
   pdl_wait();
-  const int rA = 2 * blockIdx.z;
+  const int rA = 2 * (a.pair_ids ? a.pair_ids[(NW == WARPS ? a.n_short : 0) + blockIdx.z]
+                                  : static_cast<int>(blockIdx.z));
   const bool hasB = rA + 1 < a.R;
   const bool shared = hasB && a.row_slot[rA] == a.row_slot[rA + 1];
   const float scale = rsqrtf(static_cast<float>(D)) * 1.4426950408889634f;
@@ -556,6 +563,22 @@ __global__ void __launch_bounds__(WARPS * 32, ATTN_PAIR_MINB) attn_pair_kernel(A
         mls[(warp * 16 + 8 + h) * 2] = m_run[1];
         mls[(warp * 16 + 8 + h) * 2 + 1] = l_run[1];
       }
+      if constexpr (NW < WARPS) {   // the idle slots' partials, as the 4-warp kernel has them
+        for (int w = NW + warp; w < WARPS; w += NW) {
+#pragma unroll
+          for (int t = 0; t < NT; ++t) {
+            const int col = t * 8 + 2 * (lane & 3);
+            *reinterpret_cast<float2*>(&red[(w * 16 + h) * D + col]) = make_float2(0.f, 0.f);
+            *reinterpret_cast<float2*>(&red[(w * 16 + 8 + h) * D + col]) = make_float2(0.f, 0.f);
+          }
+          if ((lane & 3) == 0) {
+            mls[(w * 16 + h) * 2] = -INFINITY;
+            mls[(w * 16 + h) * 2 + 1] = 0.f;
+            mls[(w * 16 + 8 + h) * 2] = -INFINITY;
+            mls[(w * 16 + 8 + h) * 2 + 1] = 0.f;
+          }
+        }
+      }
     }
     // per (row, head) slot: the running max over the warps, each warp's
     // rescale factor and the merged denominator, once per slot instead of
@@ -578,7 +601,7 @@ __global__ void __launch_bounds__(WARPS * 32, ATTN_PAIR_MINB) attn_pair_kernel(A
       cws[slot * (WARPS + 2) + WARPS + 1] = L;
     }
     __syncthreads();
-    for (int i = threadIdx.x; i < 2 * G * D; i += WARPS * 32) {
+    for (int i = threadIdx.x; i < 2 * G * D; i += NW * 32) {
       const int x = i / (G * D), g = (i / D) % G, d = i % D;
       if (x == 1 && !two) break;
       const int rr = x == 0 ? r0 : rA + 1;
@@ -637,6 +660,8 @@ static int launch_attn(const AttnArgs& a, cudaStream_t st, bool pairs) {
   constexpr int smem_red2 = WARPS * 16 * D * 4 + WARPS * 16 * 2 * 4 + 16 * (WARPS + 2) * 4;
   constexpr int smem_pipe2 = WARPS * ATTN_PAIR_STAGES * 2 * CHUNK * D * 2;
   constexpr int smem2 = smem_pipe2 > smem_red2 ? smem_pipe2 : smem_red2;
+  constexpr int smem_pipe2s = 2 * ATTN_PAIR_STAGES * 2 * CHUNK * D * 2;   // 2-warp short pairs
+  constexpr int smem2s = smem_pipe2s > smem_red2 ? smem_pipe2s : smem_red2;
   static bool attr[64] = {false};
   int dev = 0;
   RLB_CUDA(cudaGetDevice(&dev));
@@ -644,6 +669,8 @@ static int launch_attn(const AttnArgs& a, cudaStream_t st, bool pairs) {
     RLB_CUDA(cudaFuncSetAttribute(attn_mma_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     RLB_CUDA(cudaFuncSetAttribute(attn_pair_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   smem2));
+    RLB_CUDA(cudaFuncSetAttribute(attn_pair_kernel<D, 2>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, smem2s));
     RLB_CUDA(cudaFuncSetAttribute(attn_mma_persistent<D>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     attr[dev & 63] = true;
@@ -654,7 +681,14 @@ static int launch_attn(const AttnArgs& a, cudaStream_t st, bool pairs) {
     const char* e = std::getenv("RLB_ATTN_PERSIST");
     return e ? std::atoi(e) : 0;
   }();
-  if (pairs) {
+  if (pairs && a.pair_ids) {
+    if (a.n_short > 0)
+      RLB_CUDA(launch_k(attn_pair_kernel<D, 2>, dim3(a.max_splits, a.NKV, a.n_short), dim3(64),
+                        smem2s, st, a));
+    if (a.n_long > 0)
+      RLB_CUDA(launch_k(attn_pair_kernel<D>, dim3(a.max_splits, a.NKV, a.n_long),
+                        dim3(WARPS * 32), smem2, st, a));
+  } else if (pairs) {
     RLB_CUDA(launch_k(attn_pair_kernel<D>, dim3(a.max_splits, a.NKV, (a.R + 1) / 2),
                       dim3(WARPS * 32), smem2, st, a));
   } else if (persist) {

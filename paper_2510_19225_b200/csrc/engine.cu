@@ -221,6 +221,12 @@ struct rlb_instance {
   int32_t *d_ring = nullptr, *d_ring_ctr = nullptr, *d_ring_cur = nullptr, *h_ring = nullptr;
   // K5 export scratch (rlb_export_partials)
   int* d_exp_slots = nullptr;
+  // prefill row pairs split by context length (short: <= 2 pages, 2-warp
+  // attention CTAs); set per chunk by admit_and_prefill (RLB_ATTN_SPLIT=0: off)
+  int* d_pairs = nullptr;
+  std::vector<int> h_pairs;
+  int pairs_short = 0, pairs_long = 0;
+  bool attn_split = true;
   int64_t* d_exp_cu = nullptr;
   int32_t* d_exp_out = nullptr;
   float2* d_rope = nullptr;
@@ -405,7 +411,7 @@ rlb_instance::~rlb_instance() {
   void* bufs[] = {arena, kv, d_bt, d_seq_tokens, d_seq_len, d_seq_target, d_row_tok, d_row_pos,
                   d_row_slot, d_logit_src, d_logit_slot, d_dec_slots, d_h, d_xn, d_qkv, d_q,
                   d_attn, d_act, d_logits, d_ws, d_ring, d_ring_ctr, d_ring_cur, d_rope,
-                  d_part, d_exp_slots, d_exp_cu, d_exp_out};
+                  d_part, d_exp_slots, d_exp_cu, d_exp_out, d_pairs};
   for (void* b : bufs)
     if (b) cudaFree(b);
   if (shadow.arena) cudaFree(shadow.arena);
@@ -492,6 +498,7 @@ int rlb_instance::init() {
   if (const char* ov = std::getenv("RLB_GU_MC")) mc_gu = std::atoi(ov) == 2 ? 2 : 1;
   if (const char* ov = std::getenv("RLB_QKV_BN")) bn_qkv_decode = std::atoi(ov) == 128 ? 128 : 64;
   if (const char* ov = std::getenv("RLB_ATTN_PAIRS")) attn_pairs = std::atoi(ov) != 0;
+  if (const char* ov = std::getenv("RLB_ATTN_SPLIT")) attn_split = std::atoi(ov) != 0;
   if (const char* ov = std::getenv("RLB_QKV_KPS")) qkv_kps2 = std::atoi(ov) == 2;
   if (const char* ov = std::getenv("RLB_O_KPS")) o_kps2 = std::atoi(ov) == 2;
   if (const char* ov = std::getenv("RLB_SMALL_GU_WAVE")) small_gu_wave = std::atoi(ov) != 0;
@@ -564,6 +571,7 @@ int rlb_instance::init() {
   const size_t part = std::max({static_cast<size_t>(sp_o) * H, static_cast<size_t>(sp_down) * H});
   if ((rc = dalloc(&d_part, part * R))) return rc;
   if ((rc = dalloc(&d_ring, static_cast<size_t>(RING_ROWS) * max_slots))) return rc;
+  if ((rc = dalloc(&d_pairs, max_rows / 2 + 1))) return rc;
   if ((rc = dalloc(&d_exp_slots, max_slots)) || (rc = dalloc(&d_exp_cu, max_slots + 1)) ||
       (rc = dalloc(&d_exp_out, static_cast<size_t>(max_slots) * max_seq)))
     return rc;
@@ -676,6 +684,11 @@ int rlb_instance::forward_layers(int R, bool prefill) {
     if ((rc = qkv_launch(tp, w, pq))) return rc;
     AttnArgs a{d_q, NQ * D, kv_l, d_bt, pps, d_row_slot, d_row_pos, R, NQ, NKV, D, max_splits,
                d_ws, d_attn, NQ * D};
+    if (prefill && attn_pairs && attn_split && pairs_short + pairs_long > 0) {
+      a.pair_ids = d_pairs;
+      a.n_short = pairs_short;
+      a.n_long = pairs_long;
+    }
     if ((rc = attention_launch(a, st, prefill && attn_pairs))) return rc;
     if (cl_o && !pair_o(R)) {
       if ((rc = proj(m_attn, w.m_o, BN_O, sp_o, EPI_RESADD, R, H, NQ * D, nullptr, d_h, H,
@@ -874,10 +887,32 @@ int rlb_instance::admit_and_prefill(int* rows_run) {
       RLB_CUDA(cudaMemcpyAsync(d_logit_src, lsrc + beg, nl * sizeof(int), cudaMemcpyHostToDevice, st));
       RLB_CUDA(cudaMemcpyAsync(d_logit_slot, lslot + beg, nl * sizeof(int), cudaMemcpyHostToDevice, st));
     }
+    // row pairs (2p, 2p+1) of this chunk: those whose rows all see <= 2 pages
+    // of context first (2-warp attention CTAs), then the rest
+    pairs_short = pairs_long = 0;
+    if (attn_pairs && attn_split) {
+      const int np = static_cast<int>((n + 1) / 2);
+      h_pairs.resize(np);
+      int lo = 0, hi = np;
+      for (int z = 0; z < np; ++z) {
+        const size_t a0 = beg + 2 * static_cast<size_t>(z);
+        const bool short_pair = pos[a0] < 2 * PAGE && (a0 + 1 >= beg + n || pos[a0 + 1] < 2 * PAGE);
+        if (short_pair) h_pairs[lo++] = z;
+        else h_pairs[--hi] = z;
+      }
+      std::reverse(h_pairs.begin() + hi, h_pairs.end());   // long pairs in row order
+      pairs_short = lo;
+      pairs_long = np - lo;
+      RLB_CUDA(cudaMemcpyAsync(d_pairs, h_pairs.data(), np * sizeof(int), cudaMemcpyHostToDevice, st));
+      stats.h2d_bytes += static_cast<int64_t>(np) * 4;
+      if (pairs_short && pairs_long) stats.kernel_launches += m.layers;   // two attention launches
+    }
     if ((rc = seed_tokens_launch(d_row_tok, d_row_pos, d_row_slot, static_cast<int>(n), d_seq_tokens,
                                  max_seq, st)))
       return rc;
-    if ((rc = forward_layers(static_cast<int>(n), true))) return rc;
+    rc = forward_layers(static_cast<int>(n), true);
+    pairs_short = pairs_long = 0;   // the lists belong to this chunk only
+    if (rc) return rc;
     if ((rc = head(nl, true))) return rc;
     stats.h2d_bytes += static_cast<int64_t>(n) * 12 + static_cast<int64_t>(nl) * 8;
     stats.kernel_launches += 1 + launches_per_forward(nl);
@@ -1480,6 +1515,7 @@ int rlb_score(rlb_instance* h, const int32_t* tokens, int32_t n, float* out_logi
     pos[i] = i;
     slot[i] = s;
   }
+  h->pairs_short = h->pairs_long = 0;   // every row pair on the 4-warp kernel
   for (int beg = 0; beg < n && rc == 0; beg += h->prefill_rows) {
     const int cnt = std::min(h->prefill_rows, n - beg);
     RLB_CUDA(cudaMemcpyAsync(h->d_row_tok, tok + beg, cnt * 4, cudaMemcpyHostToDevice, h->st));

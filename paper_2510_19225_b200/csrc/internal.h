@@ -60,6 +60,11 @@ struct AttnArgs {
   int R, NQ, NKV, D, max_splits;
   float* ws;                        // [R][NQ][max_splits][D+2]
   bf16* out; int ldo;
+  // prefill row pairs split by length (row_pairs mode): pair_ids[0, n_short)
+  // hold pairs whose rows all have <= 2 pages of context (a 2-warp kernel),
+  // pair_ids[n_short, n_short + n_long) the rest; null = every pair, 4 warps
+  const int* pair_ids = nullptr;
+  int n_short = 0, n_long = 0;
 };
 int attention_launch(const AttnArgs& a, cudaStream_t st, bool row_pairs = false);
 int attention_windows(int max_seq);   // CTA windows per row (AttnArgs.max_splits)

@@ -314,3 +314,18 @@ def test_o_two_k_blocks_per_stage_same_tokens(mid, monkeypatch, n_prompts):
     monkeypatch.setenv("RLB_O_KPS", "1")
     ref = _rollout(_instance(shape, w, max_slots=512, max_seq_len=1024), prompts, 40)
     assert got == ref
+
+
+def test_prefill_short_pairs_same_tokens(mid, monkeypatch):
+    """Prefill row pairs with <= 2 pages of context run on 2-warp attention
+    CTAs (the idle warp slots merged as empty partials): migration resume
+    and rollouts give the same tokens as the single 4-warp launch
+    (RLB_ATTN_SPLIT=0)."""
+    shape, w, _ = mid
+    prompts = synth_prompts(10, shape.vocab, 60, 300, seed=23)
+    got = _rollout(_instance(shape, w, max_slots=16, max_seq_len=1024, max_prefill_rows=700),
+                   prompts, 48)
+    monkeypatch.setenv("RLB_ATTN_SPLIT", "0")
+    ref = _rollout(_instance(shape, w, max_slots=16, max_seq_len=1024, max_prefill_rows=700),
+                   prompts, 48)
+    assert got == ref
