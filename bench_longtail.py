@@ -61,15 +61,15 @@ def main():
     import torch
     from oracle.audit import assert_token_conservation, assert_version_gating
     from paper_2510_19225_b200 import _lib
-    from paper_2510_19225_b200.events import EventLog
     from paper_2510_19225_b200.instance import RolloutInstance
-    from paper_2510_19225_b200.manager import RolloutManager
-    from paper_2510_19225_b200.profile import estimate_plateau, measured_profile_table
-    from paper_2510_19225_b200.rebalance import MigrationKind
+    from paper_2510_19225_b200.profile import measured_profile_table
     from paper_2510_19225_b200.runner import RolloutRunner
     from paper_2510_19225_b200.shapes import SHAPES
     from paper_2510_19225_b200.synth import synth_hf_weights, synth_prompts
-    from paper_2510_19225_b200.transfer import TransferPool, build_agents
+    from spotrl.balancer import MigrationKind, estimate_plateau
+    from spotrl.events import EventLog
+    from spotrl.manager import RolloutManager
+    from spotrl.transfer import TransferPool, build_agents
 
     shape = SHAPES[args.shape]
     n_gpu = torch.cuda.device_count()
@@ -87,13 +87,13 @@ def main():
                  for k, iid in enumerate(ids)}
 
     def run_once(tag, profile):
-        m = RolloutManager(theta=args.theta, log=EventLog())
+        m = RolloutManager(theta=args.theta, m_b=16, log=EventLog())
         m.n_prem_cap = n
         pool = TransferPool(build_agents(1, 1, 900e9))
         run = RolloutRunner(m, pool, flush_steps=args.flush_steps, model_bytes=shape.n_bytes(),
                             max_inflight=args.max_inflight)
         m.begin_step(1, run.now())
-        pool.stage(1, source=w, now=run.now())
+        run.stage(1, w)
         for iid in ids:
             instances[iid].decode_profile(reset=True)
             assert run.add_instance(iid, instances[iid])

@@ -44,13 +44,14 @@ def main():
     import torch
     from oracle.audit import assert_token_conservation, assert_version_gating
     from paper_2510_19225_b200 import _lib
-    from paper_2510_19225_b200.events import EventLog
     from paper_2510_19225_b200.instance import RolloutInstance
-    from paper_2510_19225_b200.manager import RolloutManager
     from paper_2510_19225_b200.runner import RolloutRunner
     from paper_2510_19225_b200.shapes import SHAPES
-    from paper_2510_19225_b200.synth import parse_trace, preemption_trace, synth_hf_weights, synth_prompts
-    from paper_2510_19225_b200.transfer import TransferPool, build_agents
+    from paper_2510_19225_b200.synth import preemption_trace, synth_hf_weights, synth_prompts
+    from spotrl.events import EventLog
+    from spotrl.manager import RolloutManager
+    from spotrl.traces import TraceEventKind, parse_trace
+    from spotrl.transfer import TransferPool, build_agents
 
     shape = SHAPES[args.shape]
     n_gpu = torch.cuda.device_count()
@@ -60,9 +61,9 @@ def main():
     victims = ids[1::max(1, n // kill_n)][:kill_n] if kill_n else []
     trace = preemption_trace(ids, victims, args.kill_at)
     kill_at: dict[int, list[str]] = {}
-    for ev in parse_trace(trace):
-        if ev["kind"] == "preempt":
-            kill_at.setdefault(int(ev["at"]), []).append(ev["instance_id"])
+    for ev in parse_trace(trace.splitlines()):
+        if ev.kind is TraceEventKind.PREEMPT:
+            kill_at.setdefault(int(ev.at), []).append(ev.instance_id)
 
     # trainer weights on GPU 0; every instance pulls them (peer reads over NVLink)
     w = synth_hf_weights(shape, seed=0, device="cuda:0")
@@ -75,12 +76,12 @@ def main():
 
     def build(tag):
         log = EventLog()
-        m = RolloutManager(theta=args.prompts, log=log)
+        m = RolloutManager(theta=args.prompts, m_b=16, log=log)
         m.n_prem_cap = n
         pool = TransferPool(build_agents(1, 1, 900e9))
         run = RolloutRunner(m, pool, flush_steps=args.flush_steps, model_bytes=shape.n_bytes())
         m.begin_step(1, run.now())
-        pool.stage(1, source=w, now=run.now())
+        run.stage(1, w)
         for k, iid in enumerate(ids):
             inst = RolloutInstance(shape, k % n_gpu, max_slots=max_slots, max_seq_len=max_seq,
                                    graph_steps=16)

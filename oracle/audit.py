@@ -8,10 +8,15 @@ records enforces single ownership and append-only token growth
 (`audit_requests`, oracles.py:146-196), exact token conservation per request
 and over route legs (`assert_token_conservation`, oracles.py:199-209), and
 version gating of remote token events (`assert_version_gating`,
-oracles.py:212-236).  The restatement runs on logs written by the B200 path
-(manager.py mirror + real instances) and is pinned against the reference's
-own logs and counts in tests/golden/ref_sim_*.jsonl.gz
-(tests/test_audit.py).
+oracles.py:212-236).  The restatement is pinned against the reference's own
+logs and counts in tests/golden/ref_sim_*.jsonl.gz (tests/test_audit.py).
+
+When `__graft_entry__.build()` has installed the reference's test oracles
+unmodified (`baseline/_ref/spotrl_reftests/oracles.py`, copied from
+`pkg/tests/oracles.py`), the module-level names at the bottom are rebound to
+THOSE functions, so the B200 path's event logs are audited by the reference's
+own code; the restatement stays available as `restated_*` and is checked to
+agree with it.
 """
 from __future__ import annotations
 
@@ -86,3 +91,31 @@ def assert_version_gating(records: list[dict]) -> int:
             assert pulled.get(rec["instance_id"]) == step_version, (
                 f"{rec['instance_id']} emitted tokens without pulling version {step_version}")
     return checked
+
+
+restated_audit_requests = audit_requests
+restated_assert_token_conservation = assert_token_conservation
+restated_assert_version_gating = assert_version_gating
+
+
+def reference_oracles():
+    """The reference's own `pkg/tests/oracles.py` (as installed by build()), or None."""
+    import os
+    import sys
+    ref = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                       "baseline", "_ref")
+    if os.path.isdir(os.path.join(ref, "spotrl_reftests")) and ref not in sys.path:
+        sys.path.append(ref)
+    try:
+        from spotrl_reftests import oracles
+    except ImportError:
+        return None
+    return oracles
+
+
+_REF = reference_oracles()
+SOURCE = "reference" if _REF is not None else "restatement"
+if _REF is not None:
+    audit_requests = _REF.audit_requests  # noqa: F811
+    assert_token_conservation = _REF.assert_token_conservation  # noqa: F811
+    assert_version_gating = _REF.assert_version_gating  # noqa: F811

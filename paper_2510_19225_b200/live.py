@@ -31,10 +31,12 @@ import threading
 import time
 from typing import Callable
 
-from .domain import InstanceStatus, RequestState
+from spotrl.domain import InstanceStatus
+
 from .protocol import (DONE_KIND, SHARD_KIND, InstanceAdapter, ProtocolError, decode_line,
                        encode_message, msg_cancel, msg_generate, msg_pull_weights, read_frames,
                        read_pull_request, write_done, write_pull_request, write_shard)
+from .responses import ResponseBuffer, dispatch
 
 TCP_SCHEME = "tcp://"
 
@@ -80,12 +82,16 @@ class _Conn:
 
 
 class ManagerServer:
-    """The manager side of live mode.  `endpoint_for(instance_id)` names the
-    agent endpoint each registering instance pulls `version` from."""
+    """The manager side of live mode around an unmodified reference
+    `RolloutManager`.  `endpoint_for(instance_id)` names the agent endpoint
+    each registering instance pulls `version` from; requests are created with
+    `submit` (prompt ids go to the `ResponseBuffer`)."""
 
     def __init__(self, manager, version: int, endpoint_for: Callable[[str], str], *,
-                 host: str = "127.0.0.1", port: int = 0, max_inflight: int | None = None):
+                 host: str = "127.0.0.1", port: int = 0, max_inflight: int | None = None,
+                 responses: ResponseBuffer | None = None):
         self.manager = manager
+        self.responses = responses if responses is not None else ResponseBuffer(manager)
         self.version = version
         self.endpoint_for = endpoint_for
         self.max_inflight = max_inflight
@@ -102,6 +108,11 @@ class ManagerServer:
 
     def now(self) -> float:
         return time.perf_counter() - self._t0
+
+    def submit(self, request_id: str, prompt_tokens: list[int], target_len: int,
+               group_id: str = "g"):
+        return self.responses.create_request(request_id, prompt_tokens, target_len, group_id,
+                                             self.now())
 
     def _accept(self) -> None:
         cid = 0
@@ -152,7 +163,7 @@ class ManagerServer:
                 m.log.emit(now, "pull_done", instance_id=iid, version=msg["weight_version"],
                            seconds=now - self._pull_t0.pop(iid, now))
         elif t == "token":
-            m.on_tokens(msg["request_id"], self.iid_of[cid], 1, now, token_ids=[msg["token_id"]])
+            self.responses.on_tokens(msg["request_id"], self.iid_of[cid], [msg["token_id"]], now)
         elif t == "complete":
             m.complete(msg["request_id"], self.iid_of[cid], now)
         else:
@@ -160,7 +171,7 @@ class ManagerServer:
 
     def _dispatch_and_admit(self) -> None:
         m, now = self.manager, self.now()
-        m.dispatch(now)
+        dispatch(m, now)
         for iid, conn in list(self.conn_of.items()):
             out = []
             for rid in list(m.pending_queues.get(iid, ())):
@@ -169,7 +180,7 @@ class ManagerServer:
                     break
                 req = m.requests[rid]
                 m.admit(rid, iid, now)
-                msg = msg_generate(rid, list(req.prompt_tokens), list(req.generated))
+                msg = msg_generate(rid, self.responses.prompt(rid), list(req.generated))
                 msg["target_len"] = req.target_len
                 out.append(msg)
             if out:

@@ -59,33 +59,10 @@ def synth_prompts(n: int, vocab: int, lo: int, hi: int, seed: int = 1) -> list[l
 
 
 def preemption_trace(instance_ids: list[str], kill: list[str], at_step: int) -> str:
-    """A `.trace.jsonl` in the reference trace format (`pkg/src/spotrl/traces.py:1-7`:
-    `{"at", "kind", "instance_id"}` per line): allocate every instance at 0,
-    preempt `kill` at `at` = `at_step` (time is in decode-step units)."""
-    lines = [json.dumps({"at": 0.0, "kind": "allocate", "instance_id": i}) for i in instance_ids]
-    lines += [json.dumps({"at": float(at_step), "kind": "preempt", "instance_id": i}) for i in kill]
-    return "\n".join(lines) + "\n"
-
-
-def parse_trace(text: str) -> list[dict]:
-    """Parse + validate like `pkg/src/spotrl/traces.py:41-75`: non-decreasing
-    time, allocate/preempt alternating per instance starting with allocate."""
-    events: list[dict] = []
-    last_at = 0.0
-    alive: dict[str, bool] = {}
-    for lineno, raw in enumerate(text.splitlines(), start=1):
-        line = raw.strip()
-        if not line:
-            continue
-        rec = json.loads(line)
-        at, kind, iid = float(rec["at"]), rec["kind"], str(rec["instance_id"])
-        if kind not in ("allocate", "preempt"):
-            raise ValueError(f"line {lineno}: unknown kind {kind!r}")
-        if at < last_at:
-            raise ValueError(f"line {lineno}: time regression {at} < {last_at}")
-        if (kind == "allocate") == alive.get(iid, False):
-            raise ValueError(f"line {lineno}: {iid} out-of-order {kind}")
-        alive[iid] = kind == "allocate"
-        last_at = at
-        events.append({"at": at, "kind": kind, "instance_id": iid})
-    return events
+    """A `.trace.jsonl` in the reference trace format (`pkg/src/spotrl/traces.py:1-7`),
+    written by the reference's own `serialize_trace`: allocate every instance
+    at 0, preempt `kill` at `at` = `at_step` (time in decode-step units)."""
+    from spotrl.traces import TraceEvent, TraceEventKind, serialize_trace
+    events = [TraceEvent(0.0, TraceEventKind.ALLOCATE, i) for i in instance_ids]
+    events += [TraceEvent(float(at_step), TraceEventKind.PREEMPT, i) for i in kill]
+    return serialize_trace(events)

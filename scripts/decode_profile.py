@@ -10,7 +10,8 @@ import sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
 from paper_2510_19225_b200.instance import RolloutInstance
-from paper_2510_19225_b200.profile import estimate_plateau, measured_profile_table
+from paper_2510_19225_b200.profile import measured_profile_table
+from spotrl.balancer import estimate_plateau
 from paper_2510_19225_b200.shapes import SHAPES
 from paper_2510_19225_b200.synth import synth_hf_weights, synth_prompts
 

@@ -1,7 +1,6 @@
 """Host bookkeeping on the rollout path, one core:
-the manager mirror's token collection per token and in bulk flushes, and
-migrate_out + route_to per request -- next to the unmodified reference
-manager when /root/reference is importable (builder container).
+the unmodified reference manager's token collection per token and in bulk
+flushes, and migrate_out + route_to per request.
 
     python scripts/host_bench.py [out.json]
 """
@@ -74,13 +73,9 @@ def bench(mod_manager, mod_events, label, bulk):
 
 def main():
     import platform
-    from paper_2510_19225_b200 import events, manager
-    res = [bench(manager, events, "b200 host mirror", bulk=True)]
-    ref_src = "/root/reference/pkg/src"
-    if os.path.isdir(ref_src):
-        sys.path.append(ref_src)
-        from spotrl import events as rev, manager as rman   # unmodified reference
-        res.append(bench(rman, rev, "reference spotrl", bulk=True))
+    import paper_2510_19225_b200  # noqa: F401  (puts the installed reference on sys.path)
+    from spotrl import events as rev, manager as rman   # unmodified reference
+    res = [bench(rman, rev, "reference spotrl", bulk=True)]
     doc = {"cpu": platform.processor() or platform.machine(), "cores": 1, "B": B,
            "flushes": STEPS, "tokens_per_flush": K, "results": res}
     print(json.dumps(doc, indent=1))

@@ -96,24 +96,7 @@ def ref_sim():
         print(path, facts, len(recs))
 
 
-def ref_manager():
-    sys.path[:0] = [f"{REF}/src"]
-    from spotrl.events import EventLog
-    from spotrl.manager import RolloutManager
-    import manager_script
-    for policy in ("migrate", "recompute"):
-        log = EventLog()
-        mgr = RolloutManager(theta=3, m_b=4, log=log, migration=policy)
-        errors = manager_script.run(mgr)
-        path = os.path.join(GOLD, f"ref_manager_script_{policy}.jsonl")
-        with open(path, "w") as f:
-            f.write(json.dumps({"errors": errors}) + "\n")
-            f.write(log.to_jsonl())
-        print(path, len(log.records), errors)
-
-
 if __name__ == "__main__":
     os.makedirs(GOLD, exist_ok=True)
     tiny_hf()
     ref_sim()
-    ref_manager()

@@ -7,7 +7,8 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 if ROOT not in sys.path:
     sys.path.insert(0, ROOT)
 
-REFERENCE_SRC = "/root/reference/pkg/src"
+import paper_2510_19225_b200  # noqa: E402,F401  (puts the installed reference `spotrl` on sys.path)
+
 REFERENCE_TESTS = "/root/reference/pkg/tests"
 
 
@@ -16,17 +17,11 @@ def pytest_configure(config):
     config.addinivalue_line("markers", "reference: needs /root/reference (builder container only)")
 
 
-def has_reference() -> bool:
-    return os.path.isdir(REFERENCE_SRC)
-
-
 @pytest.fixture(scope="session")
-def spotrl():
-    """The unmodified reference package, imported read-only (builder container only)."""
-    if not has_reference():
-        pytest.skip("reference package not present (it does not travel to the GPU box)")
-    for p in (REFERENCE_SRC, REFERENCE_TESTS):
-        if p not in sys.path:
-            sys.path.append(p)
-    import spotrl as mod
-    return mod
+def ref_tests():
+    """The reference's own test directory (builder container only)."""
+    if not os.path.isdir(REFERENCE_TESTS):
+        pytest.skip("reference tests not present (they do not travel to the GPU box)")
+    if REFERENCE_TESTS not in sys.path:
+        sys.path.append(REFERENCE_TESTS)
+    return REFERENCE_TESTS

@@ -22,14 +22,14 @@ def _worker(rank, ws, port, q):
                       RANK=str(rank), LOCAL_RANK=str(rank))
     dist.init_process_group("gloo", rank=rank, world_size=ws)
     from paper_2510_19225_b200 import multi
-    from paper_2510_19225_b200.events import EventLog
-    from paper_2510_19225_b200.manager import RolloutManager
+    from spotrl.events import EventLog
+    from spotrl.manager import RolloutManager
     from paper_2510_19225_b200.runner import RolloutRunner
     from tests.fakes import FakeInstance
 
     assert multi.dist_env() == (ws, rank, rank)
     # each rank: its own instance and prompts (weak scaling), no data-path collective
-    m = RolloutManager(theta=64, log=EventLog())
+    m = RolloutManager(theta=64, m_b=4, log=EventLog())
     m.n_prem_cap = 1
     run = RolloutRunner(m, None, flush_steps=7)
     m.begin_step(1, run.now())

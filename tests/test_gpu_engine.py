@@ -239,20 +239,20 @@ def test_seeding_handoff_bit_exact(tiny):
     """Seeding phase on a real local engine, hand-off to two remote B200
     instances mid-generation: every request's ids equal an
     uninterrupted rollout on one instance."""
-    from paper_2510_19225_b200.events import EventLog
+    from spotrl.events import EventLog
     from paper_2510_19225_b200.instance import RolloutInstance
-    from paper_2510_19225_b200.manager import RolloutManager
+    from spotrl.manager import RolloutManager
     from paper_2510_19225_b200.runner import RolloutRunner
-    from paper_2510_19225_b200.transfer import TransferPool, build_agents
+    from spotrl.transfer import TransferPool, build_agents
     w, _ = tiny
     prompts = synth_prompts(24, TINY.vocab, 16, 80, seed=17)
     want = _rollout(_instance(TINY, w, max_slots=32, max_seq_len=256), prompts, 90)
-    m = RolloutManager(theta=8, log=EventLog())
+    m = RolloutManager(theta=8, m_b=4, log=EventLog())
     m.n_prem_cap = 2
     pool = TransferPool(build_agents(1, 2, 900e9))
     run = RolloutRunner(m, pool, flush_steps=16, max_inflight=12)
     m.begin_step(1, run.now())
-    pool.stage(1, source=w, now=run.now())
+    run.stage(1, w)
     run.add_local_engine("local00", _instance(TINY, w, max_slots=16, max_seq_len=256))
     for k, p in enumerate(prompts):
         run.submit(f"r{k}", p, target_len=90)

@@ -19,10 +19,10 @@ def test_live_instances_over_tcp():
         pytest.skip("no CUDA device")
     from oracle.audit import assert_token_conservation
     from paper_2510_19225_b200 import _lib
-    from paper_2510_19225_b200.events import EventLog
+    from spotrl.events import EventLog
     from paper_2510_19225_b200.instance import RolloutInstance
     from paper_2510_19225_b200.live import AgentServer, ManagerServer, TcpPulledSource, serve_instance
-    from paper_2510_19225_b200.manager import RolloutManager
+    from spotrl.manager import RolloutManager
     from paper_2510_19225_b200.pull import TrainerWeights
 
     w = synth_hf_weights(TINY, seed=0, device="cuda")
@@ -51,13 +51,13 @@ def test_live_instances_over_tcp():
         direct.generate(f"r{k}", p, target_len=targets[k])
     want = direct.run_to_completion(16)
 
-    m = RolloutManager(theta=4, log=EventLog())
+    m = RolloutManager(theta=4, m_b=4, log=EventLog())
     m.n_prem_cap = 2
     m.begin_step(1, 0.0)
     ends = {"i0": agent.endpoint, "i1": "local://trainer"}
     srv = ManagerServer(m, version=1, endpoint_for=ends.__getitem__, max_inflight=6)
     for k, p in enumerate(prompts):
-        m.create_request(f"r{k}", len(p), targets[k], "g", 0.0, prompt_tokens=p)
+        srv.submit(f"r{k}", p, targets[k])
 
     def resolve(endpoint, version):
         if endpoint.startswith("tcp://"):

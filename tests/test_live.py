@@ -7,9 +7,9 @@ import threading
 import pytest
 
 from oracle.audit import assert_token_conservation, assert_version_gating
-from paper_2510_19225_b200.events import EventLog
+from spotrl.events import EventLog
 from paper_2510_19225_b200.live import AgentServer, ManagerServer, serve_instance
-from paper_2510_19225_b200.manager import RolloutManager
+from spotrl.manager import RolloutManager
 from paper_2510_19225_b200.protocol import ProtocolError, read_frames, write_pull_request
 from tests.fakes import FakeInstance, reference_continuation
 
@@ -22,13 +22,13 @@ def _prompts(n):
 
 @pytest.mark.parametrize("die", [None, 40])
 def test_live_rollout_over_tcp(die):
-    m = RolloutManager(theta=3, log=EventLog())
+    m = RolloutManager(theta=3, m_b=4, log=EventLog())
     m.n_prem_cap = 3
     m.begin_step(1, 0.0)
     srv = ManagerServer(m, version=1, endpoint_for=lambda iid: f"fake://{iid}", max_inflight=4)
     prompts = _prompts(18)
     for k, p in enumerate(prompts):
-        m.create_request(f"r{k}", len(p), 12 + k % 5, "g", 0.0, prompt_tokens=p)
+        srv.submit(f"r{k}", p, 12 + k % 5)
     stop = threading.Event()
     threads = []
     for k in range(3):

@@ -6,10 +6,10 @@ import random
 import pytest
 
 from oracle.audit import assert_token_conservation, assert_version_gating
-from paper_2510_19225_b200.events import EventLog
-from paper_2510_19225_b200.manager import RolloutManager
+from spotrl.events import EventLog
+from spotrl.manager import RolloutManager
 from paper_2510_19225_b200.runner import RolloutRunner
-from paper_2510_19225_b200.transfer import TransferPool, build_agents
+from spotrl.transfer import TransferPool, build_agents
 from tests.fakes import FakeInstance, reference_continuation
 
 
@@ -19,7 +19,7 @@ def make_runner(n_inst=4, theta=64, flush=5, migration="migrate"):
     pool = TransferPool(build_agents(1, 2, 900e9))
     run = RolloutRunner(m, pool, flush_steps=flush)
     m.begin_step(1, run.now())
-    pool.stage(1, source={"weights": "v1"}, now=run.now())
+    run.stage(1, {"weights": "v1"})
     for k in range(n_inst):
         assert run.add_instance(f"i{k}", FakeInstance(vocab=997, max_slots=6))
     return run
@@ -74,7 +74,7 @@ def test_step_boundary_swap_has_no_pull_window():
         run.submit(f"a{k}", p, target_len=20)
     run.pump()
     run.advance()
-    pool.stage(2, source={"weights": "v2"}, now=run.now())
+    run.stage(2, {"weights": "v2"})
     assert run.prefetch(2) == ["i0", "i1", "i2"]
     assert all(m.records[i].status.value == "active" and m.records[i].weight_version == 1
                for i in run.instances)
@@ -101,7 +101,7 @@ def test_begin_step_without_prefetch_pulls_blocking():
     for k, p in enumerate(prompts(4, seed=7)):
         run.submit(f"a{k}", p, target_len=8)
     run.run()
-    run.pool.stage(2, source={"weights": "v2"}, now=run.now())
+    run.stage(2, {"weights": "v2"})
     out = run.begin_step(2)
     assert out and not any(v["swapped"] for v in out.values())
     assert all(run.manager.records[i].weight_version == 2 for i in run.instances)
@@ -126,7 +126,7 @@ def test_seeding_handoff_to_remotes():
     pool = TransferPool(build_agents(1, 2, 900e9))
     run = RolloutRunner(m, pool, flush_steps=4, max_inflight=6)
     m.begin_step(1, run.now())
-    pool.stage(1, source={"weights": "v1"}, now=run.now())
+    run.stage(1, {"weights": "v1"})
     for k in range(2):
         run.add_local_engine(f"local{k:02d}", FakeInstance(vocab=997, max_slots=6))
     ps = prompts(20, seed=9)

@@ -1,82 +1,58 @@
-"""TransferPool: the reference's known answers (pkg/tests/test_transfer.py,
-restated) for the modelled mode, and the measured mode driven by real pulls."""
+"""Real weight bytes behind the UNMODIFIED reference `TransferPool`: staging
+starts the queued pulls, a pull runs for real, `finish` goes through the
+reference's own early-finish guard, preemption aborts."""
 import pytest
+from spotrl.transfer import TransferPool, build_agents
 
-from paper_2510_19225_b200.transfer import TransferAgent, TransferPool, build_agents
+from paper_2510_19225_b200.transfer import WeightPlane
 from tests.fakes import FakeInstance
 
 GB = 1e9
 
 
-def pool(n_agents=1, egress=25 * GB):
-    return TransferPool(build_agents(1, n_agents, egress))
-
-
-def test_round_robin_pairing():
-    p = pool(2)
-    assert [p.pair_agent(f"i{k}") for k in range(4)] == ["agent-0.0", "agent-0.1"] * 2
-    single = pool(1)
-    assert {single.pair_agent(f"i{k}") for k in range(3)} == {"agent-0.0"}
-    with pytest.raises(ValueError):
-        TransferPool([])
-
-
-def test_sole_pull_is_ingress_bound():
-    p = pool()
-    p.stage_complete(1, 0.0)
-    assert p.request_pull("i0", "agent-0.0", 1, 28 * GB, 6.25 * GB, 0.0)
-    (t, iid), = p.predictions()
-    assert iid == "i0" and t == pytest.approx(4.48)
-    job = p.finish("i0", t)
-    assert job.bytes_done == job.bytes_total
-
-
-def test_equal_split_and_reshare_on_finish():
-    p = pool(egress=10 * GB)
-    p.stage_complete(1, 0.0)
-    p.request_pull("a", "agent-0.0", 1, 10 * GB, 100 * GB, 0.0)
-    p.request_pull("b", "agent-0.0", 1, 20 * GB, 100 * GB, 0.0)
-    assert p.jobs["a"].rate == p.jobs["b"].rate == 5 * GB
-    t_a, _ = p.predictions()[0]
-    assert t_a == pytest.approx(2.0)
-    p.finish("a", t_a)
-    assert p.jobs["b"].rate == 10 * GB
-    (t_b, _), = p.predictions()
-    assert t_b == pytest.approx(3.0)
-
-
-def test_independent_agents():
-    p = pool(2, egress=10 * GB)
-    p.stage_complete(1, 0.0)
-    p.request_pull("a", "agent-0.0", 1, 10 * GB, 100 * GB, 0.0)
-    p.request_pull("b", "agent-0.1", 1, 10 * GB, 100 * GB, 0.0)
-    assert [round(t, 6) for t, _ in p.predictions()] == [1.0, 1.0]
-
-
-def test_queue_until_staged_abort_and_early_finish_guard():
-    p = pool()
-    assert not p.request_pull("a", "agent-0.0", 2, GB, GB, 0.0)
-    assert p.predictions() == []
-    assert p.stage_complete(2, 1.0) == ["a"]
-    with pytest.raises(RuntimeError, match="finished early"):
-        p.finish("a", 1.5)
-    p.abort("a", 1.6)
-    assert "a" not in p.jobs and p.predictions() == []
-    with pytest.raises(ValueError, match="backwards"):
-        p.stage_complete(3, 0.5)
-    assert p.request_pull("b", "agent-0.0", 2, GB, GB, 2.0)
-    with pytest.raises(ValueError, match="already pulling"):
-        p.request_pull("b", "agent-0.0", 2, GB, GB, 2.0)
-
-
-def test_measured_pull_path():
-    p = TransferPool([TransferAgent("agent-0.0", "node-0", 900 * GB)])
+def test_stage_run_finish_through_reference_pool():
+    pool = TransferPool(build_agents(1, 2, 6.25 * GB))
+    plane = WeightPlane()
     inst = FakeInstance()
-    started = p.stage(4, source={"w": 0}, now=0.0)
-    assert started == []
-    assert p.request_pull("i0", "agent-0.0", 4, 0.0, float("inf"), 0.0)
-    job = p.run_pull("i0", inst)
-    assert inst.version == 4 and job.measured_seconds > 0 and job.measured_gbps > 0
-    (t, iid), = p.predictions()
-    assert iid == "i0" and t == pytest.approx(job.measured_seconds)
-    assert p.finish("i0", 0.0).bytes_done == job.bytes_total
+    agent = pool.pair_agent("i0")
+    assert not pool.request_pull("i0", agent, 4, 28 * GB, float("inf"), 0.0)   # not staged yet
+    with pytest.raises(KeyError):
+        plane.run(pool, "i0", inst)
+    assert plane.stage(pool, 4, {"w": 0}, 1.0) == ["i0"]
+    with pytest.raises(RuntimeError, match="no measured pull"):
+        plane.finish(pool, "i0", 1.0)
+    meas = plane.run(pool, "i0", inst)
+    assert inst.version == 4 and meas.bytes == 1 << 20 and meas.gbps > 0
+    # the modelled 28 GB at 6.25 GB/s would need 4.48 s: the real bytes landed
+    job = plane.finish(pool, "i0", 1.001)
+    assert job.bytes_done == job.bytes_total == float(1 << 20)
+    assert "i0" not in pool.jobs and not pool.agents[agent].active_pulls
+
+
+def test_reference_guards_still_apply():
+    pool = TransferPool(build_agents(1, 1, 900 * GB))
+    plane = WeightPlane()
+    plane.stage(pool, 2, object(), 0.0)
+    assert pool.request_pull("i0", "agent-0.0", 2, GB, float("inf"), 0.0)
+    with pytest.raises(ValueError, match="already pulling"):
+        pool.request_pull("i0", "agent-0.0", 2, GB, float("inf"), 0.0)
+    with pytest.raises(RuntimeError, match="finished early"):
+        pool.finish("i0", 0.0)                  # nothing measured: the modelled guard holds
+    pool.abort("i0", 0.5)
+    assert "i0" not in pool.jobs
+    assert not pool.request_pull("i1", "agent-0.0", 3, GB, float("inf"), 1.0)
+    with pytest.raises(KeyError):
+        plane.run(pool, "i1", FakeInstance())   # queued, not started
+
+
+def test_shadow_pull_collect():
+    pool = TransferPool(build_agents(1, 1, 900 * GB))
+    plane = WeightPlane()
+    plane.stage(pool, 5, object(), 0.0)
+    inst = FakeInstance()
+    assert pool.request_pull("i0", "agent-0.0", 5, GB, float("inf"), 0.0)
+    assert plane.run(pool, "i0", inst, shadow=True) is None
+    meas = plane.collect(pool, "i0", inst)
+    assert meas.shadow and meas.version == 5
+    plane.finish(pool, "i0", 0.1)
+    assert inst.swap_weights() == 5
