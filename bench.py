@@ -17,10 +17,16 @@ Printed JSON line (rank 0):
   roofline     the dominant kernel (split-K paged decode attention), re-launched
                mid-rollout on the instance stream and timed with CUDA events;
                achieved = algorithmic K+V(+q,out) bytes per launch / avg duration
-  cpu_baseline the fp32 CPU oracle (oracle/qwen2_fp32.py) on a bounded sample
-               of the same workload, rank 0 at N=1 only
-`--impl reference` times only that CPU implementation (the reference has no
-decoder of its own -- SURVEY.md §0 -- so its CPU path is the oracle port).
+  cpu_baseline BASELINE.md §4, rank 0 at N=1 only, on the box's host cores:
+               the fp32 CPU oracle (oracle/qwen2_fp32.py, batched greedy
+               decode, all threads) on config 2 REDUCED to 16 prompts x 64
+               tokens (`value`) and on config 1 in full; the CPU model; and
+               the reference's own host code on the path (unmodified
+               spotrl RolloutManager.on_tokens / migrate_out + route_to,
+               TransferPool's modelled pull time), 1 core
+`--impl reference` times only the CPU decoder (the reference has no decoder
+of its own -- SURVEY.md §0 -- so its CPU path is the oracle port), each step
+a batched rollout of 4 prompts x 32 tokens.
 """
 from __future__ import annotations
 
@@ -40,8 +46,9 @@ N_PROMPTS = 512
 NEW_TOKENS = 1024
 P_LO, P_HI = 128, 384
 MAX_SEQ = 1408            # P_HI + NEW_TOKENS
-CPU_SAMPLE = (4, 32)      # prompts x new tokens for the CPU oracle sample
-NCU_ATTN_FILE = "profiles/r1_attn_ncu.json"
+CPU_SAMPLE = (16, 64)     # config 2 reduced: prompts x new tokens
+REF_ARM_SAMPLE = (4, 32)  # --impl reference: one step = a batched rollout of this sample
+NCU_ATTN_FILE = "profiles/r2_attn_mid_ncu.json"   # ncu --set full of the profiled launch
 HBM_KERNELS = ("attention", "resid_norm")   # bytes-bound (others: FLOPs)   # ncu --set full capture of K1 (traffic)
 
 
@@ -56,6 +63,10 @@ def parse():
     ap.add_argument("--flush-steps", type=int, default=64, help="decode steps per rlb_step call")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--prefill-rows", type=int, default=16384, help="token rows per prefill chunk")
+    ap.add_argument("--split-o", type=int, default=0, help="O split-K (0 = measured default)")
+    ap.add_argument("--split-down", type=int, default=0, help="down split-K (0 = measured default)")
+    ap.add_argument("--profile-at", type=float, default=0.5,
+                    help="fraction of the rollout's tokens after which the kernels are profiled")
     ap.add_argument("--strong", action="store_true",
                     help="strong scaling: --prompts in total, split over the ranks (default: weak, "
                          "--prompts per rank)")
@@ -114,28 +125,105 @@ class ClockSampler:
                 "sm_max_mhz": int(rows[0][1]), "reasons": reasons, "samples": len(busy)}
 
 
-def cpu_oracle_sample(shape, weights_cpu, seed: int, threads: int) -> dict:
-    """Greedy rollout of a bounded sample of the workload on the CPU oracle."""
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+    return platform.processor() or platform.machine()
+
+
+def cpu_oracle_rollout(shape, weights_cpu, n: int, new: int, lo: int, hi: int, seed: int,
+                       threads: int) -> tuple[int, float]:
+    """Batched greedy rollout of n prompts x new tokens on the fp32 CPU oracle:
+    (generated tokens, seconds)."""
     import torch
     from oracle.qwen2_fp32 import Qwen2Fp32
     from paper_2510_19225_b200.synth import synth_prompts
     torch.set_num_threads(threads)
     oracle = Qwen2Fp32(shape, weights_cpu)
-    n, new = CPU_SAMPLE
-    prompts = synth_prompts(n, shape.vocab, P_LO, P_HI, seed=seed)
+    prompts = synth_prompts(n, shape.vocab, lo, hi, seed=seed)
     t0 = time.perf_counter()
-    toks = 0
-    for p in prompts:
-        toks += len(oracle.generate(p, new))
-    dt = time.perf_counter() - t0
-    return {"value": toks / dt, "unit": "tokens/s", "cores": threads, "kind": "port",
-            "sample": f"{n} prompts (len U[{P_LO},{P_HI}]) x {new} greedy tokens, fp32 torch CPU, "
-                      f"batch 1, {dt:.1f}s"}
+    gens = oracle.generate_batch(prompts, new)
+    return sum(len(g) for g in gens), time.perf_counter() - t0
+
+
+def reference_host_path() -> dict:
+    """The reference's own code on the path, unmodified (`spotrl`), 1 core
+    (BASELINE.md §4 item 2): token collection per token and in bulk flushes,
+    migrate_out + route_to per request, and the TransferPool's modelled pull
+    time for the config-2 and config-4 weight bytes at its default TCP rate."""
+    import paper_2510_19225_b200  # noqa: F401  (the installed reference on sys.path)
+    from spotrl.events import EventLog
+    from spotrl.manager import RolloutManager
+    from spotrl.transfer import TransferPool, build_agents
+    B, STEPS, K = 512, 16, 64
+
+    def manager():
+        m = RolloutManager(theta=B, m_b=16, log=EventLog())
+        m.n_prem_cap = 2
+        for iid in ("i0", "i1"):
+            m.register_instance(iid, 1, 0.0)
+            m.mark_active(iid, 0, 0.0)
+        m.begin_step(0, 0.0)
+        for r in range(B):
+            m.create_request(f"r{r}", 16, STEPS * K + 1, "g", 0.0)
+        m.dispatch(0.0)
+        for iid in ("i0", "i1"):
+            for rid in list(m.pending_queues[iid]):
+                m.admit(rid, iid, 0.0)
+        return m, dict(m.owner)
+
+    out = {"cores": 1, "impl": "spotrl (unmodified reference)"}
+    m, owner = manager()
+    t0 = time.perf_counter()
+    for _ in range(K):
+        for rid, iid in owner.items():
+            m.on_tokens(rid, iid, 1, 0.0)
+    out["on_tokens_count1_tok_per_s"] = B * K / (time.perf_counter() - t0)
+    m, owner = manager()
+    t0 = time.perf_counter()
+    for _ in range(STEPS):
+        for rid, iid in owner.items():
+            m.on_tokens(rid, iid, K, 0.0)
+    out["on_tokens_bulk_k64_tok_per_s"] = B * STEPS * K / (time.perf_counter() - t0)
+    t0 = time.perf_counter()
+    for rid in list(owner)[:B // 2]:
+        m.migrate_out(rid, 0.0, reason="preempt")
+        m.route_to(rid, "i1" if owner[rid] == "i0" else "i0", 0.0)
+    out["migrate_out_route_to_us_per_request"] = 1e6 * (time.perf_counter() - t0) / (B // 2)
+    for label, nbytes in (("config2_1.5b", 3_087_428_608), ("config4_7b", 15_231_233_024)):
+        pool = TransferPool(build_agents(1, 1, 25e9))
+        pool.stage_complete(1, 0.0)
+        pool.request_pull("i0", "agent-0.0", 1, float(nbytes), 6.25e9, 0.0)
+        out[f"transferpool_modelled_pull_s_{label}"] = pool.predictions()[0][0]
+    return out
+
+
+def cpu_baseline(shape, threads: int) -> dict:
+    """config 2 reduced (value), config 1 in full, host path."""
+    from paper_2510_19225_b200.shapes import TINY
+    from paper_2510_19225_b200.synth import synth_hf_weights
+    n, new = CPU_SAMPLE
+    w = synth_hf_weights(shape, seed=0, device="cpu")
+    toks, sec = cpu_oracle_rollout(shape, w, n, new, P_LO, P_HI, seed=77, threads=threads)
+    del w
+    wt = synth_hf_weights(TINY, seed=0, device="cpu")
+    t1, s1 = cpu_oracle_rollout(TINY, wt, 64, 128, 16, 64, seed=1, threads=threads)
+    return {"value": toks / sec, "unit": "tokens/s", "cores": threads, "kind": "port",
+            "cpu_model": cpu_model(),
+            "sample": f"REDUCED config 2: {n} prompts (len U[{P_LO},{P_HI}]) x {new} greedy "
+                      f"tokens, batched fp32 torch CPU oracle, {sec:.1f}s",
+            "config1_full": {"value": t1 / s1, "unit": "tokens/s", "seconds": round(s1, 2),
+                             "sample": "64 prompts (len U[16,64]) x 128 tokens, tiny decoder"},
+            "reference_host_path": reference_host_path()}
 
 
 def run_reference(args):
     """--impl reference: the CPU implementation of the path, timed on host cores."""
-    import torch
     from paper_2510_19225_b200.shapes import QWEN25_1_5B
     from paper_2510_19225_b200.synth import synth_hf_weights
     ws, rank, _ = dist_env()
@@ -143,17 +231,21 @@ def run_reference(args):
         return
     threads = os.cpu_count() or 1
     w = synth_hf_weights(QWEN25_1_5B, seed=0, device="cpu")
-    vals = []
+    n, new = REF_ARM_SAMPLE
+    toks = secs = 0.0
     for i in range(args.warmup + args.steps):
-        r = cpu_oracle_sample(QWEN25_1_5B, w, seed=100 + i, threads=threads)
+        t, sec = cpu_oracle_rollout(QWEN25_1_5B, w, n, new, P_LO, P_HI, seed=100 + i,
+                                    threads=threads)
         if i >= args.warmup:
-            vals.append(r)
-    value = statistics.mean(v["value"] for v in vals)
-    sample = vals[0]["sample"]
+            toks += t
+            secs += sec
+    value = toks / secs
+    sample = (f"{n} prompts (len U[{P_LO},{P_HI}]) x {new} greedy tokens per step, batched fp32 "
+              f"torch CPU oracle, {threads} threads, {cpu_model()}")
     line = {
         "metric": "rollout tokens/s", "value": value, "unit": "tokens/s", "impl": "reference",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": 1000.0 * CPU_SAMPLE[0] * CPU_SAMPLE[1] / value,
+        "ms_per_step": 1000.0 * secs / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic",
         "config": {"workload": "config2: qwen2.5-1.5b-shape random-init rollout, 512 prompts x 1024 "
@@ -187,10 +279,13 @@ def main():
         n_prompts = args.prompts // ws + (1 if rank < args.prompts % ws else 0)
     w = synth_hf_weights(shape, seed=0, device=f"cuda:{local}")
     inst = RolloutInstance(shape, local, max_slots=n_prompts, max_seq_len=MAX_SEQ,
-                           max_prefill_rows=args.prefill_rows, graph_steps=16)
+                           max_prefill_rows=args.prefill_rows, graph_steps=16,
+                           split_o=args.split_o, split_down=args.split_down)
     pull = inst.load_weights(w, version=1)
     prompts = synth_prompts(n_prompts, shape.vocab, P_LO, P_HI, seed=1000 + rank)
     h2d_prompt_bytes = 4 * sum(len(p) for p in prompts)
+
+    ctx_at_profile: list[float] = []
 
     def rollout(tag: str, profile: bool = False):
         for i, p in enumerate(prompts):
@@ -200,10 +295,16 @@ def main():
         while True:
             out = inst.step(args.flush_steps)
             got += sum(len(t) for _, t, _ in out)
-            if profile and not prof and got >= n_prompts * (new // 2):
+            if profile and not prof and got >= n_prompts * int(new * args.profile_at):
+                # the profiled re-launches are the only region an
+                # `ncu --profile-from-start off` capture sees
+                torch.cuda.synchronize()
+                torch.cuda.profiler.start()
                 for k in ("attention", "gate_up", "down", "qkv", "o_proj", "lm_head",
                           "resid_norm"):
                     prof[k] = inst.profile_kernel(k, iters=20)
+                torch.cuda.profiler.stop()
+                ctx_at_profile.append(h2d_prompt_bytes / 4 / n_prompts + got / n_prompts)
             st = inst.status()
             if st["m_pending"] == 0 and st["m_exec"] == 0:
                 break
@@ -247,13 +348,22 @@ def main():
         except OSError:
             pass
         hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
-        ncu_ratio = None
+        nc = None
         try:
             nc = _j.load(open(os.path.join(ROOT, NCU_ATTN_FILE)))
-            ncu_ratio = nc["dram_bytes"] / nc["algorithmic_bytes"]
-        except (OSError, KeyError, ValueError):
+        except (OSError, ValueError):
             pass
         att_ms, att_bytes = prof["attention"]
+        traffic = traffic_src = None
+        if nc:
+            # the committed ncu --set full capture of this very launch (same
+            # config, same profile point -> same context and algorithmic bytes)
+            same = abs(nc["algorithmic_bytes"] - att_bytes) <= 1e-6 * att_bytes
+            ratio = nc["dram_bytes"] / nc["algorithmic_bytes"]
+            traffic = round(nc["dram_bytes"] if same else att_bytes * ratio)
+            traffic_src = (f"{NCU_ATTN_FILE}: dram__bytes_read+write of the profiled launch "
+                           f"(context {nc.get('context')}, {nc['duration_us']} us under ncu)"
+                           + ("" if same else f", scaled by its ratio {ratio:.3f} to this launch"))
         achieved = att_bytes / (att_ms / 1e3) / 1e9
         kern = {k: {"avg_ms": round(v[0], 4), "work": v[1],
                     ("GB/s" if k in HBM_KERNELS else "TFLOP/s"):
@@ -277,11 +387,9 @@ def main():
             "roofline": {"bound": "hbm", "kernel": "attn_mma_kernel<128> (K1, paged GQA decode attention)",
                          "achieved": round(achieved, 1), "peak": hbm_peak, "unit": "GB/s",
                          "frac": round(achieved / hbm_peak, 4),
-                         "traffic": (round(att_bytes * ncu_ratio) if ncu_ratio else None),
-                         "traffic_source": (f"ncu --set full DRAM read+write / algorithmic bytes = "
-                                            f"{ncu_ratio:.3f} on the captured launch ({NCU_ATTN_FILE}), "
-                                            "scaled to this launch" if ncu_ratio else None),
+                         "traffic": traffic, "traffic_source": traffic_src,
                          "bytes_per_launch": att_bytes, "avg_launch_ms": att_ms,
+                         "context": round(ctx_at_profile[0], 1) if ctx_at_profile else None,
                          "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback"},
             "kernels_mid_rollout": kern,
             "phases_ms_rank0": {"prefill": round(st["prefill_ms"], 1), "decode": round(st["decode_ms"], 1),
@@ -291,8 +399,7 @@ def main():
         }
         if ws == 1 and not args.no_cpu_baseline:
             del w
-            wc = synth_hf_weights(shape, seed=0, device="cpu")
-            line["cpu_baseline"] = cpu_oracle_sample(shape, wc, seed=77, threads=os.cpu_count() or 1)
+            line["cpu_baseline"] = cpu_baseline(shape, threads=os.cpu_count() or 1)
         print(json.dumps(line), flush=True)
     inst.close()
     if ws > 1:

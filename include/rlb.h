@@ -58,7 +58,14 @@ typedef struct {
   int32_t num_pages;          /* KV pages of 64 tokens; 0 = max_slots*ceil(max_seq_len/64) */
   int32_t max_prefill_rows;   /* token rows per prefill chunk */
   int32_t graph_steps;        /* decode steps per captured CUDA graph; 0 = eager */
-  int32_t reserved[3];
+  /* Numerics plan: the split-K factors of the O and down projections fix the
+   * order in which a row's dot products are summed, so they are part of the
+   * bits an instance produces.  0 = the measured default for the shape.
+   * Instances that migrate requests between them must share the plan
+   * (rlb_numerics_plan). */
+  int32_t split_o;
+  int32_t split_down;
+  int32_t reserved;
 } rlb_engine_cfg;
 
 /* Output of rlb_step: per request that produced tokens this call, its key,
@@ -89,6 +96,16 @@ int rlb_instance_create(int device, const rlb_model_cfg* model, const rlb_engine
 int rlb_instance_destroy(rlb_instance* h);
 const char* rlb_last_error(void);
 
+/* Everything that fixes the bits a row's arithmetic produces, as int32s:
+ * [0] plan format version, [1] QKV split-K, [2] O split-K, [3] down split-K,
+ * [4] attention positions per CTA window, [5] positions per KV page,
+ * [6] greedy tie rule (0 = lowest index).  Two instances whose plans are
+ * equal produce identical ids for the same request whatever their batch,
+ * slot count or tile shapes (those never change a row's bits); a resume
+ * across unequal plans is not bit-exact.  Returns the number of ints (7),
+ * writes at most cap. */
+int32_t rlb_numerics_plan(const rlb_instance* h, int32_t* out, int32_t cap);
+
 /* ---- weights (K7) ------------------------------------------------------ */
 /* Engine-arena size in bytes for a model shape. */
 int64_t rlb_arena_bytes(const rlb_model_cfg* model);
@@ -100,13 +117,19 @@ int64_t rlb_relayout_table(const rlb_model_cfg* model, int64_t* out, int64_t cap
 /* Pull a full HF-layout weight set into the instance's engine arena with the
  * re-layout fused into the copy.  hf_ptrs are device pointers (local, or a
  * peer's memory mapped with rlb_ipc_open -- the copy then runs over NVLink).
+ * ready_event (a cudaEvent_t, any device, or NULL): the copy waits on the
+ * device until the producer of the source tensors recorded it (e.g. after the
+ * trainer's optimizer step), so it never reads weights still being written.
+ * Refused (RLB_ERR_STATE) while requests are on the instance: in-flight
+ * sequences must not mix weight versions (use the shadow arena + swap).
  * Synchronous; the new version serves from the next rlb_step. */
 int rlb_load_weights(rlb_instance* h, const void* const* hf_ptrs, int32_t n_tensors,
-                     uint64_t version, rlb_pull_stats* stats);
+                     uint64_t version, void* ready_event, rlb_pull_stats* stats);
 /* Engine arena device pointer + bytes (for bytewise checks / chained hops). */
 int rlb_weights_arena(rlb_instance* h, void** arena, int64_t* bytes);
 /* Declare the arena filled with `version` by an external copy (the fan-out
- * writes it with rlb_relayout_copy_range / rlb_copy_bytes). */
+ * writes it with rlb_relayout_copy_range / rlb_copy_bytes).  Refused while
+ * requests are on the instance, like rlb_load_weights. */
 int rlb_mark_weights(rlb_instance* h, uint64_t version);
 
 /* ---- double-buffered weights ------------------------
@@ -118,7 +141,8 @@ int rlb_mark_weights(rlb_instance* h, uint64_t version);
  *   rlb_shadow_arena   shadow arena pointer + bytes (allocated on first use;
  *                      the target of external fan-out / IPC / NCCL pulls)
  *   rlb_load_shadow    fused re-layout copy of HF tensors into the shadow,
- *                      enqueued on the copy stream; returns immediately
+ *                      enqueued on the copy stream after `ready_event` (the
+ *                      producer's, or NULL); returns immediately
  *   rlb_mark_shadow    the shadow was filled externally by work enqueued on
  *                      `stream` (NULL = legacy default stream) with `version`
  *   rlb_shadow_status  state 0 empty / 1 copy in flight / 2 filled; seconds =
@@ -129,7 +153,7 @@ int rlb_mark_weights(rlb_instance* h, uint64_t version);
  *                      old set becomes the empty shadow; out = active version */
 int rlb_shadow_arena(rlb_instance* h, void** arena, int64_t* bytes);
 int rlb_load_shadow(rlb_instance* h, const void* const* hf_ptrs, int32_t n_tensors,
-                    uint64_t version);
+                    uint64_t version, void* ready_event);
 int rlb_mark_shadow(rlb_instance* h, uint64_t version, void* stream);
 int rlb_shadow_status(rlb_instance* h, uint64_t* version, int32_t* state, double* seconds);
 int rlb_swap_weights(rlb_instance* h, uint64_t* version);

@@ -44,7 +44,8 @@ class ModelCfg(ctypes.Structure):
 class EngineCfg(ctypes.Structure):
     _fields_ = [("max_slots", ctypes.c_int32), ("max_seq_len", ctypes.c_int32),
                 ("num_pages", ctypes.c_int32), ("max_prefill_rows", ctypes.c_int32),
-                ("graph_steps", ctypes.c_int32), ("reserved", ctypes.c_int32 * 3)]
+                ("graph_steps", ctypes.c_int32), ("split_o", ctypes.c_int32),
+                ("split_down", ctypes.c_int32), ("reserved", ctypes.c_int32)]
 
 
 class TokenBatch(ctypes.Structure):
@@ -78,11 +79,12 @@ _SIGS = {
     "rlb_instance_create": (ctypes.c_int, [ctypes.c_int, ctypes.POINTER(ModelCfg),
                                            ctypes.POINTER(EngineCfg), ctypes.POINTER(_P)]),
     "rlb_instance_destroy": (ctypes.c_int, [_P]),
+    "rlb_numerics_plan": (ctypes.c_int32, [_P, _P, ctypes.c_int32]),
     "rlb_last_error": (ctypes.c_char_p, []),
     "rlb_arena_bytes": (ctypes.c_int64, [ctypes.POINTER(ModelCfg)]),
     "rlb_hf_tensor_count": (ctypes.c_int32, [ctypes.POINTER(ModelCfg)]),
     "rlb_relayout_table": (ctypes.c_int64, [ctypes.POINTER(ModelCfg), _P, ctypes.c_int64]),
-    "rlb_load_weights": (ctypes.c_int, [_P, _P, ctypes.c_int32, ctypes.c_uint64,
+    "rlb_load_weights": (ctypes.c_int, [_P, _P, ctypes.c_int32, ctypes.c_uint64, _P,
                                         ctypes.POINTER(PullStats)]),
     "rlb_weights_arena": (ctypes.c_int, [_P, ctypes.POINTER(_P), ctypes.POINTER(ctypes.c_int64)]),
     "rlb_mark_weights": (ctypes.c_int, [_P, ctypes.c_uint64]),
@@ -113,7 +115,7 @@ _SIGS = {
     "rlb_score": (ctypes.c_int, [_P, _P, ctypes.c_int32, _P]),
     "rlb_shadow_arena": (ctypes.c_int, [_P, ctypes.POINTER(ctypes.c_void_p),
                                         ctypes.POINTER(ctypes.c_int64)]),
-    "rlb_load_shadow": (ctypes.c_int, [_P, _P, ctypes.c_int32, ctypes.c_uint64]),
+    "rlb_load_shadow": (ctypes.c_int, [_P, _P, ctypes.c_int32, ctypes.c_uint64, _P]),
     "rlb_mark_shadow": (ctypes.c_int, [_P, ctypes.c_uint64, _P]),
     "rlb_shadow_status": (ctypes.c_int, [_P, ctypes.POINTER(ctypes.c_uint64),
                                          ctypes.POINTER(ctypes.c_int32),

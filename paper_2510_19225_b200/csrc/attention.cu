@@ -651,6 +651,7 @@ __global__ void attn_combine_kernel(AttnArgs a) {
 }
 
 int attention_windows(int max_seq) { return (max_seq + SUPER - 1) / SUPER; }
+int attention_window_positions() { return SUPER; }
 
 template <int D>
 static int launch_attn(const AttnArgs& a, cudaStream_t st, bool pairs) {

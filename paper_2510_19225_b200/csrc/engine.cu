@@ -402,6 +402,29 @@ struct rlb_instance {
   int flush(rlb_token_batch* out);
   int upload_slots();
   void release(Req* r);
+  // row pairs (2p, 2p+1) of a prefill chunk (positions pos[0..n)): those
+  // whose rows all see <= 2 pages of context first (2-warp attention CTAs),
+  // then the rest in row order; the lists belong to the next forward only
+  int build_pairs(const int* pos, size_t n) {
+    pairs_short = pairs_long = 0;
+    if (!(attn_pairs && attn_split)) return RLB_OK;
+    const int np = static_cast<int>((n + 1) / 2);
+    h_pairs.resize(np);
+    int lo = 0, hi = np;
+    for (int z = 0; z < np; ++z) {
+      const size_t a0 = 2 * static_cast<size_t>(z);
+      const bool short_pair = pos[a0] < 2 * PAGE && (a0 + 1 >= n || pos[a0 + 1] < 2 * PAGE);
+      if (short_pair) h_pairs[lo++] = z;
+      else h_pairs[--hi] = z;
+    }
+    std::reverse(h_pairs.begin() + hi, h_pairs.end());   // long pairs in row order
+    pairs_short = lo;
+    pairs_long = np - lo;
+    RLB_CUDA(cudaMemcpyAsync(d_pairs, h_pairs.data(), np * sizeof(int), cudaMemcpyHostToDevice, st));
+    stats.h2d_bytes += static_cast<int64_t>(np) * 4;
+    if (pairs_short && pairs_long) stats.kernel_launches += m.layers;   // two attention launches
+    return RLB_OK;
+  }
 };
 
 rlb_instance::~rlb_instance() {
@@ -473,17 +496,15 @@ int rlb_instance::init() {
     sp_o = 4;
     sp_down = 4;
   }
-  if (const char* ov = std::getenv("RLB_SPLITS")) {   // "qkv,o,down" (tuning; process-wide)
-    int a = 0, b = 0, c = 0;
-    if (std::sscanf(ov, "%d,%d,%d", &a, &b, &c) == 3) {
-      const int kq = H / 64, ko = NQ * D / 64, kd = F / 64;
-      RLB_CHECK(a >= 1 && a <= 8 && kq >= 4 * a && b >= 1 && b <= 8 && ko >= 4 * b && c >= 1 &&
-                    c <= 8 && kd >= 4 * c,
-                RLB_ERR_ARG, "RLB_SPLITS: 1..8 splits of >= 4 K blocks");
-      sp_qkv = a;
-      sp_o = b;
-      sp_down = c;
-    }
+  // the numerics plan of the instance config (not process environment):
+  // split factors set the reduction order of a row's dot products
+  {
+    const int ko = NQ * D / 64, kd = F / 64;
+    RLB_CHECK(e.split_o >= 0 && e.split_o <= 8 && (e.split_o == 0 || ko >= 4 * e.split_o) &&
+                  e.split_down >= 0 && e.split_down <= 8 && (e.split_down == 0 || kd >= 4 * e.split_down),
+              RLB_ERR_ARG, "split_o / split_down: 0 (default) or 1..8 splits of >= 4 K blocks");
+    if (e.split_o) sp_o = e.split_o;
+    if (e.split_down) sp_down = e.split_down;
   }
 
   if (const char* ov = std::getenv("RLB_CLUSTER")) {   // "o,down[,down_large]" 0/1 (tuning)
@@ -887,26 +908,7 @@ int rlb_instance::admit_and_prefill(int* rows_run) {
       RLB_CUDA(cudaMemcpyAsync(d_logit_src, lsrc + beg, nl * sizeof(int), cudaMemcpyHostToDevice, st));
       RLB_CUDA(cudaMemcpyAsync(d_logit_slot, lslot + beg, nl * sizeof(int), cudaMemcpyHostToDevice, st));
     }
-    // row pairs (2p, 2p+1) of this chunk: those whose rows all see <= 2 pages
-    // of context first (2-warp attention CTAs), then the rest
-    pairs_short = pairs_long = 0;
-    if (attn_pairs && attn_split) {
-      const int np = static_cast<int>((n + 1) / 2);
-      h_pairs.resize(np);
-      int lo = 0, hi = np;
-      for (int z = 0; z < np; ++z) {
-        const size_t a0 = beg + 2 * static_cast<size_t>(z);
-        const bool short_pair = pos[a0] < 2 * PAGE && (a0 + 1 >= beg + n || pos[a0 + 1] < 2 * PAGE);
-        if (short_pair) h_pairs[lo++] = z;
-        else h_pairs[--hi] = z;
-      }
-      std::reverse(h_pairs.begin() + hi, h_pairs.end());   // long pairs in row order
-      pairs_short = lo;
-      pairs_long = np - lo;
-      RLB_CUDA(cudaMemcpyAsync(d_pairs, h_pairs.data(), np * sizeof(int), cudaMemcpyHostToDevice, st));
-      stats.h2d_bytes += static_cast<int64_t>(np) * 4;
-      if (pairs_short && pairs_long) stats.kernel_launches += m.layers;   // two attention launches
-    }
+    if ((rc = build_pairs(pos + beg, n))) return rc;
     if ((rc = seed_tokens_launch(d_row_tok, d_row_pos, d_row_slot, static_cast<int>(n), d_seq_tokens,
                                  max_seq, st)))
       return rc;
@@ -1018,6 +1020,23 @@ int rlb_instance::flush(rlb_token_batch* out) {
     if (slot_req[s]) h_seq_len[s] = static_cast<int32_t>(slot_req[s]->tokens.size());
   int n = 0;
   int64_t nt = 0;
+  if (out) {
+    // capacity first: on failure no request state has changed and the ids
+    // stay in the host mirror for a retry with a larger batch
+    int need_n = 0;
+    int64_t need_t = 0;
+    for (int s = 0; s < max_slots; ++s) {
+      const Req* r = slot_req[s];
+      if (!r) continue;
+      const int newc = r->generated() - r->reported;
+      if (newc <= 0 && !r->complete()) continue;
+      ++need_n;
+      need_t += newc;
+    }
+    RLB_CHECK(need_n <= out->cap_entries && need_t <= out->cap_tokens, RLB_ERR_CAPACITY,
+              "token batch capacity exceeded (" + std::to_string(need_n) + " entries, " +
+                  std::to_string(need_t) + " tokens)");
+  }
   std::vector<Req*> finished;
   for (int s = 0; s < max_slots; ++s) {
     Req* r = slot_req[s];
@@ -1026,8 +1045,6 @@ int rlb_instance::flush(rlb_token_batch* out) {
     const bool done = r->complete();
     if (newc <= 0 && !done) continue;
     if (out) {
-      RLB_CHECK(n < out->cap_entries && nt + newc <= out->cap_tokens, RLB_ERR_CAPACITY,
-                "token batch capacity exceeded");
       out->keys[n] = r->key;
       out->counts[n] = newc;
       out->done[n] = done ? 1 : 0;
@@ -1080,12 +1097,23 @@ int rlb_instance_destroy(rlb_instance* h) {
   return RLB_OK;
 }
 
+int32_t rlb_numerics_plan(const rlb_instance* h, int32_t* out, int32_t cap) {
+  if (!h) return 0;
+  const int32_t plan[7] = {1, h->sp_qkv, h->sp_o, h->sp_down, attention_window_positions(), PAGE, 0};
+  for (int i = 0; i < 7 && i < cap && out; ++i) out[i] = plan[i];
+  return 7;
+}
+
 int rlb_load_weights(rlb_instance* h, const void* const* hf_ptrs, int32_t n_tensors,
-                     uint64_t version, rlb_pull_stats* stats) {
+                     uint64_t version, void* ready_event, rlb_pull_stats* stats) {
   RLB_CHECK(h && hf_ptrs, RLB_ERR_ARG, "null argument");
   RLB_CHECK(!h->has_weights || version >= h->version, RLB_ERR_ARG,
             "weight version " + std::to_string(version) + " < " + std::to_string(h->version));
+  RLB_CHECK(h->reqs.empty(), RLB_ERR_STATE,
+            "active weights replaced only at a step boundary (" + std::to_string(h->reqs.size()) +
+                " requests on the instance; pull into the shadow arena and swap)");
   RLB_CUDA(cudaSetDevice(h->device));
+  if (ready_event) RLB_CUDA(cudaStreamWaitEvent(h->st, static_cast<cudaEvent_t>(ready_event), 0));
   RLB_CUDA(cudaEventRecord(h->ev0, h->st));
   int rc = relayout_copy(h->m, hf_ptrs, n_tensors, h->arena, h->st);
   if (rc) return rc;
@@ -1116,6 +1144,9 @@ int rlb_weights_arena(rlb_instance* h, void** arena, int64_t* bytes) {
 
 int rlb_mark_weights(rlb_instance* h, uint64_t version) {
   RLB_CHECK(h, RLB_ERR_ARG, "null handle");
+  RLB_CHECK(h->reqs.empty(), RLB_ERR_STATE,
+            "active weights replaced only at a step boundary (" + std::to_string(h->reqs.size()) +
+                " requests on the instance)");
   RLB_CHECK(!h->has_weights || version >= h->version, RLB_ERR_ARG,
             "weight version " + std::to_string(version) + " < " + std::to_string(h->version));
   h->version = version;
@@ -1136,7 +1167,7 @@ int rlb_shadow_arena(rlb_instance* h, void** arena, int64_t* bytes) {
 }
 
 int rlb_load_shadow(rlb_instance* h, const void* const* hf_ptrs, int32_t n_tensors,
-                    uint64_t version) {
+                    uint64_t version, void* ready_event) {
   RLB_CHECK(h && hf_ptrs, RLB_ERR_ARG, "null argument");
   RLB_CHECK(!h->has_weights || version >= h->version, RLB_ERR_ARG,
             "weight version " + std::to_string(version) + " < " + std::to_string(h->version));
@@ -1147,6 +1178,8 @@ int rlb_load_shadow(rlb_instance* h, const void* const* hf_ptrs, int32_t n_tenso
   // it as the active set are ordered before the overwrite
   RLB_CUDA(cudaEventRecord(h->ev_shadow, h->st));
   RLB_CUDA(cudaStreamWaitEvent(h->st_copy, h->ev_shadow, 0));
+  if (ready_event)      // the producer finished writing the source tensors
+    RLB_CUDA(cudaStreamWaitEvent(h->st_copy, static_cast<cudaEvent_t>(ready_event), 0));
   RLB_CUDA(cudaEventRecord(h->ev_s0, h->st_copy));
   if ((rc = relayout_copy(h->m, hf_ptrs, n_tensors, h->shadow.arena, h->st_copy))) return rc;
   RLB_CUDA(cudaEventRecord(h->ev_s1, h->st_copy));
@@ -1515,13 +1548,16 @@ int rlb_score(rlb_instance* h, const int32_t* tokens, int32_t n, float* out_logi
     pos[i] = i;
     slot[i] = s;
   }
-  h->pairs_short = h->pairs_long = 0;   // every row pair on the 4-warp kernel
   for (int beg = 0; beg < n && rc == 0; beg += h->prefill_rows) {
     const int cnt = std::min(h->prefill_rows, n - beg);
     RLB_CUDA(cudaMemcpyAsync(h->d_row_tok, tok + beg, cnt * 4, cudaMemcpyHostToDevice, h->st));
     RLB_CUDA(cudaMemcpyAsync(h->d_row_pos, pos + beg, cnt * 4, cudaMemcpyHostToDevice, h->st));
     RLB_CUDA(cudaMemcpyAsync(h->d_row_slot, slot + beg, cnt * 4, cudaMemcpyHostToDevice, h->st));
-    if ((rc = h->forward_layers(cnt, true))) break;
+    // the same pair lists (2-warp short pairs + 4-warp long pairs) as prefill
+    if ((rc = h->build_pairs(pos + beg, cnt))) break;
+    rc = h->forward_layers(cnt, true);
+    h->pairs_short = h->pairs_long = 0;
+    if (rc) break;
     for (int lb = 0; lb < cnt; lb += h->max_slots) {
       const int ln = std::min(h->max_slots, cnt - lb);
       for (int i = 0; i < ln; ++i) lsrc[i] = lb + i;

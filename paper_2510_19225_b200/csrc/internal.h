@@ -68,6 +68,7 @@ struct AttnArgs {
 };
 int attention_launch(const AttnArgs& a, cudaStream_t st, bool row_pairs = false);
 int attention_windows(int max_seq);   // CTA windows per row (AttnArgs.max_splits)
+int attention_window_positions();     // positions per CTA window (numerics plan)
 
 int embed_launch(const bf16* embed, int H, const int* tok, int R, float* h, cudaStream_t st);
 int resid_norm_launch(float* h, const float* part, int S, int Mp, const int* src_rows, int R,

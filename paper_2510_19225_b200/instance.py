@@ -48,7 +48,10 @@ class PullResult:
 class RolloutInstance:
     def __init__(self, shape: ModelShape, device: int = 0, *, max_slots: int = 512,
                  max_seq_len: int = 1536, max_prefill_rows: int = 16384, graph_steps: int = 8,
-                 num_pages: int = 0):
+                 num_pages: int = 0, split_o: int = 0, split_down: int = 0):
+        """split_o / split_down: split-K factors of the O / down projections
+        (0 = the measured default).  They are part of the numerics plan:
+        instances exchanging requests must agree on it (`plan`)."""
         self.shape = shape
         self.device = device
         self.max_slots = max_slots
@@ -56,7 +59,8 @@ class RolloutInstance:
         if os.environ.get("RLB_GRAPH_STEPS"):
             graph_steps = int(os.environ["RLB_GRAPH_STEPS"])
         self._cfg = _lib.ModelCfg.from_shape(shape)
-        ecfg = _lib.EngineCfg(max_slots, max_seq_len, num_pages, max_prefill_rows, graph_steps)
+        ecfg = _lib.EngineCfg(max_slots, max_seq_len, num_pages, max_prefill_rows, graph_steps,
+                              split_o, split_down, 0)
         h = ctypes.c_void_p()
         check(_lib.lib().rlb_instance_create(device, ctypes.byref(self._cfg), ctypes.byref(ecfg),
                                              ctypes.byref(h)))
@@ -72,6 +76,7 @@ class RolloutInstance:
         self._tokens = np.zeros(self._tok_cap, np.int32)
         self.last_steps = 0
         self.last_prefill_rows = 0
+        self._events: list = []
 
     # -- lifecycle ---------------------------------------------------------
 
@@ -98,13 +103,34 @@ class RolloutInstance:
             return [int(p) for p in src.ptrs]
         return [int(p) for p in src]
 
+    def _ready_event(self, src):
+        """For a torch tensor dict: an event recorded on the producing stream
+        (torch's current stream of the tensors' device), so the copy kernels
+        wait on the device for whatever is still writing the weights (e.g. the
+        trainer's optimizer step).  Other sources order themselves."""
+        if not isinstance(src, dict):
+            return None
+        import torch
+        t = next(iter(src.values()))
+        if not t.is_cuda:
+            return None
+        ev = torch.cuda.Event()
+        ev.record(torch.cuda.current_stream(t.device))
+        self._events.append(ev)            # kept alive until the copy is enqueued / done
+        del self._events[:-2]
+        return ev
+
     def load_weights(self, hf_weights, version: int) -> PullResult:
         """Pull an HF-layout weight set (dict name -> CUDA tensor, or a list of
-        device pointers in `hf_manifest` order) with the fused re-layout."""
+        device pointers in `hf_manifest` order) with the fused re-layout.
+        Only at a step boundary (no requests on the instance)."""
         ptrs = self._source_ptrs(hf_weights)
         arr = (ctypes.c_void_p * len(ptrs))(*ptrs)
         stats = _lib.PullStats()
-        check(_lib.lib().rlb_load_weights(self._h, arr, len(ptrs), version, ctypes.byref(stats)))
+        ev = self._ready_event(hf_weights)
+        check(_lib.lib().rlb_load_weights(self._h, arr, len(ptrs), version,
+                                          ev.cuda_event if ev is not None else None,
+                                          ctypes.byref(stats)))
         return PullResult(version, stats.bytes, stats.seconds)
 
     pull_weights = load_weights
@@ -132,7 +158,9 @@ class RolloutInstance:
         copy stream); returns at once while the active weights keep serving."""
         ptrs = self._source_ptrs(hf_weights)
         arr = (ctypes.c_void_p * len(ptrs))(*ptrs)
-        check(_lib.lib().rlb_load_shadow(self._h, arr, len(ptrs), version))
+        ev = self._ready_event(hf_weights)
+        check(_lib.lib().rlb_load_shadow(self._h, arr, len(ptrs), version,
+                                         ev.cuda_event if ev is not None else None))
 
     @property
     def pull_bytes(self) -> int:
@@ -259,11 +287,24 @@ class RolloutInstance:
             out.append((seq[:npr[i]].tolist(), seq[npr[i]:].tolist()))
         return out
 
+    PLAN_FIELDS = ("format", "split_qkv", "split_o", "split_down", "attn_window", "page",
+                   "tie_rule")
+
+    @property
+    def plan(self) -> str:
+        """The numerics plan (`rlb_numerics_plan`): what fixes the bits of a
+        row's arithmetic.  A resume is bit-exact only between equal plans."""
+        buf = (ctypes.c_int32 * 8)()
+        n = _lib.lib().rlb_numerics_plan(self._h, buf, 8)
+        return ".".join(f"{k}{buf[i]}" for i, k in zip(range(n), ("v", "q", "o", "d", "w", "p", "t")))
+
     def status(self) -> dict:
-        """protocol `status` payload."""
+        """protocol `status` payload (+ the numerics plan, an extra field the
+        protocol permits, `protocol.py:23-24`)."""
         mp, me, wv = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_uint64()
         check(_lib.lib().rlb_status(self._h, ctypes.byref(mp), ctypes.byref(me), ctypes.byref(wv)))
-        return {"m_pending": mp.value, "m_exec": me.value, "weight_version": int(wv.value)}
+        return {"m_pending": mp.value, "m_exec": me.value, "weight_version": int(wv.value),
+                "plan": self.plan}
 
     def score(self, tokens) -> np.ndarray:
         """Teacher-forced fp32 logits [len(tokens), vocab] of one sequence."""

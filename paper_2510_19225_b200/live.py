@@ -100,6 +100,7 @@ class ManagerServer:
         self.iid_of: dict[int, str] = {}
         self.conn_of: dict[str, _Conn] = {}
         self._pull_t0: dict[str, float] = {}
+        self.plan: str | None = None          # numerics plan shared by every instance
         self._t0 = time.perf_counter()
         self._lsock = socket.create_server((host, port))
         self.address = self._lsock.getsockname()
@@ -156,6 +157,17 @@ class ManagerServer:
             conn.send(msg_pull_weights(self.version, endpoint))
         elif t == "status":
             iid = self.iid_of[cid]
+            plan = msg.get("plan")
+            if plan is not None:
+                if self.plan is None:
+                    self.plan = plan
+                elif plan != self.plan:
+                    # a resume across plans would not be bit-exact: refuse the
+                    # instance (its close event is handled like a preemption)
+                    m.log.emit(now, "plan_mismatch", instance_id=iid, plan=plan,
+                               expected=self.plan)
+                    self.conns[cid].close()
+                    return
             rec = m.records[iid]
             if rec.status is InstanceStatus.PULLING_WEIGHTS and \
                     msg["weight_version"] >= self.version:

@@ -198,7 +198,8 @@ def test_decode_profile_measured(tiny):
     """rlb_decode_profile: per batch size, device-timed decode steps that add
     up to the instance's decode accounting; it builds a ProfileTable the
     plateau rule accepts."""
-    from paper_2510_19225_b200.profile import estimate_plateau, measured_profile_table
+    from paper_2510_19225_b200.profile import measured_profile_table
+    from spotrl.balancer import estimate_plateau
     w, _ = tiny
     prompts = synth_prompts(32, TINY.vocab, 16, 48, seed=12)
     inst = _instance(TINY, w, max_slots=32, max_seq_len=256)
@@ -316,16 +317,72 @@ def test_o_two_k_blocks_per_stage_same_tokens(mid, monkeypatch, n_prompts):
     assert got == ref
 
 
-def test_prefill_short_pairs_same_tokens(mid, monkeypatch):
+def test_prefill_short_pairs_same_bits(mid, monkeypatch):
     """Prefill row pairs with <= 2 pages of context run on 2-warp attention
-    CTAs (the idle warp slots merged as empty partials): migration resume
-    and rollouts give the same tokens as the single 4-warp launch
-    (RLB_ATTN_SPLIT=0)."""
+    CTAs (the idle warp slots merged as empty partials).  Bit-level A/B:
+    teacher-forced logits (rlb_score builds the same pair lists as prefill)
+    are bitwise equal to the single 4-warp launch (RLB_ATTN_SPLIT=0); and a
+    migration resumed on the split path continues bit-exactly."""
     shape, w, _ = mid
-    prompts = synth_prompts(10, shape.vocab, 60, 300, seed=23)
-    got = _rollout(_instance(shape, w, max_slots=16, max_seq_len=1024, max_prefill_rows=700),
-                   prompts, 48)
-    monkeypatch.setenv("RLB_ATTN_SPLIT", "0")
-    ref = _rollout(_instance(shape, w, max_slots=16, max_seq_len=1024, max_prefill_rows=700),
-                   prompts, 48)
-    assert got == ref
+    prompts = synth_prompts(4, shape.vocab, 60, 300, seed=23)
+    got = [_instance(shape, w, max_slots=4, max_seq_len=1024, max_prefill_rows=700).score(p)
+           for p in prompts]
+    with monkeypatch.context() as mp:
+        mp.setenv("RLB_ATTN_SPLIT", "0")
+        ref = [_instance(shape, w, max_slots=4, max_seq_len=1024, max_prefill_rows=700).score(p)
+               for p in prompts]
+    for a, b in zip(got, ref):
+        assert np.array_equal(a.view(np.uint32), b.view(np.uint32))
+    # migrate after 20 tokens, resume (prompt + prefix prefill on the split path)
+    full = _rollout(_instance(shape, w, max_slots=8, max_seq_len=1024, max_prefill_rows=700),
+                    prompts, 48)
+    src = _instance(shape, w, max_slots=8, max_seq_len=1024, max_prefill_rows=700, graph_steps=0)
+    for i, p in enumerate(prompts):
+        src.generate(f"r{i}", p, target_len=48)
+    src.step(19)
+    parts = src.export_partials([f"r{i}" for i in range(len(prompts))])
+    dst = _instance(shape, w, max_slots=8, max_seq_len=1024, max_prefill_rows=300)
+    assert _rollout(dst, prompts, 48, prefix=[g for _, g in parts]) == full
+
+
+def test_numerics_plan_in_config(mid):
+    """The split-K factors come from the instance config, are reported in
+    status(), and a runner refuses to mix instances with different plans
+    (a resume between them would not be bit-exact)."""
+    from paper_2510_19225_b200.instance import RolloutInstance
+    from paper_2510_19225_b200.runner import RolloutRunner
+    from spotrl.events import EventLog
+    from spotrl.manager import RolloutManager
+    shape, w, _ = mid
+    a = RolloutInstance(shape, 0, max_slots=4, max_seq_len=256)
+    b = RolloutInstance(shape, 0, max_slots=4, max_seq_len=256, split_o=a_o(a) % 3 + 1)
+    assert a.plan != b.plan and a.status()["plan"] == a.plan
+    assert "o" + str(a_o(a)) in a.plan
+    run = RolloutRunner(RolloutManager(theta=4, m_b=4, log=EventLog()))
+    run.manager.n_prem_cap = 4
+    run.manager.begin_step(0, 0.0)
+    assert run.add_instance("a", a)
+    with pytest.raises(ValueError, match="numerics plan"):
+        run.add_instance("b", b)
+    b.close()
+    with pytest.raises(ValueError):
+        RolloutInstance(shape, 0, max_slots=4, max_seq_len=256, split_o=99)
+
+
+def a_o(inst):
+    return int(inst.plan.split(".")[2][1:])
+
+
+def test_active_weights_only_replaced_at_step_boundary(mid):
+    """rlb_load_weights refuses to overwrite the serving arena
+    while requests are in flight; the shadow arena + swap is the way."""
+    from paper_2510_19225_b200._lib import RlbStateError
+    shape, w, _ = mid
+    inst = _instance(shape, w, max_slots=4, max_seq_len=512)
+    inst.generate("r", synth_prompts(1, shape.vocab, 20, 20, seed=3)[0], target_len=8)
+    inst.step(2)
+    with pytest.raises(RlbStateError):
+        inst.load_weights(w, version=2)
+    inst.pull_shadow(w, version=2)
+    inst.run_to_completion(8)
+    assert inst.swap_weights() == 2
