@@ -1,6 +1,7 @@
-"""The N>1 host logic over gloo with world_size 2 on CPU: timing reduction
-(max over ranks / sums), object exchange (IPC-handle table, NCCL id), and
-independent per-rank rollouts with the CPU fake instance."""
+"""The N>1 host logic over gloo on CPU, at world_size 2 and 8 (the driver's
+8-GPU scaling run, which gpurun cannot reach): timing reduction (max over
+ranks / sums), object exchange (IPC-handle table, NCCL id), independent
+per-rank rollouts with the CPU fake instance; and the 1->7 fan-out plan."""
 import os
 import socket
 
@@ -48,21 +49,37 @@ def _worker(rank, ws, port, q):
     dist.destroy_process_group()
 
 
-def test_two_rank_gloo_plumbing():
-    ws, port = 2, _free_port()
+@pytest.mark.parametrize("ws", [2, 8])
+def test_gloo_plumbing(ws):
+    port = _free_port()
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     procs = [ctx.Process(target=_worker, args=(r, ws, port, q)) for r in range(ws)]
     for p in procs:
         p.start()
-    results = sorted(q.get(timeout=120) for _ in range(ws))
+    results = sorted(q.get(timeout=300) for _ in range(ws))
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
     tokens_per_rank = sum(20 + k for k in range(6))
     for rank, mx, sm, order, ipc1, uid, value in results:
-        assert mx[0] == 2.0 and sm[0] == 3.0              # max / sum of seconds
-        assert sm[1] == 2 * tokens_per_rank               # both ranks' tokens
-        assert order == [0, 1] and ipc1 == bytes([1])
+        assert mx[0] == float(ws) and sm[0] == ws * (ws + 1) / 2    # max / sum of seconds
+        assert sm[1] == ws * tokens_per_rank              # every rank's tokens
+        assert order == list(range(ws)) and ipc1 == bytes([1])
         assert uid == b"nccl-id-from-rank0"
-        assert value == pytest.approx(2 * tokens_per_rank / 2.0)
+        assert value == pytest.approx(ws * tokens_per_rank / ws)   # weak scaling: tokens / slowest
+
+
+@pytest.mark.parametrize("n,rounds", [(1, 1), (3, 8), (7, 8), (7, 3)])
+def test_fanout_plan_partitions_the_arena(n, rounds):
+    """Scatter + all-gather slices for 1 -> n receivers: every arena byte in
+    exactly one (round, receiver) slice, 16-byte aligned, in order."""
+    from paper_2510_19225_b200.pull import FanoutPlan
+    total = 15_231_233_024           # the 7B weight set of config 4
+    plan = FanoutPlan(n, rounds, total)
+    edges = [plan.slice(k, j) for k in range(rounds) for j in range(n)]
+    assert edges[0][0] == 0 and edges[-1][1] == total
+    for (lo, hi), (lo2, _) in zip(edges, edges[1:]):
+        assert lo % 16 == 0 and lo < hi == lo2
+    sizes = [hi - lo for lo, hi in edges]
+    assert max(sizes) - min(sizes) <= 32
