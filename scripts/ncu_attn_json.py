@@ -25,7 +25,7 @@ def main(rep, bench_json, out):
         scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-3,
                  "usecond": 1, "msecond": 1e3}.get(u, 1)
         return v * scale
-    line = json.loads(open(bench_json).read().strip().splitlines()[-1])
+    line = json.loads([ln for ln in open(bench_json) if ln.startswith("{")][-1])
     roof = line["roofline"]
     rd, wr = val("dram__bytes_read.sum"), val("dram__bytes_write.sum")
     dur = val("gpu__time_duration.sum")

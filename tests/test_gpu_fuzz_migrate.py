@@ -7,8 +7,9 @@ Per seed: 4 rollout instances of the tiny decoder share one B200 under
 At random flushes an instance is preempted and a replacement registers,
 pulls the weights and becomes Active; the next victim is the instance holding
 the most already-migrated requests, so requests move more than once; after
-every replacement the reference `lb_tick` (plateau 2) moves executing
-requests onto the idle newcomer.  Every request must end bit-identical to an
+every flush the reference `lb_tick` (plateau 2) runs, moving pending requests
+to empty queues and, once the queues drain, executing requests above the
+plateau onto an instance that runs nothing.  Every request must end bit-identical to an
 uninterrupted single-instance rollout, and the reference's own log audits
 (`pkg/tests/oracles.py`) must pass."""
 import random
@@ -85,8 +86,10 @@ def test_fuzzed_multihop_migration_bit_exact(setup, seed):
             run.preempt(victim)
             new_instance(f"i{next_id}")
             next_id += 1
-            run.rebalance(plateau2)
             run.pump()
+        # the reference rebalancer every flush: its executing branch fires once
+        # every queue is drained and some instance runs nothing
+        run.rebalance(plateau2)
         run.advance()
         flush += 1
         assert flush < 2000
