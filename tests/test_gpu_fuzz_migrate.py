@@ -75,6 +75,7 @@ def test_fuzzed_multihop_migration_bit_exact(setup, seed):
     kills = sorted(rng.sample(range(2, 14), 3))
     next_id = 4
     flush = 0
+    late_joined = False
     while not m.all_generated():
         run.pump()
         if kills and flush >= kills[0]:
@@ -87,8 +88,13 @@ def test_fuzzed_multihop_migration_bit_exact(setup, seed):
             new_instance(f"i{next_id}")
             next_id += 1
             run.pump()
-        # the reference rebalancer every flush: its executing branch fires once
-        # every queue is drained and some instance runs nothing
+        if not kills and not late_joined and not m.held and \
+                not any(m.pending_queues[i] for i in run.instances):
+            # a late joiner once the queues are drained: it runs nothing, so
+            # the reference lb_tick's executing branch moves requests onto it
+            new_instance(f"i{next_id}")
+            late_joined = True
+        # the reference rebalancer every flush
         run.rebalance(plateau2)
         run.advance()
         flush += 1
