@@ -106,6 +106,10 @@ const char* rlb_last_error(void);
  * writes at most cap. */
 int32_t rlb_numerics_plan(const rlb_instance* h, int32_t* out, int32_t cap);
 
+/* (test hook) The paged KV pool: device base pointer and bytes.  Bitwise
+ * A/B checks of kernels that must not change a row's bits compare it. */
+int rlb_kv_pool(rlb_instance* h, void** base, int64_t* bytes);
+
 /* ---- weights (K7) ------------------------------------------------------ */
 /* Engine-arena size in bytes for a model shape. */
 int64_t rlb_arena_bytes(const rlb_model_cfg* model);

@@ -80,6 +80,7 @@ _SIGS = {
                                            ctypes.POINTER(EngineCfg), ctypes.POINTER(_P)]),
     "rlb_instance_destroy": (ctypes.c_int, [_P]),
     "rlb_numerics_plan": (ctypes.c_int32, [_P, _P, ctypes.c_int32]),
+    "rlb_kv_pool": (ctypes.c_int, [_P, ctypes.POINTER(_P), ctypes.POINTER(ctypes.c_int64)]),
     "rlb_last_error": (ctypes.c_char_p, []),
     "rlb_arena_bytes": (ctypes.c_int64, [ctypes.POINTER(ModelCfg)]),
     "rlb_hf_tensor_count": (ctypes.c_int32, [ctypes.POINTER(ModelCfg)]),

@@ -224,6 +224,11 @@ struct rlb_instance {
   // prefill row pairs split by context length (short: <= 2 pages, 2-warp
   // attention CTAs); set per chunk by admit_and_prefill (RLB_ATTN_SPLIT=0: off)
   int* d_pairs = nullptr;
+  int* d_attn_sched = nullptr;   // claim / exit counters of the streaming attention grid
+  // decode attention on the streaming grid (K1s); RLB_ATTN_STREAM=0 at
+  // instance creation selects the per-item grid (K1) -- the same bits, the
+  // A/B reference of tests/test_gpu_engine.py
+  bool attn_stream = true;
   std::vector<int> h_pairs;
   int pairs_short = 0, pairs_long = 0;
   bool attn_split = true;
@@ -434,7 +439,7 @@ rlb_instance::~rlb_instance() {
   void* bufs[] = {arena, kv, d_bt, d_seq_tokens, d_seq_len, d_seq_target, d_row_tok, d_row_pos,
                   d_row_slot, d_logit_src, d_logit_slot, d_dec_slots, d_h, d_xn, d_qkv, d_q,
                   d_attn, d_act, d_logits, d_ws, d_ring, d_ring_ctr, d_ring_cur, d_rope,
-                  d_part, d_exp_slots, d_exp_cu, d_exp_out, d_pairs};
+                  d_part, d_exp_slots, d_exp_cu, d_exp_out, d_pairs, d_attn_sched};
   for (void* b : bufs)
     if (b) cudaFree(b);
   if (shadow.arena) cudaFree(shadow.arena);
@@ -520,6 +525,7 @@ int rlb_instance::init() {
   if (const char* ov = std::getenv("RLB_QKV_BN")) bn_qkv_decode = std::atoi(ov) == 128 ? 128 : 64;
   if (const char* ov = std::getenv("RLB_ATTN_PAIRS")) attn_pairs = std::atoi(ov) != 0;
   if (const char* ov = std::getenv("RLB_ATTN_SPLIT")) attn_split = std::atoi(ov) != 0;
+  if (const char* ov = std::getenv("RLB_ATTN_STREAM")) attn_stream = std::atoi(ov) != 0;
   if (const char* ov = std::getenv("RLB_QKV_KPS")) qkv_kps2 = std::atoi(ov) == 2;
   if (const char* ov = std::getenv("RLB_O_KPS")) o_kps2 = std::atoi(ov) == 2;
   if (const char* ov = std::getenv("RLB_SMALL_GU_WAVE")) small_gu_wave = std::atoi(ov) != 0;
@@ -560,6 +566,9 @@ int rlb_instance::init() {
   RLB_CUDA(cudaMemset(arena, 0, arena_bytes));
   layer_stride = static_cast<size_t>(num_pages) * NKV * 2 * PAGE * D;
   if ((rc = dalloc(&kv, layer_stride * m.layers))) return rc;
+  // zeroed once: pages never written read as zeros (bytewise KV comparisons,
+  // compute-sanitizer initcheck)
+  RLB_CUDA(cudaMemset(kv, 0, layer_stride * m.layers * sizeof(bf16)));
   if ((rc = dalloc(&d_bt, static_cast<size_t>(max_slots) * pps))) return rc;
   h_bt.assign(static_cast<size_t>(max_slots) * pps, 0);
   RLB_CUDA(cudaMemset(d_bt, 0, sizeof(int) * h_bt.size()));
@@ -593,6 +602,8 @@ int rlb_instance::init() {
   if ((rc = dalloc(&d_part, part * R))) return rc;
   if ((rc = dalloc(&d_ring, static_cast<size_t>(RING_ROWS) * max_slots))) return rc;
   if ((rc = dalloc(&d_pairs, max_rows / 2 + 1))) return rc;
+  if ((rc = dalloc(&d_attn_sched, 2))) return rc;
+  RLB_CUDA(cudaMemset(d_attn_sched, 0, 2 * sizeof(int)));
   if ((rc = dalloc(&d_exp_slots, max_slots)) || (rc = dalloc(&d_exp_cu, max_slots + 1)) ||
       (rc = dalloc(&d_exp_out, static_cast<size_t>(max_slots) * max_seq)))
     return rc;
@@ -705,6 +716,7 @@ int rlb_instance::forward_layers(int R, bool prefill) {
     if ((rc = qkv_launch(tp, w, pq))) return rc;
     AttnArgs a{d_q, NQ * D, kv_l, d_bt, pps, d_row_slot, d_row_pos, R, NQ, NKV, D, max_splits,
                d_ws, d_attn, NQ * D};
+    if (!prefill && attn_stream) a.sched = d_attn_sched;
     if (prefill && attn_pairs && attn_split && pairs_short + pairs_long > 0) {
       a.pair_ids = d_pairs;
       a.n_short = pairs_short;
@@ -1097,6 +1109,13 @@ int rlb_instance_destroy(rlb_instance* h) {
   return RLB_OK;
 }
 
+int rlb_kv_pool(rlb_instance* h, void** base, int64_t* bytes) {
+  RLB_CHECK(h, RLB_ERR_ARG, "null handle");
+  if (base) *base = h->kv;
+  if (bytes) *bytes = static_cast<int64_t>(h->layer_stride * h->m.layers * sizeof(bf16));
+  return RLB_OK;
+}
+
 int32_t rlb_numerics_plan(const rlb_instance* h, int32_t* out, int32_t cap) {
   if (!h) return 0;
   const int32_t plan[7] = {1, h->sp_qkv, h->sp_o, h->sp_down, attention_window_positions(), PAGE, 0};
@@ -1433,6 +1452,7 @@ int rlb_profile_kernel(rlb_instance* h, int32_t which, int32_t iters, double* av
       case 0: {
         AttnArgs a{h->d_q, NQ * D, h->kv, h->d_bt, h->pps, h->d_row_slot, h->d_row_pos, R, NQ,
                    h->NKV, D, h->max_splits, h->d_ws, h->d_attn, NQ * D};
+        if (h->attn_stream) a.sched = h->d_attn_sched;
         return attention_launch(a, h->st);
       }
       // projections with their fused epilogues, outputs to scratch where the

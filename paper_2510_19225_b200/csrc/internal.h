@@ -65,6 +65,9 @@ struct AttnArgs {
   // pair_ids[n_short, n_short + n_long) the rest; null = every pair, 4 warps
   const int* pair_ids = nullptr;
   int n_short = 0, n_long = 0;
+  // decode: claim / exit counters of the streaming grid (2 ints, zero between
+  // launches; the last CTA of a launch resets them); null = attn_mma_kernel
+  int* sched = nullptr;
 };
 int attention_launch(const AttnArgs& a, cudaStream_t st, bool row_pairs = false);
 int attention_windows(int max_seq);   // CTA windows per row (AttnArgs.max_splits)

@@ -139,6 +139,12 @@ class RolloutInstance:
         """The arena was filled externally (fan-out pull) with `version`."""
         check(_lib.lib().rlb_mark_weights(self._h, version))
 
+    def kv_pool(self) -> tuple[int, int]:
+        """(test hook) device pointer + bytes of the paged KV pool."""
+        p, n = ctypes.c_void_p(), ctypes.c_int64()
+        check(_lib.lib().rlb_kv_pool(self._h, ctypes.byref(p), ctypes.byref(n)))
+        return int(p.value or 0), int(n.value)
+
     def arena(self) -> tuple[int, int]:
         p, n = ctypes.c_void_p(), ctypes.c_int64()
         check(_lib.lib().rlb_weights_arena(self._h, ctypes.byref(p), ctypes.byref(n)))
