@@ -53,6 +53,11 @@ def main():
     ap.add_argument("--lb-every", type=int, default=2)
     ap.add_argument("--epsilon", type=float, default=0.05)
     ap.add_argument("--shape", default="qwen2.5-7b")
+    ap.add_argument("--late-join", type=int, default=0,
+                    help="the last instance registers after this many decode steps (a spot "
+                         "instance arriving mid-step; 0 = all from the start)")
+    ap.add_argument("--kv-gb", type=float, default=0.0,
+                    help="KV page pool per instance in GB (0 = max_inflight x max_seq)")
     ap.add_argument("--no-warmup", action="store_true",
                     help="skip the discarded first run (it captures the decode graphs of every "
                          "batch size, so the timed runs compare like with like)")
@@ -82,9 +87,12 @@ def main():
     prompts = synth_prompts(total, shape.vocab, 128, 384, seed=77)
     targets = longtail_lengths(total, args.min_len, args.max_len, seed=78)
     max_seq = 384 + args.max_len
+    kv_tok = 2 * shape.layers * shape.n_kv_heads * shape.head_dim * 2
+    pages = int(args.kv_gb * 1e9 / (64 * kv_tok)) if args.kv_gb > 0 else 0
     instances = {iid: RolloutInstance(shape, k % n_gpu, max_slots=args.max_inflight,
-                                      max_seq_len=max_seq, graph_steps=16)
+                                      max_seq_len=max_seq, graph_steps=16, num_pages=pages)
                  for k, iid in enumerate(ids)}
+    late = ids[-1] if args.late_join > 0 else None
 
     def run_once(tag, profile):
         m = RolloutManager(theta=args.theta, m_b=16, log=EventLog())
@@ -96,12 +104,14 @@ def main():
         run.stage(1, w)
         for iid in ids:
             instances[iid].decode_profile(reset=True)
-            assert run.add_instance(iid, instances[iid])
+            if iid != late:
+                assert run.add_instance(iid, instances[iid])
+        join = {args.late_join: [(late, instances[late])]} if late else None
         for r, (p, t) in enumerate(zip(prompts, targets)):
             run.submit(f"r{r}", p, target_len=t)
         t0 = time.perf_counter()
         run.run(profile=profile, lb_every=args.lb_every if profile is not None else 0,
-                epsilon=args.epsilon)
+                epsilon=args.epsilon, join_at=join)
         wall = time.perf_counter() - t0
         recs = m.log.records
         res = {"wall_s": wall,
@@ -136,7 +146,9 @@ def main():
                                   f"({shape.name}), response lengths lognormal in "
                                   f"[{args.min_len}, {args.max_len}], JSQ theta={args.theta}, "
                                   f"max_inflight={args.max_inflight}, lb_tick every "
-                                  f"{args.lb_every} flushes of {args.flush_steps} steps",
+                                  f"{args.lb_every} flushes of {args.flush_steps} steps"
+                                  + (f", {late} joins at decode step {args.late_join}"
+                                     if late else ""),
                       "target_len_mean": sum(targets) / len(targets),
                       "target_len_max": max(targets)},
            "static": static, "rebalanced": rebal,

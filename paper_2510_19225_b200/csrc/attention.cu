@@ -305,372 +305,6 @@ __global__ void __launch_bounds__(WARPS * 32, ATTN_MINB) attn_mma_kernel(AttnArg
   attn_run_item<D>(a, blockIdx.x, blockIdx.y, blockIdx.z, it, smem);
 }
 
-// ------------------------------------------------------------ streaming --
-// K1s: the decode kernel as a persistent, continuously streaming grid.
-//
-// attn_mma_kernel pays a fixed cost per CTA -- the dependent loads of the
-// row's metadata and q, the cp.async pipeline filling from empty, the
-// CTA-wide merge and its __syncthreads -- while its SM slot streams nothing.
-// ncu (profiles/r2_attn_{mid,short}_ncu.json) puts it at ~17 us per launch
-// (73 us at context 772, 45 us at 388: a 7.3 TB/s marginal rate).  Here a
-// grid of 2 CTAs per SM claims items (row, kv head, window) dynamically from
-// a per-instance counter (longest rows first, like the hardware's block
-// order) and each WARP streams its chunks without ever draining its ring:
-// the chunk stream of a warp runs across items, the next items' page ids
-// and q are loaded while the current one streams, and the four warp
-// partials of an item meet in a shared-memory merge slot whose last
-// arriving warp merges and writes the row while the other warps already
-// stream the next item.
-//
-// Same bits as attn_mma_kernel: every warp processes the same pages
-// (page p of the window -> warp p mod 4) in the same 16-token chunk order
-// with the same online-softmax arithmetic, and the merge combines the four
-// warp partials in warp order with the same max / exp2 / fma / divide
-// sequence per output element.
-constexpr int JQ = 8;   // claimed-item ring per CTA
-
-struct StreamSlot {     // per-CTA control block (after the merge slot in smem)
-  int jobs[JQ];         // claimed item ids (-1: no more items)
-  int nclaimed;         // jobs claimed so far (written by warp 0, lane 0)
-  int cnt;              // warps that deposited the current merge
-  int epoch;            // merge sequence number the slot accepts next
-  int pad;
-};
-
-template <int D>
-struct StreamJob {
-  int item;       // -1: end of the stream
-  int n, wn;      // row context; positions of this window
-  int ws, kvh, r;
-  int my_page;    // this lane's page (segment = lane) of this warp
-  int nchunks;    // this warp's chunks
-};
-
-__device__ __forceinline__ int ld_volatile(const int* p) {
-  return *reinterpret_cast<const volatile int*>(p);
-}
-
-template <int D>
-__device__ __forceinline__ void stream_job_desc(const AttnArgs& a, int item, StreamJob<D>& J) {
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  J.item = item;
-  J.n = J.wn = J.nchunks = J.my_page = 0;
-  J.ws = J.kvh = J.r = 0;
-  if (item < 0) return;
-  J.ws = item % a.max_splits;
-  J.kvh = (item / a.max_splits) % a.NKV;
-  J.r = item / (a.max_splits * a.NKV);
-  const int n = a.row_pos[J.r] + 1;
-  const int w0 = J.ws * SUPER;
-  if (w0 >= n) return;
-  J.n = n;
-  J.wn = min(SUPER, n - w0);
-  const int npages = (J.wn + PAGE - 1) / PAGE;
-  const int nseg = npages > warp ? (npages - warp + WARPS - 1) / WARPS : 0;
-  if (lane < nseg)
-    J.my_page = a.block_table[static_cast<size_t>(a.row_slot[J.r]) * a.bt_stride + w0 / PAGE +
-                              warp + lane * WARPS];
-  const int last_seg_tokens = nseg > 0 ? min(PAGE, J.wn - (warp + (nseg - 1) * WARPS) * PAGE) : 0;
-  J.nchunks = nseg > 0 ? (nseg - 1) * (PAGE / CHUNK) + (last_seg_tokens + CHUNK - 1) / CHUNK : 0;
-}
-
-template <int D>
-__device__ __forceinline__ void stream_q(const AttnArgs& a, const StreamJob<D>& J,
-                                         uint32_t (&qa)[D / 16][2]) {
-  const int lane = threadIdx.x & 31;
-  const int G = a.NQ / a.NKV;
-  const int h = lane >> 2;
-  const bool ok = J.n > 0 && h < G;
-  const bf16* qrow = a.q + static_cast<size_t>(J.r) * a.ldq + static_cast<size_t>(J.kvh * G + h) * D;
-#pragma unroll
-  for (int kk = 0; kk < D / 16; ++kk) {
-    const int c = kk * 16 + 2 * (lane & 3);
-    qa[kk][0] = ok ? *reinterpret_cast<const uint32_t*>(qrow + c) : 0u;
-    qa[kk][1] = ok ? *reinterpret_cast<const uint32_t*>(qrow + c + 8) : 0u;
-  }
-}
-
-template <int N>
-__device__ __forceinline__ void cp_wait_le(int pending) {
-  // wait until at most `pending` (0..N) committed groups are outstanding
-  if constexpr (N >= 2) {
-    if (pending >= 2) { cp_wait<2>(); return; }
-  }
-  if (pending >= 1) { cp_wait<1>(); return; }
-  cp_wait<0>();
-}
-
-template <int D>
-__global__ void __launch_bounds__(WARPS * 32, ATTN_MINB) attn_stream_kernel(AttnArgs a) {
-  constexpr int ROWB = D * 2;
-  constexpr int CPR = ROWB / 16;
-  constexpr int KSTEPS = D / 16;
-  constexpr int NT = D / 8;
-  constexpr int STAGE_BYTES = 2 * CHUNK * ROWB;
-  constexpr int WARP_SMEM = STAGES * STAGE_BYTES;
-  static_assert(STAGES <= 3, "cp_wait_le covers at most 2 groups ahead");
-  extern __shared__ __align__(128) uint8_t smem[];
-  float* red = reinterpret_cast<float*>(smem + WARPS * WARP_SMEM);   // [WARPS][8][D]
-  float* mls = red + WARPS * 8 * D;                                   // [WARPS][8][2]
-  float* cwl = mls + WARPS * 8 * 2;                                   // [8][WARPS] weights, [8] L
-  StreamSlot* ctl = reinterpret_cast<StreamSlot*>(cwl + 8 * WARPS + 8);
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int G = a.NQ / a.NKV;
-  const int items = a.R * a.NKV * a.max_splits;
-  const float scale = rsqrtf(static_cast<float>(D)) * 1.4426950408889634f;
-  const size_t page_stride = static_cast<size_t>(a.NKV) * (2 * PAGE * D);
-
-  pdl_trigger();
-  pdl_wait();   // q, K/V of this step and the claim counter come from the predecessors
-
-  auto claim = [&](int k) {     // warp 0, lane 0 only
-    const int it = atomicAdd(&a.sched[0], 1);
-    ctl->jobs[k % JQ] = it < items ? it : -1;
-    __threadfence_block();
-    *reinterpret_cast<volatile int*>(&ctl->nclaimed) = k + 1;
-  };
-  if (threadIdx.x == 0) {
-    ctl->cnt = 0;
-    ctl->epoch = 0;
-    for (int k = 0; k < 3; ++k) claim(k);
-  }
-  __syncthreads();
-  auto job_item = [&](int k) {  // claimed item of CTA-job k (spins until claimed)
-    while (ld_volatile(&ctl->nclaimed) <= k) __nanosleep(32);
-    __threadfence_block();
-    return ctl->jobs[k % JQ];
-  };
-
-  uint8_t* wsm = smem + warp * WARP_SMEM;
-  const uint32_t wsm_u32 = smem_u32(wsm);
-  // descriptors of jobs jc, jc+1, jc+2 (the issue pointer never runs further);
-  // separate variables, selected with ternaries, so they stay in registers
-  StreamJob<D> j0, j1, j2;
-  stream_job_desc<D>(a, job_item(0), j0);
-  stream_job_desc<D>(a, j0.item < 0 ? -1 : job_item(1), j1);
-  stream_job_desc<D>(a, j1.item < 0 ? -1 : job_item(2), j2);
-  uint32_t qa[KSTEPS][2], qn[KSTEPS][2];
-  stream_q<D>(a, j0, qa);
-  stream_q<D>(a, j1, qn);
-
-  // issue side of the warp's chunk stream: job ji (0..2 relative to jc), chunk ii
-  int ji = 0, ii = 0;
-  int issued = 0, computed = 0;          // chunks (one cp.async group each)
-  auto pick = [&](int k, int StreamJob<D>::*f) { return k == 0 ? j0.*f : (k == 1 ? j1.*f : j2.*f); };
-  auto issue_next = [&]() {
-    while (ji < 3 && pick(ji, &StreamJob<D>::item) >= 0 && ii >= pick(ji, &StreamJob<D>::nchunks)) {
-      ++ji;
-      ii = 0;
-    }
-    if (ji >= 3 || pick(ji, &StreamJob<D>::item) < 0) return;
-    const int my_page = pick(ji, &StreamJob<D>::my_page);
-    const int wn = pick(ji, &StreamJob<D>::wn);
-    const int kvh = pick(ji, &StreamJob<D>::kvh);
-    const int c = ii++;
-    const int seg = c >> 2;
-    const int page = __shfl_sync(0xffffffffu, my_page, seg);
-    const int seg_tok = min(PAGE, wn - (warp + seg * WARPS) * PAGE);
-    const bf16* kp = a.kv + static_cast<size_t>(page) * page_stride +
-                     static_cast<size_t>(kvh) * (2 * PAGE * D);
-    const uint32_t st = wsm_u32 + (issued % STAGES) * STAGE_BYTES;
-#pragma unroll
-    for (int i = 0; i < (CHUNK * CPR) / 32; ++i) {
-      const int idx = i * 32 + lane;
-      const int row = idx / CPR, ch = idx % CPR;
-      const int tok = (c & 3) * CHUNK + row;
-      const bool ok = tok < seg_tok;
-      const bf16* src = kp + static_cast<size_t>(ok ? tok : 0) * D + ch * 8;
-      const uint32_t off = row * ROWB + ((ch ^ (row & 7)) << 4);
-      cp_async16(st + off, src, ok);
-      cp_async16(st + CHUNK * ROWB + off, src + PAGE * D, ok);
-    }
-    cp_commit();
-    ++issued;
-  };
-  for (int k = 0; k < STAGES - 1; ++k) issue_next();
-
-  int merges = 0;                         // merge sequence number of the next non-empty job
-  for (int jc = 0; j0.item >= 0; ++jc) {
-    const StreamJob<D>& J = j0;
-    float o[NT][4];
-#pragma unroll
-    for (int t = 0; t < NT; ++t) o[t][0] = o[t][1] = o[t][2] = o[t][3] = 0.f;
-    float m_run = -INFINITY, l_run = 0.f;
-    for (int c = 0; c < J.nchunks; ++c) {
-      issue_next();
-      cp_wait_le<STAGES - 1>(issued - computed - 1);
-      __syncwarp();
-      const uint32_t ks = wsm_u32 + (computed % STAGES) * STAGE_BYTES;
-      const uint32_t vs = ks + CHUNK * ROWB;
-      const int seg_tok = min(PAGE, J.wn - (warp + (c >> 2) * WARPS) * PAGE);
-      const int tok0 = (c & 3) * CHUNK;
-      float s[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
-      {
-        const int mi = lane >> 3, ri = lane & 7;
-        const int row = (mi >> 1) * 8 + ri;
-#pragma unroll
-        for (int kk = 0; kk < KSTEPS; ++kk) {
-          const int ch = 2 * kk + (mi & 1);
-          uint32_t b[4];
-          ldsm_x4(ks + row * ROWB + ((ch ^ (row & 7)) << 4), b);
-          mma_bf16(s[0], qa[kk][0], qa[kk][1], b[0], b[1]);
-          mma_bf16(s[1], qa[kk][0], qa[kk][1], b[2], b[3]);
-        }
-      }
-      float mx = -INFINITY;
-#pragma unroll
-      for (int j = 0; j < 2; ++j)
-#pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          const int tok = tok0 + 8 * j + 2 * (lane & 3) + e;
-          s[j][e] = tok < seg_tok ? s[j][e] * scale : -INFINITY;
-          mx = fmaxf(mx, s[j][e]);
-        }
-      mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
-      mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
-      const float m_new = fmaxf(m_run, mx);
-      const float corr = exp2f(m_run - m_new);
-      float p[2][2], rs = 0.f;
-#pragma unroll
-      for (int j = 0; j < 2; ++j)
-#pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          p[j][e] = exp2f(s[j][e] - m_new);
-          rs += p[j][e];
-        }
-      rs += __shfl_xor_sync(0xffffffffu, rs, 1);
-      rs += __shfl_xor_sync(0xffffffffu, rs, 2);
-      l_run = __fmaf_rn(l_run, corr, rs);
-      m_run = m_new;
-#pragma unroll
-      for (int t = 0; t < NT; ++t) {
-        o[t][0] *= corr;
-        o[t][1] *= corr;
-      }
-      const uint32_t pa0 = pack_bf2(p[0][0], p[0][1]);
-      const uint32_t pa2 = pack_bf2(p[1][0], p[1][1]);
-      {
-        const int mi = lane >> 3, ri = lane & 7;
-        const int row = (mi & 1) * 8 + ri;
-#pragma unroll
-        for (int dt = 0; dt < NT / 2; ++dt) {
-          const int ch = 2 * dt + (mi >> 1);
-          uint32_t b[4];
-          ldsm_x4_t(vs + row * ROWB + ((ch ^ (row & 7)) << 4), b);
-          mma_bf16(o[2 * dt], pa0, pa2, b[0], b[1]);
-          mma_bf16(o[2 * dt + 1], pa0, pa2, b[2], b[3]);
-        }
-      }
-      ++computed;
-      __syncwarp();
-    }
-
-    if (J.n > 0) {
-      // ---- deposit this warp's partial into the merge slot (sequence `merges`)
-      while (ld_volatile(&ctl->epoch) != merges) __nanosleep(20);
-      __threadfence_block();
-      {
-        const int h = lane >> 2;
-#pragma unroll
-        for (int t = 0; t < NT; ++t) {
-          const int col = t * 8 + 2 * (lane & 3);
-          *reinterpret_cast<float2*>(&red[(warp * 8 + h) * D + col]) = make_float2(o[t][0], o[t][1]);
-        }
-        if ((lane & 3) == 0) {
-          mls[(warp * 8 + h) * 2] = m_run;
-          mls[(warp * 8 + h) * 2 + 1] = l_run;
-        }
-      }
-      __threadfence_block();
-      __syncwarp();
-      int last = 0;
-      if (lane == 0) last = atomicAdd(&ctl->cnt, 1) == WARPS - 1;
-      last = __shfl_sync(0xffffffffu, last, 0);
-      if (last) {
-        // ---- merge the four warp partials in warp order (one warp): the
-        // per-(head, warp) weights once, then every output element with the
-        // same fma sequence as attn_mma_kernel's merge
-        __threadfence_block();
-        {
-          const int g = lane >> 2, w = lane & 3;    // lane = one (head slot, warp) pair
-          float M = -INFINITY;
-#pragma unroll
-          for (int u = 0; u < WARPS; ++u) M = fmaxf(M, mls[(u * 8 + g) * 2]);
-          cwl[g * WARPS + w] = exp2f(mls[(w * 8 + g) * 2] - M);
-        }
-        __syncwarp();
-        if (lane < 8) {
-          float L = 0.f;
-#pragma unroll
-          for (int u = 0; u < WARPS; ++u)
-            L = __fmaf_rn(cwl[lane * WARPS + u], mls[(u * 8 + lane) * 2 + 1], L);
-          cwl[8 * WARPS + lane] = L;
-        }
-        __syncwarp();
-        const bool single = J.n <= SUPER;
-        for (int i = lane; i < G * D; i += 32) {
-          const int g = i / D, d = i % D;
-          float O = 0.f;
-#pragma unroll
-          for (int u = 0; u < WARPS; ++u) O = __fmaf_rn(cwl[g * WARPS + u], red[(u * 8 + g) * D + d], O);
-          const int qh = J.kvh * G + g;
-          if (single) {
-            a.out[static_cast<size_t>(J.r) * a.ldo + qh * D + d] =
-                __float2bfloat16_rn(O / cwl[8 * WARPS + g]);
-          } else {
-            float M = -INFINITY;
-#pragma unroll
-            for (int u = 0; u < WARPS; ++u) M = fmaxf(M, mls[(u * 8 + g) * 2]);
-            float* wsp = a.ws + ((static_cast<size_t>(J.r) * a.NQ + qh) * a.max_splits + J.ws) * (D + 2);
-            wsp[d] = O;
-            if (d == 0) {
-              wsp[D] = M;
-              wsp[D + 1] = cwl[8 * WARPS + g];
-            }
-          }
-        }
-        __syncwarp();
-        if (lane == 0) {
-          ctl->cnt = 0;
-          __threadfence_block();
-          *reinterpret_cast<volatile int*>(&ctl->epoch) = merges + 1;
-        }
-      }
-      ++merges;
-    }
-
-    // ---- advance: job jc+1 becomes current; claim / describe job jc+3
-    if (ji == 0) {          // every chunk of job jc issued: the pointer is at job jc+1
-      ji = 1;
-      ii = 0;
-    }
-    j0 = j1;
-    j1 = j2;
-#pragma unroll
-    for (int kk = 0; kk < KSTEPS; ++kk) {
-      qa[kk][0] = qn[kk][0];
-      qa[kk][1] = qn[kk][1];
-    }
-    if (warp == 0 && lane == 0 && j1.item >= 0 && ld_volatile(&ctl->nclaimed) == jc + 3)
-      claim(jc + 3);
-    __syncwarp();
-    stream_job_desc<D>(a, j1.item < 0 ? -1 : job_item(jc + 3), j2);
-    stream_q<D>(a, j1, qn);
-    --ji;
-  }
-  cp_wait<0>();
-  // the last CTA out resets the claim counter for the next launch
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence();
-    if (atomicAdd(&a.sched[1], 1) == static_cast<int>(gridDim.x) - 1) {
-      a.sched[0] = 0;
-      a.sched[1] = 0;
-      __threadfence();
-    }
-  }
-}
-
 // Prefill variant: one CTA serves two consecutive token rows (2p, 2p+1) of
 // the same sequence, the second row's GQA group in MMA rows 8..15 (zero in
 // the decode kernel), so every K/V chunk is loaded once for both.  Each row
@@ -992,7 +626,6 @@ static int launch_attn(const AttnArgs& a, cudaStream_t st, bool pairs) {
   constexpr int smem2 = smem_pipe2 > smem_red2 ? smem_pipe2 : smem_red2;
   constexpr int smem_pipe2s = 2 * ATTN_PAIR_STAGES * 2 * CHUNK * D * 2;   // 2-warp short pairs
   constexpr int smem2s = smem_pipe2s > smem_red2 ? smem_pipe2s : smem_red2;
-  constexpr int smem_stream = smem_pipe + smem_red + (8 * WARPS + 8) * 4 + static_cast<int>(sizeof(StreamSlot));
   static bool attr[64] = {false};
   int dev = 0;
   RLB_CUDA(cudaGetDevice(&dev));
@@ -1002,8 +635,6 @@ static int launch_attn(const AttnArgs& a, cudaStream_t st, bool pairs) {
                                   smem2));
     RLB_CUDA(cudaFuncSetAttribute(attn_pair_kernel<D, 2>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, smem2s));
-    RLB_CUDA(cudaFuncSetAttribute(attn_stream_kernel<D>,
-                                  cudaFuncAttributeMaxDynamicSharedMemorySize, smem_stream));
     attr[dev & 63] = true;
   }
   static int n_sm = 0;
@@ -1019,10 +650,6 @@ static int launch_attn(const AttnArgs& a, cudaStream_t st, bool pairs) {
   } else if (pairs) {
     RLB_CUDA(launch_k(attn_pair_kernel<D>, dim3(a.max_splits, a.NKV, (a.R + 1) / 2),
                       dim3(WARPS * 32), smem2, st, a));
-  } else if (a.sched) {     // the streaming grid (decode)
-    const int items = a.R * a.NKV * a.max_splits;
-    RLB_CUDA(launch_k(attn_stream_kernel<D>, dim3(std::min(items, ATTN_MINB * n_sm)),
-                      dim3(WARPS * 32), smem_stream, st, a));
   } else {
     RLB_CUDA(launch_k(attn_mma_kernel<D>, dim3(a.max_splits, a.NKV, a.R), dim3(WARPS * 32), smem,
                       st, a));

@@ -224,11 +224,6 @@ struct rlb_instance {
   // prefill row pairs split by context length (short: <= 2 pages, 2-warp
   // attention CTAs); set per chunk by admit_and_prefill (RLB_ATTN_SPLIT=0: off)
   int* d_pairs = nullptr;
-  int* d_attn_sched = nullptr;   // claim / exit counters of the streaming attention grid
-  // decode attention on the streaming grid (K1s); RLB_ATTN_STREAM=0 at
-  // instance creation selects the per-item grid (K1) -- the same bits, the
-  // A/B reference of tests/test_gpu_engine.py
-  bool attn_stream = true;
   std::vector<int> h_pairs;
   int pairs_short = 0, pairs_long = 0;
   bool attn_split = true;
@@ -372,7 +367,6 @@ struct rlb_instance {
   int pairp = 2 | 4 | 8 | 16;   // + bit 16: QKV (RoPE epilogue) in prefill chunks
   bool pairp_prefill = true;
   bool cl_down_large = false;
-  int mc_gu = 1;   // gate_up A-multicast pairs at > 256 rows (RLB_GU_MC=2)
   bool last_cl_down = true;   // mode of the last forward (its head sums the partials)
   // split-K O / down: sum the splits inside a cluster and add into h in the
   // GEMM epilogue (true), or write fp32 partials that the following RMSNorm
@@ -439,7 +433,7 @@ rlb_instance::~rlb_instance() {
   void* bufs[] = {arena, kv, d_bt, d_seq_tokens, d_seq_len, d_seq_target, d_row_tok, d_row_pos,
                   d_row_slot, d_logit_src, d_logit_slot, d_dec_slots, d_h, d_xn, d_qkv, d_q,
                   d_attn, d_act, d_logits, d_ws, d_ring, d_ring_ctr, d_ring_cur, d_rope,
-                  d_part, d_exp_slots, d_exp_cu, d_exp_out, d_pairs, d_attn_sched};
+                  d_part, d_exp_slots, d_exp_cu, d_exp_out, d_pairs};
   for (void* b : bufs)
     if (b) cudaFree(b);
   if (shadow.arena) cudaFree(shadow.arena);
@@ -521,11 +515,9 @@ int rlb_instance::init() {
     }
     if (n == 3) cl_down_large = c != 0;
   }
-  if (const char* ov = std::getenv("RLB_GU_MC")) mc_gu = std::atoi(ov) == 2 ? 2 : 1;
   if (const char* ov = std::getenv("RLB_QKV_BN")) bn_qkv_decode = std::atoi(ov) == 128 ? 128 : 64;
   if (const char* ov = std::getenv("RLB_ATTN_PAIRS")) attn_pairs = std::atoi(ov) != 0;
   if (const char* ov = std::getenv("RLB_ATTN_SPLIT")) attn_split = std::atoi(ov) != 0;
-  if (const char* ov = std::getenv("RLB_ATTN_STREAM")) attn_stream = std::atoi(ov) != 0;
   if (const char* ov = std::getenv("RLB_QKV_KPS")) qkv_kps2 = std::atoi(ov) == 2;
   if (const char* ov = std::getenv("RLB_O_KPS")) o_kps2 = std::atoi(ov) == 2;
   if (const char* ov = std::getenv("RLB_SMALL_GU_WAVE")) small_gu_wave = std::atoi(ov) != 0;
@@ -602,8 +594,6 @@ int rlb_instance::init() {
   if ((rc = dalloc(&d_part, part * R))) return rc;
   if ((rc = dalloc(&d_ring, static_cast<size_t>(RING_ROWS) * max_slots))) return rc;
   if ((rc = dalloc(&d_pairs, max_rows / 2 + 1))) return rc;
-  if ((rc = dalloc(&d_attn_sched, 2))) return rc;
-  RLB_CUDA(cudaMemset(d_attn_sched, 0, 2 * sizeof(int)));
   if ((rc = dalloc(&d_exp_slots, max_slots)) || (rc = dalloc(&d_exp_cu, max_slots + 1)) ||
       (rc = dalloc(&d_exp_out, static_cast<size_t>(max_slots) * max_seq)))
     return rc;
@@ -716,7 +706,6 @@ int rlb_instance::forward_layers(int R, bool prefill) {
     if ((rc = qkv_launch(tp, w, pq))) return rc;
     AttnArgs a{d_q, NQ * D, kv_l, d_bt, pps, d_row_slot, d_row_pos, R, NQ, NKV, D, max_splits,
                d_ws, d_attn, NQ * D};
-    if (!prefill && attn_stream) a.sched = d_attn_sched;
     if (prefill && attn_pairs && attn_split && pairs_short + pairs_long > 0) {
       a.pair_ids = d_pairs;
       a.n_short = pairs_short;
@@ -738,12 +727,10 @@ int rlb_instance::forward_layers(int R, bool prefill) {
     }
     {
       GemmParams pg{R, 2 * F, H, nullptr, d_act, F, 1, d_part};
-      const bool mc = mc_gu == 2 && tp.bn_gu == BN_GU && tp.bm_gu == 256 &&
-                      ((2 * F) / BN_GU) % 2 == 0;
       if (((pairp & 1) || (R > 512 && pairp_prefill)) && tp.bn_gu == BN_GU && tp.bm_gu == 256) {
         if ((rc = gemm_launch_pairp(m_xn, w.m_gu_small, EPI_SWIGLU, pg, st))) return rc;
       } else if ((rc = gemm_launch(m_xn, tp.bn_gu == BN_SMALL ? w.m_gu_small : w.m_gu, tp.bn_gu,
-                                   EPI_SWIGLU, pg, st, tp.bm_gu, mc ? 2 : 1))) {
+                                   EPI_SWIGLU, pg, st, tp.bm_gu))) {
         return rc;
       }
     }
@@ -1452,7 +1439,6 @@ int rlb_profile_kernel(rlb_instance* h, int32_t which, int32_t iters, double* av
       case 0: {
         AttnArgs a{h->d_q, NQ * D, h->kv, h->d_bt, h->pps, h->d_row_slot, h->d_row_pos, R, NQ,
                    h->NKV, D, h->max_splits, h->d_ws, h->d_attn, NQ * D};
-        if (h->attn_stream) a.sched = h->d_attn_sched;
         return attention_launch(a, h->st);
       }
       // projections with their fused epilogues, outputs to scratch where the

@@ -6,9 +6,9 @@
 // accumulators in TMEM that share every B stage (a weight tile is read once
 // per 256 rows); NACC = 1 gives twice the CTAs for the short projections,
 // which are bound by how fast one SM's shared memory can be fed.  BN is 256,
-// 128 or (RoPE only) 64.  Experiments kept off by default: A-tile multicast
-// across N-tile pairs (MC = 2) and 2-SM pair tiles (gemm_pair_tc); see
-// DESIGN.md §9 for their measurements.
+// 128 or (RoPE only) 64.  (A-tile multicast across N-tile pairs and
+// non-persistent 2-SM 512 x 256 tiles were measured slower and removed;
+// DESIGN.md §9.)
 // Warp roles (384 threads):
 //   warp 0      one elected lane issues TMA loads: A rows [m, m+128), A rows
 //               [m+128, m+256) and B rows [n, n+BN), 64-element (128 B) K
@@ -366,16 +366,10 @@ __device__ __forceinline__ void rope_direct(const GemmParams& p, uint32_t tbase,
   }
 }
 
-// MC = 2: the CTAs of two neighbouring N tiles form a (1,2,1) cluster and
-// share the A (activation) tile: each loads one 128-row half and multicasts
-// it to both, halving the A traffic from L2; both MMA warps release a stage
-// on both CTAs (multicast commit), so neither refills it before the other
-// has consumed it.
-template <int BN, int EPI, int NACC, int MC = 1, int KPS = 1>
+template <int BN, int EPI, int NACC, int KPS = 1>
 __global__ void __launch_bounds__(GEMM_THREADS, 1)
     gemm_bf16_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                  GemmParams p) {
-  static_assert(KPS == 1 || MC == 1, "3D boxes: no multicast");
   using C = GemmCfg<BN, NACC, KPS>;
   static_assert(KPS == 1 || (NACC == 1 && C::STAGES >= 2),
                 "two-K-block stages: one accumulator, at least two stages (the only tested form)");
@@ -416,7 +410,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   const bool via_cluster = kClusterEpi && p.splits > 1;
   // accumulators with at least one live row (a small-M tile skips the
   // loads, MMAs and TMEM reads of the empty one)
-  const int live_acc = MC > 1 ? NACC : ((NACC == 2 && p.M - m_blk * BMT > HM) ? 2 : 1);
+  const int live_acc = (NACC == 2 && p.M - m_blk * BMT > HM) ? 2 : 1;
   const uint32_t stage_tx = static_cast<uint32_t>(live_acc * C::A_BYTES + C::B_BYTES);
 
   if (warp == 0 && lane == 0) {
@@ -424,7 +418,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     tma_prefetch(&tmB);
     for (int s = 0; s < C::STAGES; ++s) {
       mbar_init(smem_u32(&full[s]), 1);
-      mbar_init(smem_u32(&empty[s]), MC);
+      mbar_init(smem_u32(&empty[s]), 1);
     }
     mbar_init(smem_u32(tfull), 1);
     fence_mbar_init();
@@ -432,7 +426,6 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   if (warp == 2) tmem_alloc(smem_u32(tmem_slot), C::TMEM_COLS);
   tc_fence_before();
   __syncthreads();
-  if constexpr (MC > 1) cluster_sync();      // peers' barriers initialised before any multicast
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   if (stamp && threadIdx.x == 0) p.dbg[1] = gtime();
@@ -521,18 +514,11 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           mbar_expect_tx(smem_u32(&full[s]), stage_tx);
           tma_load_2d(smem_u32(st + NACC * C::A_BYTES), &tmB, smem_u32(&full[s]), kx, n_blk * BN);
         }
-        if constexpr (MC > 1) {
-          static_assert(MC == NACC, "one A half per cluster CTA");
-          const int a = static_cast<int>(cluster_rank());
-          tma_load_2d_mc(smem_u32(st + a * C::A_BYTES), &tmA, smem_u32(&full[s]), kx,
-                         m_blk * BMT + a * HM, static_cast<uint16_t>((1u << MC) - 1));
-        } else {
 #pragma unroll
-          for (int a = 0; a < NACC; ++a)
-            if (a < live_acc)
-              tma_load_2d(smem_u32(st + a * C::A_BYTES), &tmA, smem_u32(&full[s]), kx,
-                          m_blk * BMT + a * HM);
-        }
+        for (int a = 0; a < NACC; ++a)
+          if (a < live_acc)
+            tma_load_2d(smem_u32(st + a * C::A_BYTES), &tmA, smem_u32(&full[s]), kx,
+                        m_blk * BMT + a * HM);
       }
     }
   } else if (warp == 1) {
@@ -554,10 +540,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
               umma_bf16(tmem + a * BN, umma_desc_sw128(st + a * C::A_BYTES) + 2 * k, bd + 2 * k,
                         idesc, (kb | k) != 0);
         }
-        if constexpr (MC > 1)
-          umma_commit_mc(smem_u32(&empty[s]), static_cast<uint16_t>((1u << MC) - 1));
-        else
-          umma_commit(smem_u32(&empty[s]));
+        umma_commit(smem_u32(&empty[s]));
       }
       umma_commit(smem_u32(tfull));
       if (stamp) p.dbg[3] = gtime();
@@ -780,7 +763,6 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     }
   }
   if (stamp && threadIdx.x == 128) p.dbg[6] = gtime();
-  if constexpr (MC > 1) cluster_sync();      // no peer arrives on this CTA's barriers any more
   tc_fence_before();
   __syncthreads();
   if (warp == 2) {
@@ -791,210 +773,6 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
 }
 
 // ---------------------------------------------------------------- CTA pairs --
-// K2 on 2-SM tiles (tcgen05 cta_group::2): a (2,1,1) cluster computes a
-// 512 x 256 tile.  CTA r of the pair holds rows {a*256 + r*128 + [0,128)} of
-// both 256-row pair-MMAs (a = 0, 1) and loads the half of the 256 B rows
-// (weights) with index r; each pair-MMA (M=256, N=256, K=16) reads the A
-// rows and B rows of both SMs, and writes each SM's 128 rows into its own
-// TMEM.  Per SM and K step the pair moves 2x16 KB of A + 16 KB of B for a
-// 256 x 256 accumulator (the single-SM 256 x 256 tile moves 64 KB), so the
-// shared-memory feed -- the bound of the decode projections -- drops by 25%.
-// The leader (rank 0) issues every MMA; its full barriers count both CTAs'
-// TMA bytes, and its commits release stages / accumulators on both CTAs.
-struct PairCfg {
-  static constexpr int A_BYTES = HM * BK * 2;          // 128 rows of one pair-MMA
-  static constexpr int B_BYTES = 128 * BK * 2;         // this CTA's half of N = 256
-  static constexpr int STAGE_BYTES = 2 * A_BYTES + B_BYTES;
-  static constexpr int STAGES = 4;
-  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 256;
-  static constexpr uint32_t TMEM_COLS = 512;
-};
-
-template <int EPI>
-__global__ void __launch_bounds__(GEMM_THREADS, 1)
-    gemm_pair_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                 GemmParams p) {
-  using C = PairCfg;
-  constexpr int BN = 256;
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                             ~static_cast<uintptr_t>(1023));
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE_BYTES);
-  uint64_t* full = bars;
-  uint64_t* empty = bars + C::STAGES;
-  uint64_t* tfull = bars + 2 * C::STAGES;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * C::STAGES + 1);
-
-  const int warp = threadIdx.x >> 5;
-  const int lane = threadIdx.x & 31;
-  const int r = static_cast<int>(cluster_rank());      // 0 = leader
-  const int row0 = (blockIdx.x >> 1) * 512 + r * HM;   // + a * 256: this CTA's rows
-  const int n_blk = blockIdx.y;
-  const int nk = p.K / BK;
-  const bool stamp = p.dbg != nullptr && blockIdx.x == 0 && blockIdx.y == 0;
-  auto gtime = []() {
-    unsigned long long t;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    return t;
-  };
-  if (stamp && threadIdx.x == 0) p.dbg[0] = gtime();
-
-  if (warp == 0 && lane == 0) {
-    tma_prefetch(&tmA);
-    tma_prefetch(&tmB);
-    for (int s = 0; s < C::STAGES; ++s) {
-      mbar_init(smem_u32(&full[s]), 1);
-      mbar_init(smem_u32(&empty[s]), 1);
-    }
-    mbar_init(smem_u32(tfull), 1);
-    fence_mbar_init();
-  }
-  if (warp == 2) tmem_alloc_pair(smem_u32(tmem_slot), C::TMEM_COLS);
-  tc_fence_before();
-  __syncthreads();
-  cluster_sync();                            // both CTAs' barriers exist before any signal
-  tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
-  if (stamp && threadIdx.x == 0) p.dbg[1] = gtime();
-  pdl_trigger();
-  const bool producer = warp == 0 && lane == 0;
-  const int pre = nk < C::STAGES ? nk : C::STAGES;
-  if (producer) {                            // weights do not depend on the previous kernel
-    for (int kb = 0; kb < pre; ++kb) {
-      uint8_t* st = smem + kb * C::STAGE_BYTES;
-      if (r == 0) mbar_expect_tx(smem_u32(&full[kb]), 2 * C::STAGE_BYTES);
-      tma_load_2d_pair(smem_u32(st + 2 * C::A_BYTES), &tmB, smem_u32(&full[kb]), kb * BK,
-                       n_blk * BN + r * 128);
-    }
-  }
-  pdl_wait();
-  if (stamp && threadIdx.x == 0) p.dbg[2] = gtime();
-
-  if (warp == 0) {
-    if (producer) {
-      for (int kb = 0; kb < nk; ++kb) {
-        const int s = kb % C::STAGES;
-        const uint32_t ph = (kb / C::STAGES) & 1;
-        uint8_t* st = smem + s * C::STAGE_BYTES;
-        const int kx = kb * BK;
-        if (kb >= pre) {
-          mbar_wait(smem_u32(&empty[s]), ph ^ 1);
-          if (r == 0) mbar_expect_tx(smem_u32(&full[s]), 2 * C::STAGE_BYTES);
-          tma_load_2d_pair(smem_u32(st + 2 * C::A_BYTES), &tmB, smem_u32(&full[s]), kx,
-                           n_blk * BN + r * 128);
-        }
-#pragma unroll
-        for (int a = 0; a < 2; ++a)
-          tma_load_2d_pair(smem_u32(st + a * C::A_BYTES), &tmA, smem_u32(&full[s]), kx,
-                           row0 + a * 256);
-      }
-    }
-  } else if (warp == 1) {
-    if (lane == 0 && r == 0) {
-      constexpr uint32_t idesc = umma_idesc_bf16(256, BN);
-      for (int kb = 0; kb < nk; ++kb) {
-        const int s = kb % C::STAGES;
-        const uint32_t ph = (kb / C::STAGES) & 1;
-        const uint32_t st = smem_u32(smem + s * C::STAGE_BYTES);
-        mbar_wait(smem_u32(&full[s]), ph);
-        tc_fence_after();
-        const uint64_t bd = umma_desc_sw128(st + 2 * C::A_BYTES);
-#pragma unroll
-        for (int k = 0; k < BK / 16; ++k) {
-#pragma unroll
-          for (int a = 0; a < 2; ++a)
-            umma_bf16_pair(tmem + a * BN, umma_desc_sw128(st + a * C::A_BYTES) + 2 * k,
-                           bd + 2 * k, idesc, (kb | k) != 0);
-        }
-        umma_commit_pair(smem_u32(&empty[s]), 0x3);
-      }
-      umma_commit_pair(smem_u32(tfull), 0x3);
-      if (stamp) p.dbg[3] = gtime();
-    }
-  } else if (warp >= 4) {
-    const int half = (warp - 4) >> 2;        // accumulator (pair-MMA) index
-    const int q = warp & 3;
-    const int m = row0 + half * 256 + q * 32 + lane;
-    const bool live = m < p.M;
-    const bool warp_dead = row0 + half * 256 + q * 32 >= p.M;
-    mbar_wait(smem_u32(tfull), 0);
-    if (stamp && threadIdx.x == 128) p.dbg[4] = gtime();
-    tc_fence_after();
-    const uint32_t tbase = tmem + half * BN + (static_cast<uint32_t>(q * 32) << 16);
-    if constexpr (EPI == EPI_SWIGLU) {
-      constexpr int OC = BN / 2;
-      constexpr int PITCH = OC * 2 + 16;
-      uint8_t* stage = smem;
-      const int lrow = half * HM + q * 32 + lane;        // local row 0..255
-#pragma unroll 1
-      for (int g = 0; g < (warp_dead ? 0 : BN / 128); ++g) {
-#pragma unroll 1
-        for (int jc = 0; jc < 64; jc += 32) {
-          uint32_t rg[32], ru[32];
-          tmem_ld32(tbase + g * 128 + jc, rg);
-          tmem_ld32(tbase + g * 128 + 64 + jc, ru);
-          tmem_ld_wait();
-          uint32_t pk[16];
-#pragma unroll
-          for (int i = 0; i < 16; ++i) {
-            const float a0 = silu_f(__uint_as_float(rg[2 * i])) * __uint_as_float(ru[2 * i]);
-            const float a1 = silu_f(__uint_as_float(rg[2 * i + 1])) * __uint_as_float(ru[2 * i + 1]);
-            pk[i] = pack_bf2(a0, a1);
-          }
-          uint4* d = reinterpret_cast<uint4*>(stage + lrow * PITCH + (g * 64 + jc) * 2);
-#pragma unroll
-          for (int i = 0; i < 4; ++i) d[i] = make_uint4(pk[4 * i], pk[4 * i + 1], pk[4 * i + 2], pk[4 * i + 3]);
-        }
-      }
-      asm volatile("bar.sync 1, 256;" ::: "memory");
-      bf16* out = reinterpret_cast<bf16*>(p.out);
-      constexpr int LPR = OC * 2 / 16;
-      constexpr int RPW = 32 / LPR;
-      const int ew = warp - 4;
-      const int sub = lane / LPR, cl = lane % LPR;
-      const int col = n_blk * OC + cl * 8;
-#pragma unroll 2
-      for (int rr = ew * RPW + sub; rr < 2 * HM; rr += 8 * RPW) {
-        const int mm = row0 + (rr / HM) * 256 + rr % HM;
-        if (mm >= p.M || col >= p.N / 2) continue;
-        *reinterpret_cast<uint4*>(out + static_cast<size_t>(mm) * p.ldo + col) =
-            *reinterpret_cast<const uint4*>(stage + rr * PITCH + cl * 16);
-      }
-    } else if constexpr (EPI == EPI_ARGMAX) {
-      float best = -INFINITY;
-      int bidx = 0x7fffffff;
-#pragma unroll 1
-      for (int c = 0; c < (warp_dead ? 0 : BN); c += 32) {
-        uint32_t rv[32];
-        tmem_ld32(tbase + c, rv);
-        tmem_ld_wait();
-        const int n = n_blk * BN + c;
-#pragma unroll
-        for (int i = 0; i < 32; ++i) {
-          const float v = __uint_as_float(rv[i]);
-          if (n + i < p.N && v > best) {
-            best = v;
-            bidx = n + i;
-          }
-        }
-      }
-      if (live) {
-        float2* part = reinterpret_cast<float2*>(p.out) + static_cast<size_t>(m) * p.ldo + n_blk;
-        *part = make_float2(best, __int_as_float(bidx));
-      }
-    }
-  }
-  if (stamp && threadIdx.x == 128) p.dbg[6] = gtime();
-  tc_fence_before();
-  __syncthreads();
-  cluster_sync();                            // the leader's commits have landed on both CTAs
-  if (warp == 2) {
-    tc_fence_after();
-    tmem_dealloc_pair(tmem, C::TMEM_COLS);
-    if (stamp && lane == 0) p.dbg[5] = gtime();
-  }
-}
-
 // Persistent 2-SM GEMM: every (2,1,1) cluster loops over 256 x 256 pair tiles
 // (CTA r: rows m*256 + r*128 + [0,128) and B rows n*256 + r*128 + [0,128)).
 // A tile's accumulator (128 x 256 per SM) lives in one of two TMEM buffers,
@@ -1298,9 +1076,9 @@ int make_kmajor_map3(CUtensorMap* map, const void* ptr, int64_t rows, int64_t k,
   return RLB_OK;
 }
 
-template <int BN, int EPI, int NACC, int MC = 1, int KPS = 1>
+template <int BN, int EPI, int NACC, int KPS = 1>
 static int set_attr() {
-  RLB_CUDA(cudaFuncSetAttribute(gemm_bf16_tc<BN, EPI, NACC, MC, KPS>,
+  RLB_CUDA(cudaFuncSetAttribute(gemm_bf16_tc<BN, EPI, NACC, KPS>,
                                 cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 GemmCfg<BN, NACC, KPS>::SMEM));
   return RLB_OK;
@@ -1326,14 +1104,10 @@ int gemm_prepare() {
   if (done[dev & 63]) return RLB_OK;
   int rc;
   if ((rc = set_attr_bn<128, 2>()) || (rc = set_attr_bn<256, 2>()) || (rc = set_attr_bn<128, 1>()) ||
-      (rc = set_attr_bn<256, 1>()) || (rc = set_attr<256, EPI_SWIGLU, 2, 2>()) ||
-      (rc = set_attr<64, EPI_ROPE, 1>()) || (rc = set_attr<64, EPI_ROPE, 1, 1, 2>()) ||
-      (rc = set_attr<128, EPI_PARTIAL, 1, 1, 2>()))
+      (rc = set_attr_bn<256, 1>()) ||
+      (rc = set_attr<64, EPI_ROPE, 1>()) || (rc = set_attr<64, EPI_ROPE, 1, 2>()) ||
+      (rc = set_attr<128, EPI_PARTIAL, 1, 2>()))
     return rc;
-  RLB_CUDA(cudaFuncSetAttribute(gemm_pair_tc<EPI_SWIGLU>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                PairCfg::SMEM));
-  RLB_CUDA(cudaFuncSetAttribute(gemm_pair_tc<EPI_ARGMAX>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                PairCfg::SMEM));
   RLB_CUDA(cudaFuncSetAttribute(gemm_pairp_tc<EPI_SWIGLU>,
                                 cudaFuncAttributeMaxDynamicSharedMemorySize, PairPCfg<EPI_SWIGLU>::SMEM));
   RLB_CUDA(cudaFuncSetAttribute(gemm_pairp_tc<EPI_ARGMAX>,
@@ -1346,17 +1120,14 @@ int gemm_prepare() {
   return RLB_OK;
 }
 
-template <int BN, int EPI, int NACC, int MC = 1, int KPS = 1>
+template <int BN, int EPI, int NACC, int KPS = 1>
 static int launch_one(const CUtensorMap& a, const CUtensorMap& b, const GemmParams& p,
                       cudaStream_t st) {
   using C = GemmCfg<BN, NACC, KPS>;
   RLB_CHECK((p.N + BN - 1) / BN <= 65535, RLB_ERR_ARG, "too many N tiles");
   dim3 grid((p.M + C::BMT - 1) / C::BMT, (p.N + BN - 1) / BN, p.splits);
   const bool split_cluster = cluster_epi(EPI) && BN == 128 && p.splits > 1;
-  if (split_cluster || MC > 1) {
-    // split-K CTAs of a tile (DSMEM reduction) or A-sharing N-tile pairs
-    RLB_CHECK(MC == 1 || (grid.y % MC == 0 && p.splits == 1), RLB_ERR_ARG,
-              "A multicast needs an even number of N tiles and no split");
+  if (split_cluster) {   // split-K CTAs of a tile (DSMEM reduction)
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = grid;
     cfg.blockDim = dim3(GEMM_THREADS);
@@ -1365,18 +1136,17 @@ static int launch_one(const CUtensorMap& a, const CUtensorMap& b, const GemmPara
     cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeClusterDimension;
     attr[0].val.clusterDim.x = 1;
-    attr[0].val.clusterDim.y = MC;
-    attr[0].val.clusterDim.z = split_cluster ? static_cast<unsigned>(p.splits) : 1u;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = static_cast<unsigned>(p.splits);
     attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = pdl_enabled(RLB_PDL_CLASS) ? 2 : 1;
-    RLB_CUDA(cudaLaunchKernelEx(&cfg, gemm_bf16_tc<BN, EPI, NACC, MC, KPS>, a, b, p));
+    RLB_CUDA(cudaLaunchKernelEx(&cfg, gemm_bf16_tc<BN, EPI, NACC, KPS>, a, b, p));
     return RLB_OK;
   }
-  if constexpr (MC == 1)
-    RLB_CUDA(launch_k(gemm_bf16_tc<BN, EPI, NACC, 1, KPS>, grid, dim3(GEMM_THREADS), C::SMEM, st, a,
-                      b, p));
+  RLB_CUDA(launch_k(gemm_bf16_tc<BN, EPI, NACC, KPS>, grid, dim3(GEMM_THREADS), C::SMEM, st, a, b,
+                    p));
   return RLB_OK;
 }
 
@@ -1407,14 +1177,10 @@ int gemm_launch(const CUtensorMap& a, const CUtensorMap& b, int block_n, int epi
   if (kps == 2 && epi == EPI_PARTIAL) {
     RLB_CHECK(p.ws != nullptr && p.K % BK == 0 && p.K / BK >= p.splits, RLB_ERR_ARG,
               "split-K partials need a workspace");
-    return launch_one<128, EPI_PARTIAL, 1, 1, 2>(a, b, p, st);
+    return launch_one<128, EPI_PARTIAL, 1, 2>(a, b, p, st);
   }
   if (p.M <= 0) return RLB_OK;
-  if (a_multicast == 2) {
-    RLB_CHECK(block_n == 256 && block_m == 256 && epi == EPI_SWIGLU, RLB_ERR_ARG,
-              "A multicast is built for the 256x256 SwiGLU projection");
-    return launch_one<256, EPI_SWIGLU, 2, 2>(a, b, p, st);
-  }
+  RLB_CHECK(a_multicast == 1, RLB_ERR_ARG, "A multicast is not built (measured slower)");
   RLB_CHECK(p.K % BK == 0 && p.N % 16 == 0, RLB_ERR_ARG, "GEMM shape not tileable");
   RLB_CHECK(p.splits >= 1 && p.K / BK >= p.splits, RLB_ERR_ARG,
             "split-K needs at least one K block per split");
@@ -1428,7 +1194,7 @@ int gemm_launch(const CUtensorMap& a, const CUtensorMap& b, int block_n, int epi
   if (block_n == 64) {   // the narrow tile exists for single-split RoPE (decode QKV)
     RLB_CHECK(epi == EPI_ROPE && block_m == 128 && p.splits == 1, RLB_ERR_ARG,
               "64-column tiles: RoPE epilogue, 128-row tiles, no split");
-    if (kps == 2) return launch_one<64, EPI_ROPE, 1, 1, 2>(a, b, p, st);   // 3D-box maps
+    if (kps == 2) return launch_one<64, EPI_ROPE, 1, 2>(a, b, p, st);   // 3D-box maps
     return launch_one<64, EPI_ROPE, 1>(a, b, p, st);
   }
   RLB_CHECK(epi != EPI_SWIGLU || (block_n % 128 == 0 && p.N % 128 == 0), RLB_ERR_ARG,
@@ -1441,34 +1207,6 @@ int gemm_launch(const CUtensorMap& a, const CUtensorMap& b, int block_n, int epi
   }
   set_error("block_n must be 128 or 256");
   return RLB_ERR_ARG;
-}
-
-// 2-SM pair tiles (512 x 256 per cluster); `b128` = weight map with 128-row
-// boxes (each CTA loads half of the 256 B rows).
-int gemm_launch_pair(const CUtensorMap& a, const CUtensorMap& b128, int epi, const GemmParams& p,
-                     cudaStream_t st) {
-  if (p.M <= 0) return RLB_OK;
-  RLB_CHECK(p.K % BK == 0 && p.splits == 1, RLB_ERR_ARG, "pair GEMM: K multiple of 64, no split");
-  RLB_CHECK(epi == EPI_SWIGLU || epi == EPI_ARGMAX, RLB_ERR_ARG,
-            "pair GEMM epilogues: SwiGLU, argmax");
-  RLB_CHECK(epi != EPI_SWIGLU || p.N % 256 == 0, RLB_ERR_ARG, "SwiGLU pair tiles are 256 wide");
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(2 * ((p.M + 511) / 512), (p.N + 255) / 256, 1);
-  cfg.blockDim = dim3(GEMM_THREADS);
-  cfg.dynamicSmemBytes = PairCfg::SMEM;
-  cfg.stream = st;
-  cudaLaunchAttribute attr[2];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = 2;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[1].val.programmaticStreamSerializationAllowed = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = pdl_enabled(RLB_PDL_CLASS) ? 2 : 1;
-  if (epi == EPI_SWIGLU) RLB_CUDA(cudaLaunchKernelEx(&cfg, gemm_pair_tc<EPI_SWIGLU>, a, b128, p));
-  else RLB_CUDA(cudaLaunchKernelEx(&cfg, gemm_pair_tc<EPI_ARGMAX>, a, b128, p));
-  return RLB_OK;
 }
 
 // Persistent 2-SM pair tiles (256 x 256 per cluster, double-buffered TMEM).
@@ -1555,15 +1293,12 @@ extern "C" int rlb_bench_gemm(int device, int32_t M, int32_t N, int32_t K, int32
   const int epi = S > 1 && !cluster_epi(epilogue) ? static_cast<int>(EPI_PARTIAL) : epilogue;
   RLB_CUDA(cudaEventCreate(&e0));
   RLB_CUDA(cudaEventCreate(&e1));
-  const int mc = std::getenv("RLB_GEMM_MC") ? 2 : 1;   // A multicast pairs (SwiGLU 256x256)
-  const bool pair = std::getenv("RLB_GEMM_PAIR") != nullptr;   // 2-SM tiles
+  const bool pair = std::getenv("RLB_GEMM_PAIR") != nullptr;   // persistent 2-SM tiles
   CUtensorMap mb128;
   if (pair && (rc = make_kmajor_map(&mb128, B, N, K, 128))) return rc;
   auto go = [&]() {
-    if (pair && std::atoi(std::getenv("RLB_GEMM_PAIR")) == 2)
-      return gemm_launch_pairp(ma, mb128, epi, p, 0);
-    return pair ? gemm_launch_pair(ma, mb128, epi, p, 0)
-                : gemm_launch(ma, mb, block_n, epi, p, 0, block_m, mc);
+    return pair ? gemm_launch_pairp(ma, mb128, epi, p, 0)
+                : gemm_launch(ma, mb, block_n, epi, p, 0, block_m);
   };
   if ((rc = go())) return rc;
   RLB_CUDA(cudaEventRecord(e0, 0));
@@ -1610,20 +1345,17 @@ extern "C" int rlb_gemm(int device, int32_t M, int32_t N, int32_t K, const void*
   p.out = Cout;
   p.ldo = epilogue == EPI_SWIGLU ? N / 2 : N;
   p.splits = splits < 1 ? 1 : splits;
-  if (std::getenv("RLB_GEMM_PAIR") && p.splits == 1) {   // 2-SM pair tiles
+  // (test entry) RLB_GEMM_PAIR: the persistent 2-SM tiles instead of the
+  // single-SM kernel -- the same bits (tests/test_gpu_kernels.py)
+  if (std::getenv("RLB_GEMM_PAIR") && p.splits == 1) {
     CUtensorMap mb128;
     rc = make_kmajor_map(&mb128, B, N, K, 128);
-    if (!rc)
-      rc = std::atoi(std::getenv("RLB_GEMM_PAIR")) == 2 ? gemm_launch_pairp(ma, mb128, epilogue, p, 0)
-                                                        : gemm_launch_pair(ma, mb128, epilogue, p, 0);
+    if (!rc) rc = gemm_launch_pairp(ma, mb128, epilogue, p, 0);
   } else if (p.splits == 1 || (epilogue == EPI_RESADD && block_n == 128)) {
-    // RESADD: cluster split-K; RLB_GEMM_MC: A-multicast pairs (SwiGLU 256x256)
-    rc = gemm_launch(ma, mb, block_n, epilogue, p, 0, block_m,
-                     std::getenv("RLB_GEMM_MC") ? 2 : 1);
+    rc = gemm_launch(ma, mb, block_n, epilogue, p, 0, block_m);   // RESADD: cluster split-K
   } else {
     RLB_CUDA(cudaMalloc(&p.ws, sizeof(float) * static_cast<size_t>(p.splits) * M * N));
-    const char* pe = std::getenv("RLB_GEMM_PAIR");
-    if (pe && std::atoi(pe) == 2) {   // persistent 2-SM tiles, split-K partials
+    if (std::getenv("RLB_GEMM_PAIR")) {   // persistent 2-SM tiles, split-K partials
       CUtensorMap mb128;
       rc = make_kmajor_map(&mb128, B, N, K, 128);
       if (!rc) rc = gemm_launch_pairp(ma, mb128, EPI_PARTIAL, p, 0);

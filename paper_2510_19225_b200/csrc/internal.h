@@ -46,8 +46,6 @@ int gemm_launch(const CUtensorMap& a, const CUtensorMap& b, int block_n, int epi
                 int kps = 1);
 int make_kmajor_map3(CUtensorMap* map, const void* ptr, int64_t rows, int64_t k, int box_rows,
                      int kps);
-int gemm_launch_pair(const CUtensorMap& a, const CUtensorMap& b128, int epi, const GemmParams& p,
-                     cudaStream_t st);
 int gemm_launch_pairp(const CUtensorMap& a, const CUtensorMap& b128, int epi, const GemmParams& p,
                       cudaStream_t st);
 
@@ -65,9 +63,6 @@ struct AttnArgs {
   // pair_ids[n_short, n_short + n_long) the rest; null = every pair, 4 warps
   const int* pair_ids = nullptr;
   int n_short = 0, n_long = 0;
-  // decode: claim / exit counters of the streaming grid (2 ints, zero between
-  // launches; the last CTA of a launch resets them); null = attn_mma_kernel
-  int* sched = nullptr;
 };
 int attention_launch(const AttnArgs& a, cudaStream_t st, bool row_pairs = false);
 int attention_windows(int max_seq);   // CTA windows per row (AttnArgs.max_splits)

@@ -175,3 +175,32 @@ def test_preempted_instance_torn_down_off_the_resume_path():
     rep = out["resume_i1"]
     assert rep["preempt_ms"] >= 0 and rep["route_submit_ms"] >= 0
     run.close()
+
+
+def test_late_joiner_receives_executing_requests():
+    """A spot instance registering mid-step (join_at) pulls, goes Active, and
+    the reference lb_tick's executing branch moves requests above the plateau
+    onto it (config 5's elastic case); every request stays exact."""
+    from spotrl.balancer import MigrationKind
+    from spotrl.domain import ProfileEntry, ProfileTable
+    m = RolloutManager(theta=64, m_b=4, log=EventLog())
+    m.n_prem_cap = 3
+    pool = TransferPool(build_agents(1, 1, 900e9))
+    run = RolloutRunner(m, pool, flush_steps=4, max_inflight=12)
+    m.begin_step(1, run.now())
+    run.stage(1, {"weights": "v1"})
+    for k in range(2):
+        assert run.add_instance(f"i{k}", FakeInstance(vocab=997, max_slots=12))
+    ps = prompts(24, seed=13)
+    for k, p in enumerate(ps):
+        run.submit(f"r{k}", p, target_len=60)
+    table = ProfileTable([ProfileEntry(1, 100.0), ProfileEntry(2, 190.0), ProfileEntry(4, 200.0)])
+    run.run(profile=table, lb_every=1, join_at={8: [("i2", FakeInstance(vocab=997, max_slots=12))]})
+    assert "i2" in m.records and m.records["i2"].status.value == "active"
+    assert any(o.kind is MigrationKind.EXECUTING and o.to_instance == "i2" for o in run.lb_orders)
+    recs = m.log.records
+    assert assert_token_conservation(recs) == 24
+    probe = FakeInstance(vocab=997)
+    for k, p in enumerate(ps):
+        assert m.requests[f"r{k}"].generated == reference_continuation(probe, p, 60)
+    run.close()
