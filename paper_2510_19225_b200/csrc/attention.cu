@@ -116,13 +116,28 @@ __device__ __forceinline__ void attn_load_item(const AttnArgs& a, int ws_idx, in
   }
 }
 
+// Byte offset of (token row, 16-byte column chunk ch) inside a K or V chunk
+// stage.  cp.async path: 256-byte rows, chunk index XOR (row & 7) (the XOR
+// stays inside a 128-byte half).  TMA path: the 128B-swizzled image of a 3D
+// box -- D/64 blocks of 16 rows x 128 bytes, 16-byte chunk index XOR
+// (row & 7) within each block (the hardware's SWIZZLE_128B pattern).  Both
+// keep ldmatrix bank-conflict free.
+template <int D, bool TMA>
+__device__ __forceinline__ uint32_t kv_off(int row, int ch) {
+  if constexpr (TMA)
+    return (ch >> 3) * (CHUNK * 128) + row * 128 + (((ch & 7) ^ (row & 7)) << 4);
+  else
+    return row * (D * 2) + ((ch ^ (row & 7)) << 4);
+}
+
 // One item: stream the window's K/V pages through the warps' cp.async rings
 // (S = QK^T, online softmax, O += PV on the tensor cores), merge the four warp
 // partials in warp order, write the row's output (or the window partial).
 // Called by every thread of the CTA (it synchronises the CTA).
-template <int D>
+template <int D, bool TMA = false>
 __device__ __forceinline__ void attn_run_item(const AttnArgs& a, int ws_idx, int kvh, int r,
-                                              const AttnItem<D>& it, uint8_t* smem) {
+                                              const AttnItem<D>& it, uint8_t* smem,
+                                              const CUtensorMap* kvmap = nullptr) {
   constexpr int ROWB = D * 2;            // bytes per token row
   constexpr int CPR = ROWB / 16;         // 16-byte chunks per row
   constexpr int KSTEPS = D / 16;
@@ -147,9 +162,36 @@ __device__ __forceinline__ void attn_run_item(const AttnArgs& a, int ws_idx, int
   const size_t head_off = static_cast<size_t>(kvh) * (2 * PAGE * D);
   const size_t page_stride = static_cast<size_t>(a.NKV) * (2 * PAGE * D);
 
+  // TMA path: one 3D box (16 token rows x D/64 swizzled 128-byte blocks) for
+  // K and one for V per chunk, issued by lane 0 and completed on the stage's
+  // mbarrier (tokens past the page's valid ones are loaded as they are --
+  // finite K/V of earlier tokens or zeros -- and masked to p = 0 exactly as
+  // the zero-filled rows of the cp.async path)
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + WARPS * WARP_SMEM) + warp * STAGES;
+  if constexpr (TMA) {
+    if (lane == 0) {
+      for (int i = 0; i < STAGES; ++i) mbar_init(smem_u32(&bars[i]), 1);
+      fence_mbar_init();
+    }
+    __syncwarp();
+  }
   auto issue = [&](int c) {
     const int seg = c >> 2;
     const int page = __shfl_sync(0xffffffffu, my_page, seg);
+    if constexpr (TMA) {
+      if (lane == 0) {
+        const uint32_t st = wsm_u32 + (c % STAGES) * STAGE_BYTES;
+        const uint32_t bar = smem_u32(&bars[c % STAGES]);
+        // generic-proxy reads of this stage (ldmatrix) precede the async write
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_expect_tx(bar, STAGE_BYTES);
+        const int64_t row = a.kv_row0 + (static_cast<int64_t>(page) * a.NKV + kvh) * (2 * PAGE) +
+                            (c & 3) * CHUNK;
+        tma_load_3d(st, kvmap, bar, static_cast<int32_t>(row), 0);
+        tma_load_3d(st + CHUNK * ROWB, kvmap, bar, static_cast<int32_t>(row + PAGE), 0);
+      }
+      return;
+    }
     const int seg_tok = min(PAGE, wn - (warp + seg * WARPS) * PAGE);   // valid tokens in the page
     const bf16* kp = a.kv + static_cast<size_t>(page) * page_stride + head_off;
     const uint32_t st = wsm_u32 + (c % STAGES) * STAGE_BYTES;
@@ -178,8 +220,12 @@ __device__ __forceinline__ void attn_run_item(const AttnArgs& a, int ws_idx, int
   }
   for (int c = 0; c < nchunks; ++c) {
     if (c + STAGES - 1 < nchunks) issue(c + STAGES - 1);
-    cp_commit();
-    cp_wait<STAGES - 1>();
+    if constexpr (TMA) {
+      mbar_wait(smem_u32(&bars[c % STAGES]), (c / STAGES) & 1);
+    } else {
+      cp_commit();
+      cp_wait<STAGES - 1>();
+    }
     __syncwarp();
     const uint32_t ks = wsm_u32 + (c % STAGES) * STAGE_BYTES;
     const uint32_t vs = ks + CHUNK * ROWB;
@@ -194,7 +240,7 @@ __device__ __forceinline__ void attn_run_item(const AttnArgs& a, int ws_idx, int
       for (int kk = 0; kk < KSTEPS; ++kk) {
         const int ch = 2 * kk + (mi & 1);
         uint32_t b[4];
-        ldsm_x4(ks + row * ROWB + ((ch ^ (row & 7)) << 4), b);
+        ldsm_x4(ks + kv_off<D, TMA>(row, ch), b);
         mma_bf16(s[0], it.qa[kk][0], it.qa[kk][1], b[0], b[1]);
         mma_bf16(s[1], it.qa[kk][0], it.qa[kk][1], b[2], b[3]);
       }
@@ -240,14 +286,14 @@ __device__ __forceinline__ void attn_run_item(const AttnArgs& a, int ws_idx, int
       for (int dt = 0; dt < NT / 2; ++dt) {
         const int ch = 2 * dt + (mi >> 1);
         uint32_t b[4];
-        ldsm_x4_t(vs + row * ROWB + ((ch ^ (row & 7)) << 4), b);
+        ldsm_x4_t(vs + kv_off<D, TMA>(row, ch), b);
         mma_bf16(o[2 * dt], pa0, pa2, b[0], b[1]);
         mma_bf16(o[2 * dt + 1], pa0, pa2, b[2], b[3]);
       }
     }
     __syncwarp();
   }
-  cp_wait<0>();
+  if constexpr (!TMA) cp_wait<0>();
   __syncthreads();
 
   // ---- merge the 4 warp partials in warp order
@@ -293,16 +339,27 @@ __device__ __forceinline__ void attn_run_item(const AttnArgs& a, int ws_idx, int
   }
 }
 
-// One CTA per (window, kv head, row).
-template <int D>
-__global__ void __launch_bounds__(WARPS * 32, ATTN_MINB) attn_mma_kernel(AttnArgs a) {
-  extern __shared__ __align__(128) uint8_t smem[];
+// One CTA per (window, kv head, row).  TMA: the K/V chunks arrive through
+// tensor-map boxes of the KV pool (`kvmap`, AttnArgs.kv_row0) instead of
+// per-lane cp.async -- the same bytes in the same order, the same bits.
+template <int D, bool TMA = false>
+__global__ void __launch_bounds__(WARPS * 32, ATTN_MINB)
+    attn_mma_kernel(AttnArgs a, const __grid_constant__ CUtensorMap kvmap) {
+  extern __shared__ __align__(128) uint8_t smem_raw[];
+  // the 128B-swizzle pattern of a TMA box is a function of the smem address:
+  // stages start on 1024-byte boundaries (the launch adds 1 KB of slack)
+  uint8_t* smem = TMA ? reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                                   ~static_cast<uintptr_t>(1023))
+                      : smem_raw;
+  if constexpr (TMA) {
+    if (threadIdx.x == 0) tma_prefetch(&kvmap);
+  }
   pdl_trigger();
   pdl_wait();   // q and this step's K/V rows come from the previous kernel
   AttnItem<D> it;
   attn_load_item<D>(a, blockIdx.x, blockIdx.y, blockIdx.z, it);
   if (it.n == 0) return;
-  attn_run_item<D>(a, blockIdx.x, blockIdx.y, blockIdx.z, it, smem);
+  attn_run_item<D, TMA>(a, blockIdx.x, blockIdx.y, blockIdx.z, it, smem, &kvmap);
 }
 
 // Prefill variant: one CTA serves two consecutive token rows (2p, 2p+1) of
@@ -621,6 +678,7 @@ static int launch_attn(const AttnArgs& a, cudaStream_t st, bool pairs) {
   constexpr int smem_pipe = WARPS * STAGES * 2 * CHUNK * D * 2;
   constexpr int smem_red = WARPS * 8 * D * 4 + WARPS * 8 * 2 * 4;
   constexpr int smem = smem_pipe > smem_red ? smem_pipe : smem_red;
+  constexpr int smem_tma = smem + WARPS * STAGES * 8 + 1024;   // + mbarriers, alignment slack
   constexpr int smem_red2 = WARPS * 16 * D * 4 + WARPS * 16 * 2 * 4 + 16 * (WARPS + 2) * 4;
   constexpr int smem_pipe2 = WARPS * ATTN_PAIR_STAGES * 2 * CHUNK * D * 2;
   constexpr int smem2 = smem_pipe2 > smem_red2 ? smem_pipe2 : smem_red2;
@@ -630,7 +688,9 @@ static int launch_attn(const AttnArgs& a, cudaStream_t st, bool pairs) {
   int dev = 0;
   RLB_CUDA(cudaGetDevice(&dev));
   if (!attr[dev & 63]) {
-    RLB_CUDA(cudaFuncSetAttribute(attn_mma_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    RLB_CUDA(cudaFuncSetAttribute(attn_mma_kernel<D, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    RLB_CUDA(cudaFuncSetAttribute(attn_mma_kernel<D, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  smem_tma));
     RLB_CUDA(cudaFuncSetAttribute(attn_pair_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   smem2));
     RLB_CUDA(cudaFuncSetAttribute(attn_pair_kernel<D, 2>,
@@ -650,9 +710,13 @@ static int launch_attn(const AttnArgs& a, cudaStream_t st, bool pairs) {
   } else if (pairs) {
     RLB_CUDA(launch_k(attn_pair_kernel<D>, dim3(a.max_splits, a.NKV, (a.R + 1) / 2),
                       dim3(WARPS * 32), smem2, st, a));
+  } else if (a.kv_map) {
+    RLB_CUDA(launch_k(attn_mma_kernel<D, true>, dim3(a.max_splits, a.NKV, a.R), dim3(WARPS * 32),
+                      smem_tma, st, a, *a.kv_map));
   } else {
-    RLB_CUDA(launch_k(attn_mma_kernel<D>, dim3(a.max_splits, a.NKV, a.R), dim3(WARPS * 32), smem,
-                      st, a));
+    CUtensorMap none{};
+    RLB_CUDA(launch_k(attn_mma_kernel<D, false>, dim3(a.max_splits, a.NKV, a.R), dim3(WARPS * 32),
+                      smem, st, a, none));
   }
   return RLB_OK;
 }

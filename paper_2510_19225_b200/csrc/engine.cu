@@ -224,6 +224,11 @@ struct rlb_instance {
   // prefill row pairs split by context length (short: <= 2 pages, 2-warp
   // attention CTAs); set per chunk by admit_and_prefill (RLB_ATTN_SPLIT=0: off)
   int* d_pairs = nullptr;
+  // decode attention K/V through TMA boxes of the whole pool (RLB_ATTN_TMA=0
+  // at instance creation: per-lane cp.async -- the same bits, the A/B
+  // reference of tests/test_gpu_engine.py)
+  bool attn_tma = true;
+  CUtensorMap kv_map{};
   std::vector<int> h_pairs;
   int pairs_short = 0, pairs_long = 0;
   bool attn_split = true;
@@ -518,6 +523,7 @@ int rlb_instance::init() {
   if (const char* ov = std::getenv("RLB_QKV_BN")) bn_qkv_decode = std::atoi(ov) == 128 ? 128 : 64;
   if (const char* ov = std::getenv("RLB_ATTN_PAIRS")) attn_pairs = std::atoi(ov) != 0;
   if (const char* ov = std::getenv("RLB_ATTN_SPLIT")) attn_split = std::atoi(ov) != 0;
+  if (const char* ov = std::getenv("RLB_ATTN_TMA")) attn_tma = std::atoi(ov) != 0;
   if (const char* ov = std::getenv("RLB_QKV_KPS")) qkv_kps2 = std::atoi(ov) == 2;
   if (const char* ov = std::getenv("RLB_O_KPS")) o_kps2 = std::atoi(ov) == 2;
   if (const char* ov = std::getenv("RLB_SMALL_GU_WAVE")) small_gu_wave = std::atoi(ov) != 0;
@@ -561,6 +567,9 @@ int rlb_instance::init() {
   // zeroed once: pages never written read as zeros (bytewise KV comparisons,
   // compute-sanitizer initcheck)
   RLB_CUDA(cudaMemset(kv, 0, layer_stride * m.layers * sizeof(bf16)));
+  if (attn_tma &&
+      (rc = make_kv_map(&kv_map, kv, static_cast<int64_t>(layer_stride / D) * m.layers, D)))
+    return rc;
   if ((rc = dalloc(&d_bt, static_cast<size_t>(max_slots) * pps))) return rc;
   h_bt.assign(static_cast<size_t>(max_slots) * pps, 0);
   RLB_CUDA(cudaMemset(d_bt, 0, sizeof(int) * h_bt.size()));
@@ -706,6 +715,10 @@ int rlb_instance::forward_layers(int R, bool prefill) {
     if ((rc = qkv_launch(tp, w, pq))) return rc;
     AttnArgs a{d_q, NQ * D, kv_l, d_bt, pps, d_row_slot, d_row_pos, R, NQ, NKV, D, max_splits,
                d_ws, d_attn, NQ * D};
+    if (!prefill && attn_tma) {
+      a.kv_map = &kv_map;
+      a.kv_row0 = static_cast<int64_t>(layer_stride / D) * l;
+    }
     if (prefill && attn_pairs && attn_split && pairs_short + pairs_long > 0) {
       a.pair_ids = d_pairs;
       a.n_short = pairs_short;
@@ -1439,6 +1452,7 @@ int rlb_profile_kernel(rlb_instance* h, int32_t which, int32_t iters, double* av
       case 0: {
         AttnArgs a{h->d_q, NQ * D, h->kv, h->d_bt, h->pps, h->d_row_slot, h->d_row_pos, R, NQ,
                    h->NKV, D, h->max_splits, h->d_ws, h->d_attn, NQ * D};
+        if (h->attn_tma) a.kv_map = &h->kv_map;     // layer 0: kv_row0 = 0
         return attention_launch(a, h->st);
       }
       // projections with their fused epilogues, outputs to scratch where the

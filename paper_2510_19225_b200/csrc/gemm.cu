@@ -1055,6 +1055,12 @@ int make_kmajor_map(CUtensorMap* map, const void* ptr, int64_t rows, int64_t k, 
   return RLB_OK;
 }
 
+int make_kv_map(CUtensorMap* map, const void* kv, int64_t rows, int head_dim) {
+  RLB_CHECK(head_dim % BK == 0 && rows < (int64_t{1} << 31), RLB_ERR_ARG,
+            "KV map: head_dim multiple of 64, < 2^31 rows");
+  return make_kmajor_map3(map, kv, rows, head_dim, 16, head_dim / BK);
+}
+
 // 3D view of a K-major [rows, k] bf16 matrix: (64 elements, rows, k / 64
 // K blocks), boxes of box_rows rows x kps K blocks (gemm_bf16_tc<..., KPS>)
 int make_kmajor_map3(CUtensorMap* map, const void* ptr, int64_t rows, int64_t k, int box_rows,

@@ -46,6 +46,9 @@ int gemm_launch(const CUtensorMap& a, const CUtensorMap& b, int block_n, int epi
                 int kps = 1);
 int make_kmajor_map3(CUtensorMap* map, const void* ptr, int64_t rows, int64_t k, int box_rows,
                      int kps);
+// The KV pool as rows of head_dim bf16 ([layer][page][kv head][K|V][64 tok])
+// in 16-token x head_dim boxes (3D, 128B swizzle) for the decode attention
+int make_kv_map(CUtensorMap* map, const void* kv, int64_t rows, int head_dim);
 int gemm_launch_pairp(const CUtensorMap& a, const CUtensorMap& b128, int epi, const GemmParams& p,
                       cudaStream_t st);
 
@@ -63,6 +66,10 @@ struct AttnArgs {
   // pair_ids[n_short, n_short + n_long) the rest; null = every pair, 4 warps
   const int* pair_ids = nullptr;
   int n_short = 0, n_long = 0;
+  // decode K/V loads through TMA: a 3D tensor map over the whole KV pool
+  // (make_kv_map) and this layer's first row in it; null = cp.async
+  const CUtensorMap* kv_map = nullptr;
+  int64_t kv_row0 = 0;
 };
 int attention_launch(const AttnArgs& a, cudaStream_t st, bool row_pairs = false);
 int attention_windows(int max_seq);   // CTA windows per row (AttnArgs.max_splits)

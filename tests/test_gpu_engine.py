@@ -395,3 +395,40 @@ def _kv_bytes(inst):
     _lib.check(_lib.lib().rlb_copy_bytes(0, buf.data_ptr(), p, n, None))
     torch.cuda.synchronize()
     return buf
+
+
+def _kv_bytes(inst):
+    from paper_2510_19225_b200 import _lib
+    p, n = inst.kv_pool()
+    buf = torch.empty(n, dtype=torch.uint8, device="cuda")
+    _lib.check(_lib.lib().rlb_copy_bytes(0, buf.data_ptr(), p, n, None))
+    torch.cuda.synchronize()
+    return buf
+
+
+@pytest.mark.parametrize("case", ["mid-3", "mid-300", "tiny-long"])
+def test_attention_tma_same_bits(request, monkeypatch, case):
+    """Decode attention with K/V chunks through TMA boxes of the KV pool
+    against the per-lane cp.async loads (RLB_ATTN_TMA=0): after the same
+    rollout the whole paged KV pool is bytewise identical (every later
+    layer's K/V depends on each earlier attention output) and so are the
+    tokens.  Covers 1..300 rows, head_dim 128 and 64, multi-window rows."""
+    if case.startswith("mid"):
+        shape, w, _ = request.getfixturevalue("mid")
+        n = int(case.split("-")[1])
+        prompts = synth_prompts(n, shape.vocab, 60, 384, seed=29)
+        kw, new = dict(max_slots=512, max_seq_len=512), 40
+    else:
+        w, _ = request.getfixturevalue("tiny")
+        shape = TINY
+        prompts = synth_prompts(3, TINY.vocab, 2000, 2300, seed=31)
+        kw, new = dict(max_slots=4, max_seq_len=2560, max_prefill_rows=1024), 120
+    out = {}
+    for flag in ("0", "1"):
+        monkeypatch.setenv("RLB_ATTN_TMA", flag)
+        inst = _instance(shape, w, **kw)
+        toks = _rollout(inst, prompts, new)
+        out[flag] = (toks, _kv_bytes(inst))
+        inst.close()
+    assert out["0"][0] == out["1"][0]
+    assert torch.equal(out["0"][1], out["1"][1])
