@@ -22,9 +22,10 @@ class FakePull:
 
 
 class FakeInstance:
-    def __init__(self, vocab: int = 1000, max_slots: int = 8):
+    def __init__(self, vocab: int = 1000, max_slots: int = 8, plan: str | None = None):
         self.vocab = vocab
         self.max_slots = max_slots
+        self.plan = plan            # numerics plan (RolloutInstance.plan); None = not reported
         self.pending: list[str] = []
         self.active: dict[str, dict] = {}
         self.version = 0
@@ -111,8 +112,11 @@ class FakeInstance:
         return [(list(self.active[r]["prompt"]), list(self.active[r]["gen"])) for r in request_ids]
 
     def status(self):
-        return {"m_pending": len(self.pending), "m_exec": len(self.active) - len(self.pending),
-                "weight_version": self.version}
+        st = {"m_pending": len(self.pending), "m_exec": len(self.active) - len(self.pending),
+              "weight_version": self.version}
+        if self.plan is not None:
+            st["plan"] = self.plan
+        return st
 
     def close(self):
         self.closed = True

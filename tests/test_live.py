@@ -73,3 +73,35 @@ def test_agent_pull_frames():
         f.flush()
         assert list(read_frames(f)) == []
     agent.close()
+
+
+def test_live_refuses_a_mismatched_numerics_plan():
+    """An instance whose numerics plan differs from the first one's is
+    refused (its connection closed -> handled as a preemption): a request
+    resumed across plans would not continue bit-exactly."""
+    m = RolloutManager(theta=3, m_b=4, log=EventLog())
+    m.n_prem_cap = 3
+    m.begin_step(1, 0.0)
+    srv = ManagerServer(m, version=1, endpoint_for=lambda iid: f"fake://{iid}", max_inflight=4)
+    prompts = _prompts(8)
+    for k, p in enumerate(prompts):
+        srv.submit(f"r{k}", p, 10)
+    stop = threading.Event()
+    for k, plan in enumerate(["v1.q1.o3.d5.w2048.p64.t0", "v1.q1.o2.d5.w2048.p64.t0"]):
+        inst = FakeInstance(vocab=997, max_slots=4, plan=plan)
+        t = threading.Thread(target=serve_instance, args=(srv.address, inst, f"i{k}"),
+                             kwargs=dict(open_endpoint=lambda ep, v: ep, n_steps=3, stop=stop),
+                             daemon=True)
+        t.start()
+        if k == 0:
+            import time
+            time.sleep(0.3)                 # i0 reports its plan first
+    srv.run_until_done(timeout=60)
+    stop.set()
+    srv.close()
+    recs = m.log.records
+    assert [r["instance_id"] for r in recs if r["type"] == "plan_mismatch"] == ["i1"]
+    assert assert_token_conservation(recs) == 8
+    probe = FakeInstance(vocab=997)
+    for k, p in enumerate(prompts):
+        assert m.requests[f"r{k}"].generated == reference_continuation(probe, p, 10)
