@@ -53,6 +53,9 @@ def main():
     ap.add_argument("--lb-every", type=int, default=2)
     ap.add_argument("--epsilon", type=float, default=0.05)
     ap.add_argument("--shape", default="qwen2.5-7b")
+    ap.add_argument("--profile", choices=["calibrate", "online"], default="calibrate",
+                    help="plateau from a calibration sweep at one context (default) or from the "
+                         "static run's online decode profile")
     ap.add_argument("--late-join", type=int, default=0,
                     help="the last instance registers after this many decode steps (a spot "
                          "instance arriving mid-step; 0 = all from the start)")
@@ -67,7 +70,7 @@ def main():
     from oracle.audit import assert_token_conservation, assert_version_gating
     from paper_2510_19225_b200 import _lib
     from paper_2510_19225_b200.instance import RolloutInstance
-    from paper_2510_19225_b200.profile import measured_profile_table
+    from paper_2510_19225_b200.profile import calibrate_profile, measured_profile_table
     from paper_2510_19225_b200.runner import RolloutRunner
     from paper_2510_19225_b200.shapes import SHAPES
     from paper_2510_19225_b200.synth import synth_hf_weights, synth_prompts
@@ -136,7 +139,14 @@ def main():
     if not args.no_warmup:
         run_once("w", None)
     static, got_static, points = run_once("s", None)
-    table = measured_profile_table(points)
+    online = measured_profile_table(points)
+    if args.profile == "calibrate":
+        # every batch size at one context (the instances are idle between runs)
+        sizes = [b for b in (1, 2, 4, 8, 16, 32, 48, 64, 96, 128, 160, 192, 224, 256, 320, 384,
+                             448, 512) if b <= args.max_inflight]
+        table = calibrate_profile(instances[ids[0]], sizes, prompt_len=256, steps=32)
+    else:
+        table = online
     plateau = estimate_plateau(table, table.context_calibration, epsilon=args.epsilon)
     rebal, got_rebal, _ = run_once("b", table)
     same = [r for r in got_static if got_static[r] == got_rebal[r]]
@@ -153,7 +163,10 @@ def main():
                       "target_len_max": max(targets)},
            "static": static, "rebalanced": rebal,
            "speedup": static["wall_s"] / rebal["wall_s"],
-           "profile": {"entries": [[e.batch_size, round(e.decode_throughput, 1)]
+           "profile": {"source": args.profile,
+                       "online_entries": [[e.batch_size, round(e.decode_throughput, 1)]
+                                          for e in online.entries],
+                       "entries": [[e.batch_size, round(e.decode_throughput, 1)]
                                    for e in table.entries],
                        "context_calibration": table.context_calibration,
                        "plateau": plateau, "epsilon": args.epsilon},

@@ -409,6 +409,15 @@ struct rlb_instance {
   int run_decode(int steps, int* steps_run);
   int flush(rlb_token_batch* out);
   int upload_slots();
+  bool gs_enabled() const { return e.graph_steps > 0; }
+  // decode batch buckets: exact up to 16 rows, then multiples of 16 / 32 / 64
+  int decode_bucket(int R) const {
+    int b = R;
+    if (R > 512) b = (R + 63) / 64 * 64;
+    else if (R > 128) b = (R + 31) / 32 * 32;
+    else if (R > 16) b = (R + 15) / 16 * 16;
+    return std::min(b, (max_slots + 127) / 128 * 128);
+  }
   void release(Req* r);
   // row pairs (2p, 2p+1) of a prefill chunk (positions pos[0..n)): those
   // whose rows all see <= 2 pages of context first (2-warp attention CTAs),
@@ -608,24 +617,36 @@ int rlb_instance::init() {
   if (attn_tma &&
       (rc = make_kv_map(&kv_map, kv, static_cast<int64_t>(layer_stride / D) * m.layers, D)))
     return rc;
-  if ((rc = dalloc(&d_bt, static_cast<size_t>(max_slots) * pps))) return rc;
+  // + one scratch slot (index max_slots): the padding rows of bucketed decode
+  // batches -- length 1, target 1, so it never appends; its one page is
+  // reserved from the pool
+  if ((rc = dalloc(&d_bt, static_cast<size_t>(max_slots + 1) * pps))) return rc;
   h_bt.assign(static_cast<size_t>(max_slots) * pps, 0);
   RLB_CUDA(cudaMemset(d_bt, 0, sizeof(int) * h_bt.size()));
-  free_pages.resize(num_pages);
-  for (int i = 0; i < num_pages; ++i) free_pages[i] = num_pages - 1 - i;
-  if ((rc = dalloc(&d_seq_tokens, static_cast<size_t>(max_slots) * max_seq))) return rc;
-  if ((rc = dalloc(&d_seq_len, max_slots))) return rc;
-  if ((rc = dalloc(&d_seq_target, max_slots))) return rc;
+  RLB_CHECK(num_pages >= 2, RLB_ERR_ARG, "KV pool needs at least 2 pages");
+  free_pages.resize(num_pages - 1);                    // page num_pages-1: the scratch slot's
+  for (int i = 0; i < num_pages - 1; ++i) free_pages[i] = num_pages - 2 - i;
+  if ((rc = dalloc(&d_seq_tokens, static_cast<size_t>(max_slots + 1) * max_seq))) return rc;
+  if ((rc = dalloc(&d_seq_len, max_slots + 1))) return rc;
+  if ((rc = dalloc(&d_seq_target, max_slots + 1))) return rc;
   h_seq_len.assign(max_slots, 1);
   h_seq_target.assign(max_slots, 0);
   slot_req.assign(max_slots, nullptr);
   for (int s = max_slots - 1; s >= 0; --s) free_slots.push_back(s);
-  RLB_CUDA(cudaMemset(d_seq_tokens, 0, sizeof(int32_t) * max_slots * static_cast<size_t>(max_seq)));
+  RLB_CUDA(cudaMemset(d_seq_tokens, 0, sizeof(int32_t) * (max_slots + 1) * static_cast<size_t>(max_seq)));
+  {
+    const int32_t one = 1, scratch_page = num_pages - 1;
+    RLB_CUDA(cudaMemcpy(d_seq_len + max_slots, &one, sizeof(int32_t), cudaMemcpyHostToDevice));
+    RLB_CUDA(cudaMemcpy(d_seq_target + max_slots, &one, sizeof(int32_t), cudaMemcpyHostToDevice));
+    RLB_CUDA(cudaMemset(d_bt + static_cast<size_t>(max_slots) * pps, 0, sizeof(int) * pps));
+    RLB_CUDA(cudaMemcpy(d_bt + static_cast<size_t>(max_slots) * pps, &scratch_page, sizeof(int),
+                        cudaMemcpyHostToDevice));
+  }
 
   const size_t R = max_rows;
   if ((rc = dalloc(&d_row_tok, R)) || (rc = dalloc(&d_row_pos, R)) || (rc = dalloc(&d_row_slot, R)) ||
       (rc = dalloc(&d_logit_src, R)) || (rc = dalloc(&d_logit_slot, R)) ||
-      (rc = dalloc(&d_dec_slots, max_slots)))
+      (rc = dalloc(&d_dec_slots, max_rows)))
     return rc;
   if ((rc = dalloc(&d_h, R * H)) || (rc = dalloc(&d_xn, R * H)) || (rc = dalloc(&d_qkv, R * QKV)) ||
       (rc = dalloc(&d_q, R * NQ * D)) || (rc = dalloc(&d_attn, R * NQ * D)) ||
@@ -992,28 +1013,38 @@ int rlb_instance::run_decode(int steps, int* steps_run) {
         min_left = std::min(min_left, h_seq_target[s] - h_seq_len[s]);
       }
     }
-    const int R = static_cast<int>(dec_list.size());
-    if (R == 0) break;
+    const int Rreal = static_cast<int>(dec_list.size());
+    if (Rreal == 0) break;
     // longest contexts first: the attention grid dispatches rows in order, so
     // the long rows start in the first wave and the last wave is short rows
     // (every row's arithmetic is independent of its position in the batch)
     if (sort_rows)
       std::stable_sort(dec_list.begin(), dec_list.end(),
                        [&](int x, int y) { return h_seq_len[x] > h_seq_len[y]; });
+    // bucketed batch: padding rows of the scratch slot (never append, same
+    // bits for the real rows) so a shrinking long-tail batch reuses a few
+    // captured graphs instead of capturing one per batch size
+    const int R = gs_enabled() ? decode_bucket(Rreal) : Rreal;
+    dec_list.resize(R, max_slots);
     RLB_CUDA(cudaMemcpyAsync(d_dec_slots, dec_list.data(), R * sizeof(int), cudaMemcpyHostToDevice, st));
     stats.h2d_bytes += static_cast<int64_t>(R) * 4;
     last_R = R;
-    int burst = std::min(steps - *steps_run, min_left);
     const int gs = e.graph_steps;
+    // with graphs, a burst runs whole graphs up to the first row's target
+    // rounded up: a row at its target recomputes its last position (identical
+    // K/V bits) and never appends (argmax_append checks the target) for the
+    // rest of that graph, instead of the burst dropping to eager launches
+    int burst = std::min(steps - *steps_run,
+                         gs > 0 ? (min_left + gs - 1) / gs * gs : min_left);
     const int64_t per_step = 1 + launches_per_forward(R);
     double ctx0 = 0.0;
-    for (int s : dec_list) ctx0 += h_seq_len[s];
-    Burst rec{R, burst, ctx0 / R + 0.5 * (burst - 1), 0, 0};
+    for (int i = 0; i < Rreal; ++i) ctx0 += h_seq_len[dec_list[i]];
+    Burst rec{Rreal, burst, ctx0 / Rreal + 0.5 * (burst - 1), 0, 0};
     if ((rc = burst_event(&rec.e0))) return rc;
     while (burst > 0) {
       const int k = (gs > 0 && burst >= gs) ? gs : 1;
       stats.decode_steps += k;
-      stats.decode_rows += static_cast<int64_t>(k) * R;
+      stats.decode_rows += static_cast<int64_t>(k) * Rreal;
       stats.kernel_launches += k * per_step;
       if (gs > 0 && burst >= gs) {
         const auto gkey = std::make_pair(R, static_cast<const uint8_t*>(arena));
@@ -1035,12 +1066,18 @@ int rlb_instance::run_decode(int steps, int* steps_run) {
         RLB_CUDA(cudaGraphLaunch(it->second, st));
         burst -= gs;
         *steps_run += gs;
-        for (int s : dec_list) h_seq_len[s] += gs;
+        for (int i = 0; i < Rreal; ++i) {
+          const int sl = dec_list[i];
+          h_seq_len[sl] = std::min(h_seq_len[sl] + gs, h_seq_target[sl]);
+        }
       } else {
         if ((rc = decode_step_launch(R))) return rc;
         burst -= 1;
         *steps_run += 1;
-        for (int s : dec_list) h_seq_len[s] += 1;
+        for (int i = 0; i < Rreal; ++i) {
+          const int sl = dec_list[i];
+          h_seq_len[sl] = std::min(h_seq_len[sl] + 1, h_seq_target[sl]);
+        }
       }
     }
     if ((rc = burst_event(&rec.e1))) return rc;

@@ -33,3 +33,30 @@ def measured_profile_table(points: Iterable[tuple[int, int, float, float]]) -> P
         ctx_n += steps
     entries = [ProfileEntry(b, b * s / t) for b, (s, t) in sorted(acc.items())]
     return ProfileTable(entries=entries, context_calibration=ctx_w / ctx_n if ctx_n else 0.0)
+
+
+def calibrate_profile(instance, batch_sizes: Iterable[int], *, prompt_len: int = 256,
+                      steps: int = 32, seed: int = 0) -> ProfileTable:
+    """Measure the batch-size -> decode-throughput curve of an idle instance
+    at one context: for each batch size b, b throwaway requests (seeded
+    synthetic prompts of `prompt_len` ids) decode `steps` tokens together and
+    the device time of their constant-batch bursts is taken from
+    `decode_profile()`.  Every point shares the context, so the reference's
+    plateau rule compares like with like -- an online capture during a
+    long-tail step (the reference's `profile_prev`, `sim/engine.py:928-939`)
+    sees small batches only late, at long contexts, which bends the curve.
+    The instance must hold weights and no requests; it is left idle."""
+    import random
+    rng = random.Random(seed)
+    vocab = instance.shape.vocab
+    points = []
+    for b in sorted(set(int(x) for x in batch_sizes)):
+        if b <= 0:
+            continue
+        instance.decode_profile(reset=True)
+        for i in range(b):
+            instance.generate(f"__calib{b}_{i}", [rng.randrange(vocab) for _ in range(prompt_len)],
+                              target_len=steps + 1)
+        instance.run_to_completion(steps)
+        points.extend(p for p in instance.decode_profile(reset=True) if p[0] == b)
+    return measured_profile_table(points)

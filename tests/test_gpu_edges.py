@@ -116,11 +116,12 @@ def test_limits_raise(tiny):
 
 
 def test_queueing_on_slots_and_pages_is_invisible(tiny):
-    """40 requests on 6 slots, and on a KV pool of 9 pages: every request's
-    tokens equal those of a run with room for all of them at once."""
+    """40 requests on 6 slots, and on a KV pool of 9 usable pages (+1 the
+    scratch slot of bucketed decode batches reserves): every request's tokens
+    equal those of a run with room for all of them at once."""
     w, _ = tiny
     prompts = synth_prompts(40, TINY.vocab, 8, 120, seed=31)
     ref = _gen(_inst(w, max_slots=40, max_seq_len=256), prompts, 70)
     assert _gen(_inst(w, max_slots=6, max_seq_len=256), prompts, 70, n_steps=9) == ref
     # each request needs ceil((prompt + 70) / 64) <= 3 pages: at most 3 run at once
-    assert _gen(_inst(w, max_slots=16, max_seq_len=256, num_pages=9), prompts, 70) == ref
+    assert _gen(_inst(w, max_slots=16, max_seq_len=256, num_pages=10), prompts, 70) == ref

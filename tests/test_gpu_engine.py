@@ -460,3 +460,27 @@ def test_prefill_groups_same_bits(request, monkeypatch, case):
     assert np.array_equal(out["0"][0].view(np.uint32), out["1"][0].view(np.uint32))
     assert out["0"][1] == out["1"][1]
     assert torch.equal(out["0"][2], out["1"][2])
+
+
+def test_bucketed_decode_batches_same_tokens(tiny):
+    """A long-tail batch (targets 20..200) decodes on bucketed batch sizes
+    padded with scratch-slot rows and whole graphs past a row's target; every
+    request's tokens equal a one-request-at-a-time rollout, and the captured
+    graphs stay few."""
+    w, _ = tiny
+    prompts = synth_prompts(40, TINY.vocab, 8, 90, seed=43)
+    import random
+    rng = random.Random(3)
+    targets = [rng.randint(20, 200) for _ in prompts]
+    inst = _instance(TINY, w, max_slots=40, max_seq_len=320, graph_steps=8)
+    for i, p in enumerate(prompts):
+        inst.generate(f"r{i}", p, target_len=targets[i])
+    got = inst.run_to_completion(24)
+    sizes = {b for b, _, _, _ in inst.decode_profile()}
+    inst.close()
+    solo = _instance(TINY, w, max_slots=1, max_seq_len=320, graph_steps=0)
+    for i, p in enumerate(prompts[:8]):
+        solo.generate(f"s{i}", p, target_len=targets[i])
+        assert solo.run_to_completion(32)[f"s{i}"] == got[f"r{i}"]
+    assert all(len(got[f"r{i}"]) == targets[i] for i in range(len(prompts)))
+    assert len(sizes) > 10          # many real batch sizes ...

@@ -20,3 +20,34 @@ def test_measured_table_feeds_reference_plateau():
            for b in (1, 64, 128, 256, 384, 512)]
     t = measured_profile_table(pts)
     assert estimate_plateau(t, t.context_calibration) == 256
+
+
+def test_calibrate_profile_on_fake_instance():
+    """The calibration sweep submits b throwaway requests per batch size,
+    runs them and keeps the bursts of exactly b rows."""
+    from paper_2510_19225_b200.profile import calibrate_profile
+
+    class Inst:
+        shape = type("S", (), {"vocab": 50})()
+
+        def __init__(self):
+            self.pending = []
+            self.done = []
+
+        def decode_profile(self, reset=False):
+            out = [(len(self.done), 32, 1e-3 * (1 + 0.01 * len(self.done)), 270.0),
+                   (1, 1, 1.0, 270.0)] if self.done else []
+            if reset:
+                self.done = []
+            return out
+
+        def generate(self, rid, prompt, target_len):
+            assert len(prompt) == 256 and target_len == 33 and rid.startswith("__calib")
+            self.pending.append(rid)
+
+        def run_to_completion(self, n):
+            self.done, self.pending = self.pending, []
+
+    t = calibrate_profile(Inst(), [4, 1, 2, 4])
+    assert [e.batch_size for e in t.entries] == [1, 2, 4]
+    assert t.entries[2].decode_throughput == pytest.approx(4 * 32 / (1e-3 * 1.04))
