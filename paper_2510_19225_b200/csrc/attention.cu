@@ -385,9 +385,6 @@ __device__ __forceinline__ void mma_bf16_full(float (&d)[4], uint32_t a0, uint32
 #ifndef ATTN_PAIR_MINB
 #define ATTN_PAIR_MINB 3
 #endif
-#ifndef ATTN_GROUP
-#define ATTN_GROUP 3           // row pairs per prefill group CTA (K1g): 12 warps
-#endif
 // NW = 2: the short-pair variant -- rows with <= 2 pages of context only
 // have pages in warp slots 0 and 1, so two physical warps do all the work and
 // slots 2, 3 enter the merge as the empty partials (m = -inf, l = 0, o = 0)
@@ -652,252 +649,6 @@ __global__ void __launch_bounds__(NW * 32, NW == WARPS ? ATTN_PAIR_MINB : 2 * AT
   }
 }
 
-// K1g: prefill rows in groups of NP consecutive row pairs of one sequence.
-// attn_pair_kernel loads every K/V chunk once per pair, so a prefill chunk
-// of 16k rows streams each sequence's causal prefix ~8k times from L2 (the
-// r1 ncu: L2/issue bound, 445 us per chunk and layer).  Here the 4*NP warps
-// of a CTA are (page role w = warp % 4) x (pair pg = warp / 4): the NP warps
-// of a role stream the SAME chunk sequence -- the role's pages up to the
-// group's last row -- loading each chunk cooperatively into one shared
-// stage (a named barrier per role per chunk), and each computes its own
-// pair exactly as attn_pair_kernel does: the decode kernel's chunk order,
-// masking, online softmax and warp-order merge per row, with no update on
-// chunks that hold none of the row's positions.  Same bits, NP x fewer
-// K/V loads.
-template <int D, int NP>
-__global__ void __launch_bounds__(NP * WARPS * 32, 1) attn_group_kernel(AttnArgs a) {
-  constexpr int STAGES = 3;
-  constexpr int ROWB = D * 2;
-  constexpr int CPR = ROWB / 16;
-  constexpr int KSTEPS = D / 16;
-  constexpr int NT = D / 8;
-  constexpr int STAGE_BYTES = 2 * CHUNK * ROWB;
-  constexpr int ROLE_SMEM = STAGES * STAGE_BYTES;
-  constexpr int PIECES = CHUNK * CPR;                         // 16-byte pieces of a K (or V) chunk
-  extern __shared__ __align__(128) uint8_t smem[];
-
-  const int ws_idx = blockIdx.x, kvh = blockIdx.y;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int role = warp % WARPS, pg = warp / WARPS;
-  const int G = a.NQ / a.NKV;
-  pdl_trigger();
-  pdl_wait();
-  const int rG = a.group_ids[blockIdx.z];                     // first row of the group
-  const int r0 = rG + 2 * pg;                                 // this warp's pair: rows r0, r0 + 1
-  const float scale = rsqrtf(static_cast<float>(D)) * 1.4426950408889634f;
-  const int w0 = ws_idx * SUPER;
-  const int h = lane >> 2;
-  const int n0 = a.row_pos[r0] + 1, n1 = a.row_pos[r0 + 1] + 1;
-  const int wn0 = min(SUPER, n0 - w0), wn1 = min(SUPER, n1 - w0);
-  // the role's chunk sequence runs to the group's last row (the longest)
-  const int wnG = min(SUPER, a.row_pos[rG + 2 * NP - 1] + 1 - w0);
-  if (wnG <= 0) return;                                       // uniform over the CTA
-
-  uint32_t qa[KSTEPS][4];
-  {
-    const bf16* q0 = a.q + static_cast<size_t>(r0) * a.ldq + static_cast<size_t>(kvh * G + h) * D;
-    const bf16* q1 = q0 + a.ldq;
-#pragma unroll
-    for (int kk = 0; kk < KSTEPS; ++kk) {
-      const int c = kk * 16 + 2 * (lane & 3);
-      qa[kk][0] = h < G && wn0 > 0 ? *reinterpret_cast<const uint32_t*>(q0 + c) : 0u;
-      qa[kk][2] = h < G && wn0 > 0 ? *reinterpret_cast<const uint32_t*>(q0 + c + 8) : 0u;
-      qa[kk][1] = h < G && wn1 > 0 ? *reinterpret_cast<const uint32_t*>(q1 + c) : 0u;
-      qa[kk][3] = h < G && wn1 > 0 ? *reinterpret_cast<const uint32_t*>(q1 + c + 8) : 0u;
-    }
-  }
-  const int npages = (wnG + PAGE - 1) / PAGE;
-  const int nseg = npages > role ? (npages - role + WARPS - 1) / WARPS : 0;
-  int my_page = 0;
-  if (lane < nseg) {
-    const int pgi = w0 / PAGE + role + lane * WARPS;
-    my_page = a.block_table[static_cast<size_t>(a.row_slot[rG]) * a.bt_stride + pgi];
-  }
-  const int last_seg_tokens = nseg > 0 ? min(PAGE, wnG - (role + (nseg - 1) * WARPS) * PAGE) : 0;
-  const int nchunks = nseg > 0 ? (nseg - 1) * (PAGE / CHUNK) + (last_seg_tokens + CHUNK - 1) / CHUNK : 0;
-  const uint32_t rsm_u32 = smem_u32(smem + role * ROLE_SMEM);
-  const size_t head_off = static_cast<size_t>(kvh) * (2 * PAGE * D);
-  const size_t page_stride = static_cast<size_t>(a.NKV) * (2 * PAGE * D);
-  auto issue = [&](int c) {          // this warp's share of chunk c of the role
-    const int seg = c >> 2;
-    const int page = __shfl_sync(0xffffffffu, my_page, seg);
-    const int seg_tok = min(PAGE, wnG - (role + seg * WARPS) * PAGE);
-    const bf16* kp = a.kv + static_cast<size_t>(page) * page_stride + head_off;
-    const uint32_t st = rsm_u32 + (c % STAGES) * STAGE_BYTES;
-#pragma unroll
-    for (int i = 0; i < (PIECES + 32 * NP - 1) / (32 * NP); ++i) {
-      const int idx = (i * NP + pg) * 32 + lane;
-      if (idx < PIECES) {
-        const int row = idx / CPR, ch = idx % CPR;
-        const int tok = (c & 3) * CHUNK + row;
-        const bool ok = tok < seg_tok;
-        const bf16* src = kp + static_cast<size_t>(ok ? tok : 0) * D + ch * 8;
-        const uint32_t off = row * ROWB + ((ch ^ (row & 7)) << 4);
-        cp_async16(st + off, src, ok);
-        cp_async16(st + CHUNK * ROWB + off, src + PAGE * D, ok);
-      }
-    }
-  };
-  auto role_sync = [&]() {
-    asm volatile("bar.sync %0, %1;" ::"r"(1 + role), "r"(NP * 32) : "memory");
-  };
-
-  float o[NT][4];
-#pragma unroll
-  for (int t = 0; t < NT; ++t) o[t][0] = o[t][1] = o[t][2] = o[t][3] = 0.f;
-  float m_run[2] = {-INFINITY, -INFINITY}, l_run[2] = {0.f, 0.f};
-#pragma unroll
-  for (int c = 0; c < STAGES - 1; ++c) {
-    if (c < nchunks) issue(c);
-    cp_commit();
-  }
-  for (int c = 0; c < nchunks; ++c) {
-    cp_wait<STAGES - 2>();           // this warp's pieces of chunk c
-    role_sync();                     // every piece of chunk c; chunk c-1 consumed by the role
-    if (c + STAGES - 1 < nchunks) issue(c + STAGES - 1);
-    cp_commit();
-    const uint32_t ks = rsm_u32 + (c % STAGES) * STAGE_BYTES;
-    const uint32_t vs = ks + CHUNK * ROWB;
-    const int pstart = (role + (c >> 2) * WARPS) * PAGE;
-    const int tok0 = (c & 3) * CHUNK;
-    float s[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
-    {
-      const int mi = lane >> 3, ri = lane & 7;
-      const int row = (mi >> 1) * 8 + ri;
-#pragma unroll
-      for (int kk = 0; kk < KSTEPS; ++kk) {
-        const int ch = 2 * kk + (mi & 1);
-        uint32_t b[4];
-        ldsm_x4(ks + row * ROWB + ((ch ^ (row & 7)) << 4), b);
-        mma_bf16_full(s[0], qa[kk][0], qa[kk][1], qa[kk][2], qa[kk][3], b[0], b[1]);
-        mma_bf16_full(s[1], qa[kk][0], qa[kk][1], qa[kk][2], qa[kk][3], b[2], b[3]);
-      }
-    }
-    uint32_t pa[2][2];
-    float corr[2];
-#pragma unroll
-    for (int x = 0; x < 2; ++x) {
-      const int wnx = x == 0 ? wn0 : wn1;
-      const int seg_tok = min(PAGE, wnx - pstart);
-      const bool active = pstart + tok0 < wnx;
-      float mx = -INFINITY;
-#pragma unroll
-      for (int j = 0; j < 2; ++j)
-#pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          const int tok = tok0 + 8 * j + 2 * (lane & 3) + e;
-          s[j][2 * x + e] = tok < seg_tok ? s[j][2 * x + e] * scale : -INFINITY;
-          mx = fmaxf(mx, s[j][2 * x + e]);
-        }
-      mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
-      mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
-      float p[2][2] = {{0.f, 0.f}, {0.f, 0.f}};
-      corr[x] = 1.f;
-      if (active) {
-        const float m_new = fmaxf(m_run[x], mx);
-        corr[x] = exp2f(m_run[x] - m_new);
-        float rs = 0.f;
-#pragma unroll
-        for (int j = 0; j < 2; ++j)
-#pragma unroll
-          for (int e = 0; e < 2; ++e) {
-            p[j][e] = exp2f(s[j][2 * x + e] - m_new);
-            rs += p[j][e];
-          }
-        rs += __shfl_xor_sync(0xffffffffu, rs, 1);
-        rs += __shfl_xor_sync(0xffffffffu, rs, 2);
-        l_run[x] = __fmaf_rn(l_run[x], corr[x], rs);
-        m_run[x] = m_new;
-      }
-      pa[x][0] = pack_bf2(p[0][0], p[0][1]);
-      pa[x][1] = pack_bf2(p[1][0], p[1][1]);
-    }
-#pragma unroll
-    for (int t = 0; t < NT; ++t) {
-      o[t][0] *= corr[0];
-      o[t][1] *= corr[0];
-      o[t][2] *= corr[1];
-      o[t][3] *= corr[1];
-    }
-    {
-      const int mi = lane >> 3, ri = lane & 7;
-      const int row = (mi & 1) * 8 + ri;
-#pragma unroll
-      for (int dt = 0; dt < NT / 2; ++dt) {
-        const int ch = 2 * dt + (mi >> 1);
-        uint32_t b[4];
-        ldsm_x4_t(vs + row * ROWB + ((ch ^ (row & 7)) << 4), b);
-        mma_bf16_full(o[2 * dt], pa[0][0], pa[1][0], pa[0][1], pa[1][1], b[0], b[1]);
-        mma_bf16_full(o[2 * dt + 1], pa[0][0], pa[1][0], pa[0][1], pa[1][1], b[2], b[3]);
-      }
-    }
-  }
-  cp_wait<0>();
-  __syncthreads();
-
-  // merge: per pair, the 4 role partials of each row in warp order -- the
-  // pair kernel's merge with a region per pair
-  constexpr int RED = WARPS * 16 * D;                          // floats per pair
-  float* red = reinterpret_cast<float*>(smem) + pg * RED;      // [WARPS][16][D]
-  float* mls = reinterpret_cast<float*>(smem) + NP * RED + pg * WARPS * 16 * 2;   // [WARPS][16][2]
-  float* cws_all = reinterpret_cast<float*>(smem) + NP * RED + NP * WARPS * 16 * 2;   // [NP][16][W+2]
-#pragma unroll
-  for (int t = 0; t < NT; ++t) {
-    const int col = t * 8 + 2 * (lane & 3);
-    *reinterpret_cast<float2*>(&red[(role * 16 + h) * D + col]) = make_float2(o[t][0], o[t][1]);
-    *reinterpret_cast<float2*>(&red[(role * 16 + 8 + h) * D + col]) = make_float2(o[t][2], o[t][3]);
-  }
-  if ((lane & 3) == 0) {
-    mls[(role * 16 + h) * 2] = m_run[0];
-    mls[(role * 16 + h) * 2 + 1] = l_run[0];
-    mls[(role * 16 + 8 + h) * 2] = m_run[1];
-    mls[(role * 16 + 8 + h) * 2 + 1] = l_run[1];
-  }
-  __syncthreads();
-  if (threadIdx.x < 16 * NP) {
-    const int q = threadIdx.x / 16, slot = threadIdx.x % 16;
-    const float* ml = reinterpret_cast<float*>(smem) + NP * RED + q * WARPS * 16 * 2;
-    float* cws = cws_all + q * 16 * (WARPS + 2);
-    float M = -INFINITY;
-#pragma unroll
-    for (int w = 0; w < WARPS; ++w) M = fmaxf(M, ml[(w * 16 + slot) * 2]);
-    float L = 0.f;
-#pragma unroll
-    for (int w = 0; w < WARPS; ++w) {
-      const float cw = exp2f(ml[(w * 16 + slot) * 2] - M);
-      L = __fmaf_rn(cw, ml[(w * 16 + slot) * 2 + 1], L);
-      cws[slot * (WARPS + 2) + w] = cw;
-    }
-    cws[slot * (WARPS + 2) + WARPS] = M;
-    cws[slot * (WARPS + 2) + WARPS + 1] = L;
-  }
-  __syncthreads();
-  for (int i = threadIdx.x; i < NP * 2 * G * D; i += NP * WARPS * 32) {
-    const int q = i / (2 * G * D), x = (i / (G * D)) % 2, g = (i / D) % G, d = i % D;
-    const int rr = rG + 2 * q + x;
-    const int n = a.row_pos[rr] + 1;
-    if (w0 >= n) continue;                                     // no positions in this window
-    const int slot = x * 8 + g;
-    const float* cs = cws_all + (q * 16 + slot) * (WARPS + 2);
-    const float* rq = reinterpret_cast<float*>(smem) + q * RED;
-    const float M = cs[WARPS], L = cs[WARPS + 1];
-    float O = 0.f;
-#pragma unroll
-    for (int w = 0; w < WARPS; ++w) O = __fmaf_rn(cs[w], rq[(w * 16 + slot) * D + d], O);
-    const int qh = kvh * G + g;
-    if (n <= SUPER) {
-      a.out[static_cast<size_t>(rr) * a.ldo + qh * D + d] = __float2bfloat16_rn(O / L);
-    } else {
-      float* wsp = a.ws + ((static_cast<size_t>(rr) * a.NQ + qh) * a.max_splits + ws_idx) * (D + 2);
-      wsp[d] = O;
-      if (d == 0) {
-        wsp[D] = M;
-        wsp[D + 1] = L;
-      }
-    }
-  }
-}
-
 // Merge the per-window partials of rows longer than one window, in order.
 __global__ void attn_combine_kernel(AttnArgs a) {
   pdl_trigger();
@@ -921,7 +672,6 @@ __global__ void attn_combine_kernel(AttnArgs a) {
 
 int attention_windows(int max_seq) { return (max_seq + SUPER - 1) / SUPER; }
 int attention_window_positions() { return SUPER; }
-int attention_group_pairs() { return ATTN_GROUP; }
 
 template <int D>
 static int launch_attn(const AttnArgs& a, cudaStream_t st, bool pairs) {
@@ -934,9 +684,6 @@ static int launch_attn(const AttnArgs& a, cudaStream_t st, bool pairs) {
   constexpr int smem2 = smem_pipe2 > smem_red2 ? smem_pipe2 : smem_red2;
   constexpr int smem_pipe2s = 2 * ATTN_PAIR_STAGES * 2 * CHUNK * D * 2;   // 2-warp short pairs
   constexpr int smem2s = smem_pipe2s > smem_red2 ? smem_pipe2s : smem_red2;
-  constexpr int smem_grp_pipe = WARPS * 3 * 2 * CHUNK * D * 2;
-  constexpr int smem_grp_red = ATTN_GROUP * (WARPS * 16 * D * 4 + WARPS * 16 * 2 * 4 + 16 * (WARPS + 2) * 4);
-  constexpr int smem_grp = smem_grp_pipe > smem_grp_red ? smem_grp_pipe : smem_grp_red;
   static bool attr[64] = {false};
   int dev = 0;
   RLB_CUDA(cudaGetDevice(&dev));
@@ -948,17 +695,12 @@ static int launch_attn(const AttnArgs& a, cudaStream_t st, bool pairs) {
                                   smem2));
     RLB_CUDA(cudaFuncSetAttribute(attn_pair_kernel<D, 2>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, smem2s));
-    RLB_CUDA(cudaFuncSetAttribute(attn_group_kernel<D, ATTN_GROUP>,
-                                  cudaFuncAttributeMaxDynamicSharedMemorySize, smem_grp));
     attr[dev & 63] = true;
   }
   static int n_sm = 0;
   if (!n_sm) RLB_CUDA(cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev));
 
   if (pairs && a.pair_ids) {
-    if (a.n_groups > 0)
-      RLB_CUDA(launch_k(attn_group_kernel<D, ATTN_GROUP>, dim3(a.max_splits, a.NKV, a.n_groups),
-                        dim3(ATTN_GROUP * WARPS * 32), smem_grp, st, a));
     if (a.n_short > 0)
       RLB_CUDA(launch_k(attn_pair_kernel<D, 2>, dim3(a.max_splits, a.NKV, a.n_short), dim3(64),
                         smem2s, st, a));

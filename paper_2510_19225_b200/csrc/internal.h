@@ -66,10 +66,6 @@ struct AttnArgs {
   // pair_ids[n_short, n_short + n_long) the rest; null = every pair, 4 warps
   const int* pair_ids = nullptr;
   int n_short = 0, n_long = 0;
-  // prefill groups of ATTN_GROUP consecutive pairs of one sequence (first
-  // row of each), served by attn_group_kernel; their pairs are in neither list
-  const int* group_ids = nullptr;
-  int n_groups = 0;
   // decode K/V loads through TMA: a 3D tensor map over the whole KV pool
   // (make_kv_map) and this layer's first row in it; null = cp.async
   const CUtensorMap* kv_map = nullptr;
@@ -78,7 +74,6 @@ struct AttnArgs {
 int attention_launch(const AttnArgs& a, cudaStream_t st, bool row_pairs = false);
 int attention_windows(int max_seq);   // CTA windows per row (AttnArgs.max_splits)
 int attention_window_positions();     // positions per CTA window (numerics plan)
-int attention_group_pairs();          // row pairs per prefill group CTA (K1g)
 
 int embed_launch(const bf16* embed, int H, const int* tok, int R, float* h, cudaStream_t st);
 int resid_norm_launch(float* h, const float* part, int S, int Mp, const int* src_rows, int R,

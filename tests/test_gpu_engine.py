@@ -434,34 +434,6 @@ def test_attention_tma_same_bits(request, monkeypatch, case):
     assert torch.equal(out["0"][1], out["1"][1])
 
 
-@pytest.mark.parametrize("case", ["mid", "tiny-long"])
-def test_prefill_groups_same_bits(request, monkeypatch, case):
-    """Prefill attention on groups of 3 row pairs sharing each K/V chunk
-    (K1g) against every long pair on the pair kernel (RLB_ATTN_GROUPS=0):
-    teacher-forced logits bitwise equal, and after a rollout (varlen prefill
-    of many sequences + decode) the KV pool bytewise equal."""
-    if case == "mid":
-        shape, w, _ = request.getfixturevalue("mid")
-        prompts = synth_prompts(12, shape.vocab, 100, 700, seed=37)
-        kw, new = dict(max_slots=16, max_seq_len=1024, max_prefill_rows=2000), 24
-    else:
-        w, _ = request.getfixturevalue("tiny")
-        shape = TINY
-        prompts = synth_prompts(3, TINY.vocab, 2000, 2300, seed=41)
-        kw, new = dict(max_slots=4, max_seq_len=2560, max_prefill_rows=1500), 16
-    out = {}
-    for flag in ("0", "1"):
-        monkeypatch.setenv("RLB_ATTN_GROUPS", flag)
-        inst = _instance(shape, w, **kw)
-        logits = inst.score(prompts[0])
-        toks = _rollout(inst, prompts, new)
-        out[flag] = (logits, toks, _kv_bytes(inst))
-        inst.close()
-    assert np.array_equal(out["0"][0].view(np.uint32), out["1"][0].view(np.uint32))
-    assert out["0"][1] == out["1"][1]
-    assert torch.equal(out["0"][2], out["1"][2])
-
-
 def test_bucketed_decode_batches_same_tokens(tiny):
     """A long-tail batch (targets 20..200) decodes on bucketed batch sizes
     padded with scratch-slot rows and whole graphs past a row's target; every
