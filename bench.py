@@ -26,7 +26,7 @@ Printed JSON line (rank 0):
                TransferPool's modelled pull time), 1 core
 `--impl reference` times only the CPU decoder (the reference has no decoder
 of its own -- SURVEY.md §0 -- so its CPU path is the oracle port), each step
-a batched rollout of 4 prompts x 32 tokens.
+a batched rollout of 8 prompts x 64 tokens.
 """
 from __future__ import annotations
 
@@ -47,7 +47,7 @@ NEW_TOKENS = 1024
 P_LO, P_HI = 128, 384
 MAX_SEQ = 1408            # P_HI + NEW_TOKENS
 CPU_SAMPLE = (16, 64)     # config 2 reduced: prompts x new tokens
-REF_ARM_SAMPLE = (4, 32)  # --impl reference: one step = a batched rollout of this sample
+REF_ARM_SAMPLE = (8, 64)  # --impl reference: one step = a batched rollout of this sample
 NCU_ATTN_FILE = "profiles/r2_attn_mid_ncu.json"   # ncu --set full of the profiled launch
 HBM_KERNELS = ("attention", "resid_norm")   # bytes-bound (others: FLOPs)   # ncu --set full capture of K1 (traffic)
 
