@@ -111,7 +111,9 @@ __device__ __forceinline__ void attn_load_item(const AttnArgs& a, int ws_idx, in
     const int nseg = npages > warp ? (npages - warp + WARPS - 1) / WARPS : 0;
     if (lane < nseg) {
       const int p = w0 / PAGE + warp + lane * WARPS;
+      RLB_DEV_CHECK(p < a.bt_stride, "attention: position beyond the block table");
       it.my_page = a.block_table[static_cast<size_t>(a.row_slot[r]) * a.bt_stride + p];
+      RLB_DEV_CHECK(it.my_page >= 0 && it.my_page < a.num_pages, "attention: page id");
     }
   }
 }
@@ -443,7 +445,9 @@ __global__ void __launch_bounds__(NW * 32, NW == WARPS ? ATTN_PAIR_MINB : 2 * AT
     int my_page = 0;
     if (lane < nseg) {
       const int pg = w0 / PAGE + warp + lane * WARPS;
+      RLB_DEV_CHECK(pg < a.bt_stride, "pair attention: position beyond the block table");
       my_page = a.block_table[static_cast<size_t>(a.row_slot[r0]) * a.bt_stride + pg];
+      RLB_DEV_CHECK(my_page >= 0 && my_page < a.num_pages, "pair attention: page id");
     }
     const int last_seg_tokens = nseg > 0 ? min(PAGE, wn - (warp + (nseg - 1) * WARPS) * PAGE) : 0;
     const int nchunks = nseg > 0 ? (nseg - 1) * (PAGE / CHUNK) + (last_seg_tokens + CHUNK - 1) / CHUNK : 0;

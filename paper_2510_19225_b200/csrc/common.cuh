@@ -276,6 +276,28 @@ __device__ __forceinline__ float dsmem_ld(uint32_t addr) {
   return v;
 }
 
+// ------------------------------------------------- checked build (-DRLB_CHECKED) --
+// Device-side bounds checks on every index the kernels take from device
+// tables (page ids, slots, positions, sequence lengths): `make checked`
+// builds paper_2510_19225_b200/librlb_checked.so with them, and the GPU
+// tests run against it (RLB_LIB=...) -- a failed check prints the site and
+// traps, so the test process fails instead of reading or writing out of
+// bounds.  The default build compiles them out.
+#ifdef RLB_CHECKED
+#define RLB_DEV_CHECK(cond, what)                                                          \
+  do {                                                                                     \
+    if (!(cond)) {                                                                         \
+      printf("RLB device check failed: %s (%s:%d, block %d thread %d)\n", what, __FILE__,   \
+             __LINE__, static_cast<int>(blockIdx.x), static_cast<int>(threadIdx.x));        \
+      __trap();                                                                            \
+    }                                                                                      \
+  } while (0)
+#else
+#define RLB_DEV_CHECK(cond, what) \
+  do {                            \
+  } while (0)
+#endif
+
 // ------------------------------------------ programmatic dependent launch --
 // Every hot kernel is launched with programmatic stream serialization: it may
 // start (and run its prologue: barrier init, TMEM alloc, descriptor

@@ -735,10 +735,12 @@ int rlb_instance::forward_layers(int R, bool prefill) {
     const LayerW& w = L[l];
     bf16* kv_l = kv + layer_stride * l;
     GemmParams pq{R, QKV, H, w.bqkv, nullptr, 0, sp_qkv, nullptr};
-    pq.rope = RopeDst{d_row_slot, d_row_pos, d_rope, d_q, NQ * D, kv_l, d_bt, pps, NQ, NKV, D};
+    pq.rope = RopeDst{d_row_slot, d_row_pos, d_rope, d_q, NQ * D, kv_l, d_bt, pps, NQ, NKV, D,
+                      num_pages};
     if ((rc = qkv_launch(tp, w, pq))) return rc;
     AttnArgs a{d_q, NQ * D, kv_l, d_bt, pps, d_row_slot, d_row_pos, R, NQ, NKV, D, max_splits,
                d_ws, d_attn, NQ * D};
+    a.num_pages = num_pages;
     if (!prefill && attn_tma) {
       a.kv_map = &kv_map;
       a.kv_row0 = static_cast<int64_t>(layer_stride / D) * l;

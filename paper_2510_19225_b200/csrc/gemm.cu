@@ -188,7 +188,9 @@ __device__ __forceinline__ void cluster_epilogue(const GemmParams& p, uint32_t s
     if (lane < nrows) {
       const int m = m_blk * BMT + r0 + ew + NW * lane;
       pos_l = d.row_pos[m];
+      RLB_DEV_CHECK(pos_l / PAGE < d.bt_stride, "RoPE epilogue: position beyond the block table");
       const int page = d.block_table[static_cast<size_t>(d.row_slot[m]) * d.bt_stride + pos_l / PAGE];
+      RLB_DEV_CHECK(page >= 0 && page < d.num_pages, "RoPE epilogue: page id");
       kvo_l = static_cast<size_t>(page) * head_stride * d.nkv + static_cast<size_t>(pos_l % PAGE) * d.d;
     }
     int jv[2], c1v[2], headv[2];
@@ -286,7 +288,9 @@ __device__ __forceinline__ RopeRow rope_row_prefetch(const GemmParams& p, int m,
   const int hd = d.d / 2;
   const size_t head_stride = static_cast<size_t>(2) * PAGE * d.d;
   rr.pos = d.row_pos[m];
+  RLB_DEV_CHECK(rr.pos / PAGE < d.bt_stride, "RoPE epilogue: position beyond the block table");
   const int page = d.block_table[static_cast<size_t>(d.row_slot[m]) * d.bt_stride + rr.pos / PAGE];
+  RLB_DEV_CHECK(page >= 0 && page < d.num_pages, "RoPE epilogue: page id");
   rr.kv_page = d.kv + static_cast<size_t>(page) * head_stride * d.nkv +
                static_cast<size_t>(rr.pos % PAGE) * d.d;
   for (int cp = cp0; cp < cp1; ++cp) {

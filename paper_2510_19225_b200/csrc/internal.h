@@ -26,6 +26,7 @@ struct RopeDst {
   const int* block_table;
   int bt_stride;
   int nq, nkv, d;
+  int num_pages = 1 << 30;   // (checked build) page ids must be below it
 };
 
 struct GemmParams {
@@ -70,6 +71,7 @@ struct AttnArgs {
   // (make_kv_map) and this layer's first row in it; null = cp.async
   const CUtensorMap* kv_map = nullptr;
   int64_t kv_row0 = 0;
+  int num_pages = 1 << 30;          // (checked build) page ids must be below it
 };
 int attention_launch(const AttnArgs& a, cudaStream_t st, bool row_pairs = false);
 int attention_windows(int max_seq);   // CTA windows per row (AttnArgs.max_splits)

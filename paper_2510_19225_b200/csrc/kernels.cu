@@ -77,7 +77,9 @@ __global__ void __launch_bounds__(512) argmax_append_kernel(
       }
     const int s = logit_slot[r];
     const int len = seq_len[s];
+    RLB_DEV_CHECK(s >= 0 && s <= max_slots, "argmax_append: slot");
     if (len < seq_target[s]) {
+      RLB_DEV_CHECK(len >= 0 && len < max_seq, "argmax_append: sequence length");
       seq_tokens[static_cast<size_t>(s) * max_seq + len] = idx;
       seq_len[s] = len + 1;
       ring[static_cast<size_t>(*ring_cur) * max_slots + s] = idx;
@@ -108,6 +110,7 @@ __global__ void decode_prepare_kernel(const int* __restrict__ dec_slots, int R,
   if (i >= R) return;
   const int s = dec_slots[i];
   const int len = seq_len[s];
+  RLB_DEV_CHECK(len >= 1 && len <= max_seq, "decode_prepare: sequence length");
   row_tok[i] = seq_tokens[static_cast<size_t>(s) * max_seq + len - 1];
   row_pos[i] = len - 1;
   row_slot[i] = s;
@@ -133,7 +136,10 @@ __global__ void seed_tokens_kernel(const int* __restrict__ row_tok, const int* _
   pdl_trigger();
   pdl_wait();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < R) seq_tokens[static_cast<size_t>(row_slot[i]) * max_seq + row_pos[i]] = row_tok[i];
+  if (i < R) {
+    RLB_DEV_CHECK(row_pos[i] >= 0 && row_pos[i] < max_seq, "seed_tokens: position");
+    seq_tokens[static_cast<size_t>(row_slot[i]) * max_seq + row_pos[i]] = row_tok[i];
+  }
 }
 
 int seed_tokens_launch(const int* row_tok, const int* row_pos, const int* row_slot, int R,
@@ -163,6 +169,7 @@ __global__ void gather_seqs_kernel(const int* __restrict__ slots, const int64_t*
                                    int32_t* __restrict__ out) {
   const int i = blockIdx.x;
   const int64_t beg = cu[i], len = cu[i + 1] - cu[i];
+  RLB_DEV_CHECK(len >= 0 && len <= max_seq, "gather_seqs: length");
   const int32_t* src = seq_tokens + static_cast<size_t>(slots[i]) * max_seq;
   for (int64_t k = threadIdx.x; k < len; k += blockDim.x) out[beg + k] = src[k];
 }
