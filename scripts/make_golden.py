@@ -12,9 +12,6 @@ builder container; /root/reference and transformers must be importable).
    (pkg/tests/test_acceptance.py:191-227), 8 steps,
    plus the counts the reference oracles (pkg/tests/oracles.py) derive from
    them.  Pins oracle/audit.py.
-3. ref_manager_script.jsonl -- the event log of the reference RolloutManager
-   driven by a fixed call script (scripts/manager_script.py) with preemption,
-   migration and gating.  Pins paper_2510_19225_b200/manager.py.
 """
 from __future__ import annotations
 
