@@ -387,9 +387,6 @@ __device__ __forceinline__ void mma_bf16_full(float (&d)[4], uint32_t a0, uint32
 #ifndef ATTN_PAIR_MINB
 #define ATTN_PAIR_MINB 3
 #endif
-#ifndef ATTN_PAIR_PIPE
-#define ATTN_PAIR_PIPE 1       // with a 3+-stage ring: next chunk's QK^T hoisted (same bits)
-#endif
 // NW = 2: the short-pair variant -- rows with <= 2 pages of context only
 // have pages in warp slots 0 and 1, so two physical warps do all the work and
 // slots 2, 3 enter the merge as the empty partials (m = -inf, l = 0, o = 0)
@@ -481,50 +478,33 @@ __global__ void __launch_bounds__(NW * 32, NW == WARPS ? ATTN_PAIR_MINB : 2 * AT
 #pragma unroll
     for (int t = 0; t < NT; ++t) o[t][0] = o[t][1] = o[t][2] = o[t][3] = 0.f;
     float m_run[2] = {-INFINITY, -INFINITY}, l_run[2] = {0.f, 0.f};
-    // S = Q K^T of chunk c (16 tokens, two n-tiles of 8) from its ring stage
-    auto qk = [&](int c, float (&sc)[2][4]) {
-      const uint32_t ks = wsm_u32 + (c % STAGES) * STAGE_BYTES;
-      const int mi = lane >> 3, ri = lane & 7;
-      const int row = (mi >> 1) * 8 + ri;
-#pragma unroll
-      for (int j = 0; j < 2; ++j) sc[j][0] = sc[j][1] = sc[j][2] = sc[j][3] = 0.f;
-#pragma unroll
-      for (int kk = 0; kk < KSTEPS; ++kk) {
-        const int ch = 2 * kk + (mi & 1);
-        uint32_t b[4];
-        ldsm_x4(ks + row * ROWB + ((ch ^ (row & 7)) << 4), b);
-        mma_bf16_full(sc[0], qa[kk][0], qa[kk][1], qa[kk][2], qa[kk][3], b[0], b[1]);
-        mma_bf16_full(sc[1], qa[kk][0], qa[kk][1], qa[kk][2], qa[kk][3], b[2], b[3]);
-      }
-    };
-    // PIPE (3-stage ring): chunk c+1's QK^T is issued between chunk c's
-    // softmax and its PV, so its MMAs fill the softmax / PV latency.  Every
-    // accumulator still sees the same operations in the same order (same bits).
-    constexpr bool PIPE = STAGES >= 3 && ATTN_PAIR_PIPE;
 #pragma unroll
     for (int c = 0; c < STAGES - 1; ++c) {
       if (c < nchunks) issue(c);
       cp_commit();
     }
-    float s[2][4];
-    if constexpr (PIPE) {
-      if (nchunks > 0) {
-        cp_wait<STAGES - 2>();        // chunk 0
-        __syncwarp();
-        qk(0, s);
-      }
-    }
     for (int c = 0; c < nchunks; ++c) {
       if (c + STAGES - 1 < nchunks) issue(c + STAGES - 1);
       cp_commit();
-      if constexpr (!PIPE) {
-        cp_wait<STAGES - 1>();
-        __syncwarp();
-        qk(c, s);
-      }
-      const uint32_t vs = wsm_u32 + (c % STAGES) * STAGE_BYTES + CHUNK * ROWB;
+      cp_wait<STAGES - 1>();
+      __syncwarp();
+      const uint32_t ks = wsm_u32 + (c % STAGES) * STAGE_BYTES;
+      const uint32_t vs = ks + CHUNK * ROWB;
       const int pstart = (warp + (c >> 2) * WARPS) * PAGE;   // window position of the page
       const int tok0 = (c & 3) * CHUNK;
+      float s[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
+      {
+        const int mi = lane >> 3, ri = lane & 7;
+        const int row = (mi >> 1) * 8 + ri;
+#pragma unroll
+        for (int kk = 0; kk < KSTEPS; ++kk) {
+          const int ch = 2 * kk + (mi & 1);
+          uint32_t b[4];
+          ldsm_x4(ks + row * ROWB + ((ch ^ (row & 7)) << 4), b);
+          mma_bf16_full(s[0], qa[kk][0], qa[kk][1], qa[kk][2], qa[kk][3], b[0], b[1]);
+          mma_bf16_full(s[1], qa[kk][0], qa[kk][1], qa[kk][2], qa[kk][3], b[2], b[3]);
+        }
+      }
       // per row x (0: MMA rows 0-7, 1: rows 8-15): online softmax over the
       // chunk exactly as the decode kernel does, or no update at all when the
       // chunk holds none of the row's positions
@@ -566,13 +546,6 @@ __global__ void __launch_bounds__(NW * 32, NW == WARPS ? ATTN_PAIR_MINB : 2 * AT
         }
         pa[x][0] = pack_bf2(p[0][0], p[0][1]);
         pa[x][1] = pack_bf2(p[1][0], p[1][1]);
-      }
-      if constexpr (PIPE) {
-        if (c + 1 < nchunks) {
-          cp_wait<STAGES - 2>();      // chunk c+1 (and c)
-          __syncwarp();
-          qk(c + 1, s);               // s is dead after the softmax above
-        }
       }
 #pragma unroll
       for (int t = 0; t < NT; ++t) {
