@@ -55,7 +55,8 @@ typedef struct {
 typedef struct {
   int32_t max_slots;          /* concurrent sequences (decode batch) */
   int32_t max_seq_len;        /* prompt + generated tokens per sequence */
-  int32_t num_pages;          /* KV pages of 64 tokens; 0 = max_slots*ceil(max_seq_len/64) */
+  int32_t num_pages;          /* KV pages of 64 tokens (one is reserved for the padding rows of
+                                 bucketed decode batches); 0 = max_slots*ceil(max_seq_len/64)+1 */
   int32_t max_prefill_rows;   /* token rows per prefill chunk */
   int32_t graph_steps;        /* decode steps per captured CUDA graph; 0 = eager */
   /* Numerics plan: the split-K factors of the O and down projections fix the

@@ -487,7 +487,8 @@ int rlb_instance::init() {
   max_seq = e.max_seq_len;
   RLB_CHECK(max_slots > 0 && max_seq > 0, RLB_ERR_ARG, "max_slots/max_seq_len must be positive");
   pps = (max_seq + PAGE - 1) / PAGE;
-  num_pages = e.num_pages > 0 ? e.num_pages : max_slots * pps;
+  // default pool: every slot at max_seq_len, + the scratch slot's page
+  num_pages = e.num_pages > 0 ? e.num_pages : max_slots * pps + 1;
   max_splits = attention_windows(max_seq);
   const size_t ws_row = static_cast<size_t>(NQ) * max_splits * (D + 2) * sizeof(float);
   const size_t ws_budget = static_cast<size_t>(1) << 30;

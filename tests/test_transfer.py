@@ -56,3 +56,22 @@ def test_shadow_pull_collect():
     assert meas.shadow and meas.version == 5
     plane.finish(pool, "i0", 0.1)
     assert inst.swap_weights() == 5
+
+
+def test_a_job_copies_exactly_its_version():
+    """A pull started for version 2 keeps copying version 2 even if version 3
+    is staged before it runs; version 2 is released once no job names it."""
+    pool = TransferPool(build_agents(1, 1, 900 * GB))
+    plane = WeightPlane()
+    plane.stage(pool, 2, "w2", 0.0)
+    assert pool.request_pull("i0", "agent-0.0", 2, GB, float("inf"), 0.0)
+    plane.stage(pool, 3, "w3", 0.1)
+    got = []
+    inst = FakeInstance()
+    inst.pull_weights = lambda src, version: (got.append((src, version)),
+                                              FakeInstance.pull_weights(inst, src, version))[1]
+    plane.run(pool, "i0", inst)
+    assert got == [("w2", 2)]
+    plane.finish(pool, "i0", 0.2)
+    plane.stage(pool, 4, "w4", 0.3)
+    assert sorted(plane.sources) == [4]
