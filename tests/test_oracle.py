@@ -75,3 +75,25 @@ def test_teacher_forced_rule():
     rep = teacher_forced_compare(Fixed(), [[1]], [[0, 1, 2]], 2e-2)   # margin 1.0: failure
     assert not rep.ok and rep.failures[0][:4] == (0, 1, 1, 0)
     assert isinstance(rep, ParityReport)
+
+
+def test_full_depth_oracle_pinned_to_transformers():
+    """The oracle at the benchmarked depth (28-layer Qwen2.5-1.5B shape, the
+    seeded synthetic weights) against transformers' Qwen2ForCausalLM
+    (tests/golden/qwen15_hf.npz): same greedy tokens, top-32 logits within
+    1e-3 at every generated position."""
+    from paper_2510_19225_b200.shapes import QWEN25_1_5B
+    g = np.load(os.path.join(os.path.dirname(__file__), "golden", "qwen15_hf.npz"))
+    w = synth_hf_weights(QWEN25_1_5B, seed=0)
+    sums = np.array([float(w[k].float().sum()) for k in sorted(w)])
+    np.testing.assert_allclose(sums, g["weight_sums"], rtol=0, atol=1e-3)
+    oracle = Qwen2Fp32(QWEN25_1_5B, w)
+    flat, off = g["prompts"].tolist(), 0
+    for k, n in enumerate(g["prompt_lens"]):
+        p = flat[off:off + n]
+        off += n
+        want = g["tokens"][k].tolist()
+        logits = oracle.teacher_forced_logits(p, want).numpy()
+        assert [argmax_lowest(torch.from_numpy(r)) for r in logits] == want
+        got = np.take_along_axis(logits, g["top_indices"][k], axis=1)
+        np.testing.assert_allclose(got, g["top_values"][k], rtol=0, atol=1e-3)
