@@ -1,7 +1,7 @@
 """Oracle parity of the plan the bench runs.
 
 Full 28-layer Qwen2.5-1.5B shape, 512 slots: the decode batch starts at 512
-rows and shrinks as requests finish (targets U[16, 80]), so the steps run
+rows and shrinks as requests finish (targets U[16, 96]), so the steps run
 every tile plan of config 2 -- 512..129 rows (128x64 RoPE QKV tiles, O
 partials, 256-row SwiGLU tiles, pair-tile down, the persistent 2-SM argmax
 lm_head) and <=128 rows -- and the varlen prefill of 512 prompts
@@ -25,7 +25,7 @@ from paper_2510_19225_b200.synth import synth_hf_weights, synth_prompts
 
 pytestmark = pytest.mark.gpu
 TOL_BF16 = 2e-2
-N, T_LO, T_HI = 512, 16, 80
+N, T_LO, T_HI = 512, 16, 96
 SAMPLE = [0, 71, 150, 222, 301, 377, 444, 511]
 
 
