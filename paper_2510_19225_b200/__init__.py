@@ -9,8 +9,9 @@ runner that drives instances under the reference manager).
 
 `spotrl` is resolved from `sys.path` first, then from `<repo>/baseline/_ref`
 (where `__graft_entry__.build()` installs the reference from its own sources;
-that directory travels to GPU boxes with the repo snapshot).  There is no
-fallback: without the reference package the product refuses to import.
+that directory travels to GPU boxes with the repo snapshot), then -- in the
+builder container only -- from the reference source tree itself.  Without
+the reference package the product refuses to import.
 """
 from __future__ import annotations
 
@@ -25,9 +26,12 @@ def _ensure_spotrl() -> None:
     except ImportError:
         pass
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    ref = os.path.join(root, "baseline", "_ref")
-    if os.path.isdir(os.path.join(ref, "spotrl")) and ref not in sys.path:
-        sys.path.append(ref)
+    # the installed copy first; in the builder container the reference's own
+    # source tree (read-only) if build() has not installed it yet
+    for ref in (os.path.join(root, "baseline", "_ref"), "/root/reference/pkg/src"):
+        if os.path.isdir(os.path.join(ref, "spotrl")) and ref not in sys.path:
+            sys.path.append(ref)
+            break
     try:
         import spotrl  # noqa: F401,F811
     except ImportError as exc:

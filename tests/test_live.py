@@ -85,18 +85,23 @@ def test_live_refuses_a_mismatched_numerics_plan():
     srv = ManagerServer(m, version=1, endpoint_for=lambda iid: f"fake://{iid}", max_inflight=4)
     prompts = _prompts(8)
     for k, p in enumerate(prompts):
-        srv.submit(f"r{k}", p, 10)
+        srv.submit(f"r{k}", p, 300)         # long enough that i1 registers mid-run
     stop = threading.Event()
+    mgr = threading.Thread(target=srv.run_until_done, kwargs=dict(timeout=60), daemon=True)
+    mgr.start()
+    import time
     for k, plan in enumerate(["v1.q1.o3.d5.w2048.p64.t0", "v1.q1.o2.d5.w2048.p64.t0"]):
         inst = FakeInstance(vocab=997, max_slots=4, plan=plan)
         t = threading.Thread(target=serve_instance, args=(srv.address, inst, f"i{k}"),
                              kwargs=dict(open_endpoint=lambda ep, v: ep, n_steps=3, stop=stop),
                              daemon=True)
         t.start()
-        if k == 0:
-            import time
-            time.sleep(0.3)                 # i0 reports its plan first
-    srv.run_until_done(timeout=60)
+        t_end = time.monotonic() + 30
+        while k == 0 and srv.plan is None:  # i0's plan is the reference one
+            assert time.monotonic() < t_end
+            time.sleep(0.01)
+    mgr.join(timeout=90)
+    assert not mgr.is_alive()
     stop.set()
     srv.close()
     recs = m.log.records
@@ -104,4 +109,4 @@ def test_live_refuses_a_mismatched_numerics_plan():
     assert assert_token_conservation(recs) == 8
     probe = FakeInstance(vocab=997)
     for k, p in enumerate(prompts):
-        assert m.requests[f"r{k}"].generated == reference_continuation(probe, p, 10)
+        assert m.requests[f"r{k}"].generated == reference_continuation(probe, p, 300)
