@@ -653,6 +653,240 @@ __global__ void __launch_bounds__(NW * 32, NW == WARPS ? ATTN_PAIR_MINB : 2 * AT
   }
 }
 
+// K1h: prefill rows packed by head.  The pair kernel's MMA rows are 2 token
+// rows x 8 head slots, of which a GQA group of 6 (7 for the 7B shape) is
+// real.  Here a CTA serves 16 consecutive rows of one sequence for ONE query
+// head: the MMA rows are the 16 positions, all real, so a chunk's QK^T and
+// PV MMAs (and the softmax instructions around them) serve 16 rows instead
+// of 12.  Every (row, head) still goes through the decode kernel's sequence:
+// the same pages per warp slot, 16-token chunks in order, the same masking,
+// online-softmax steps (quad shuffles over the same token columns) and
+// warp-order merge -- a row whose positions end before a chunk takes no
+// update from it (computed and discarded, so the quad shuffles stay
+// converged).  Same bits as K1p and K1.
+template <int D>
+__global__ void __launch_bounds__(WARPS * 32, ATTN_PAIR_MINB) attn_head16_kernel(AttnArgs a) {
+  constexpr int STAGES = ATTN_PAIR_STAGES;
+  constexpr int ROWB = D * 2;
+  constexpr int CPR = ROWB / 16;
+  constexpr int KSTEPS = D / 16;
+  constexpr int NT = D / 8;
+  constexpr int STAGE_BYTES = 2 * CHUNK * ROWB;
+  constexpr int WARP_SMEM = STAGES * STAGE_BYTES;
+  extern __shared__ __align__(128) uint8_t smem[];
+
+  const int ws_idx = blockIdx.x, qh = blockIdx.y;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int G = a.NQ / a.NKV;
+  const int kvh = qh / G;
+  pdl_trigger();
+  pdl_wait();
+  const int rG = a.head16_ids[blockIdx.z];                 // first of the 16 rows
+  const float scale = rsqrtf(static_cast<float>(D)) * 1.4426950408889634f;
+  const int w0 = ws_idx * SUPER;
+  const int h = lane >> 2;                                  // this lane's rows: rG+h, rG+h+8
+  const int wnr[2] = {min(SUPER, a.row_pos[rG + h] + 1 - w0),
+                      min(SUPER, a.row_pos[rG + h + 8] + 1 - w0)};
+  const int wn = min(SUPER, a.row_pos[rG + 15] + 1 - w0);  // the last row sees the most
+  if (wn <= 0) return;                                      // uniform over the CTA
+
+  uint32_t qa[KSTEPS][4];
+  {
+    const bf16* q0 = a.q + static_cast<size_t>(rG + h) * a.ldq + static_cast<size_t>(qh) * D;
+    const bf16* q1 = q0 + static_cast<size_t>(8) * a.ldq;
+#pragma unroll
+    for (int kk = 0; kk < KSTEPS; ++kk) {
+      const int c = kk * 16 + 2 * (lane & 3);
+      qa[kk][0] = wnr[0] > 0 ? *reinterpret_cast<const uint32_t*>(q0 + c) : 0u;
+      qa[kk][2] = wnr[0] > 0 ? *reinterpret_cast<const uint32_t*>(q0 + c + 8) : 0u;
+      qa[kk][1] = wnr[1] > 0 ? *reinterpret_cast<const uint32_t*>(q1 + c) : 0u;
+      qa[kk][3] = wnr[1] > 0 ? *reinterpret_cast<const uint32_t*>(q1 + c + 8) : 0u;
+    }
+  }
+  const int npages = (wn + PAGE - 1) / PAGE;
+  const int nseg = npages > warp ? (npages - warp + WARPS - 1) / WARPS : 0;
+  int my_page = 0;
+  if (lane < nseg) {
+    const int pg = w0 / PAGE + warp + lane * WARPS;
+    RLB_DEV_CHECK(pg < a.bt_stride, "head16 attention: position beyond the block table");
+    my_page = a.block_table[static_cast<size_t>(a.row_slot[rG]) * a.bt_stride + pg];
+    RLB_DEV_CHECK(my_page >= 0 && my_page < a.num_pages, "head16 attention: page id");
+  }
+  const int last_seg_tokens = nseg > 0 ? min(PAGE, wn - (warp + (nseg - 1) * WARPS) * PAGE) : 0;
+  const int nchunks = nseg > 0 ? (nseg - 1) * (PAGE / CHUNK) + (last_seg_tokens + CHUNK - 1) / CHUNK : 0;
+  uint8_t* wsm = smem + warp * WARP_SMEM;
+  const uint32_t wsm_u32 = smem_u32(wsm);
+  const size_t head_off = static_cast<size_t>(kvh) * (2 * PAGE * D);
+  const size_t page_stride = static_cast<size_t>(a.NKV) * (2 * PAGE * D);
+  auto issue = [&](int c) {
+    const int seg = c >> 2;
+    const int page = __shfl_sync(0xffffffffu, my_page, seg);
+    const int seg_tok = min(PAGE, wn - (warp + seg * WARPS) * PAGE);
+    const bf16* kp = a.kv + static_cast<size_t>(page) * page_stride + head_off;
+    const uint32_t st = wsm_u32 + (c % STAGES) * STAGE_BYTES;
+#pragma unroll
+    for (int i = 0; i < (CHUNK * CPR) / 32; ++i) {
+      const int idx = i * 32 + lane;
+      const int row = idx / CPR, ch = idx % CPR;
+      const int tok = (c & 3) * CHUNK + row;
+      const bool ok = tok < seg_tok;
+      const bf16* src = kp + static_cast<size_t>(ok ? tok : 0) * D + ch * 8;
+      const uint32_t off = row * ROWB + ((ch ^ (row & 7)) << 4);
+      cp_async16(st + off, src, ok);
+      cp_async16(st + CHUNK * ROWB + off, src + PAGE * D, ok);
+    }
+  };
+
+  float o[NT][4];
+#pragma unroll
+  for (int t = 0; t < NT; ++t) o[t][0] = o[t][1] = o[t][2] = o[t][3] = 0.f;
+  float m_run[2] = {-INFINITY, -INFINITY}, l_run[2] = {0.f, 0.f};
+#pragma unroll
+  for (int c = 0; c < STAGES - 1; ++c) {
+    if (c < nchunks) issue(c);
+    cp_commit();
+  }
+  for (int c = 0; c < nchunks; ++c) {
+    if (c + STAGES - 1 < nchunks) issue(c + STAGES - 1);
+    cp_commit();
+    cp_wait<STAGES - 1>();
+    __syncwarp();
+    const uint32_t ks = wsm_u32 + (c % STAGES) * STAGE_BYTES;
+    const uint32_t vs = ks + CHUNK * ROWB;
+    const int pstart = (warp + (c >> 2) * WARPS) * PAGE;
+    const int tok0 = (c & 3) * CHUNK;
+    float s[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
+    {
+      const int mi = lane >> 3, ri = lane & 7;
+      const int row = (mi >> 1) * 8 + ri;
+#pragma unroll
+      for (int kk = 0; kk < KSTEPS; ++kk) {
+        const int ch = 2 * kk + (mi & 1);
+        uint32_t b[4];
+        ldsm_x4(ks + row * ROWB + ((ch ^ (row & 7)) << 4), b);
+        mma_bf16_full(s[0], qa[kk][0], qa[kk][1], qa[kk][2], qa[kk][3], b[0], b[1]);
+        mma_bf16_full(s[1], qa[kk][0], qa[kk][1], qa[kk][2], qa[kk][3], b[2], b[3]);
+      }
+    }
+    uint32_t pa[2][2];
+    float corr[2];
+#pragma unroll
+    for (int x = 0; x < 2; ++x) {
+      const int wnx = wnr[x];
+      const int seg_tok = min(PAGE, wnx - pstart);
+      const bool active = pstart + tok0 < wnx;             // per quad: the quad's row
+      float mx = -INFINITY;
+#pragma unroll
+      for (int j = 0; j < 2; ++j)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int tok = tok0 + 8 * j + 2 * (lane & 3) + e;
+          s[j][2 * x + e] = tok < seg_tok ? s[j][2 * x + e] * scale : -INFINITY;
+          mx = fmaxf(mx, s[j][2 * x + e]);
+        }
+      mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
+      mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
+      // every lane runs the shuffles; an inactive row keeps its state
+      const float m_new = fmaxf(m_run[x], mx);
+      const float cr = exp2f(m_run[x] - m_new);
+      float p[2][2], rs = 0.f;
+#pragma unroll
+      for (int j = 0; j < 2; ++j)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          p[j][e] = active ? exp2f(s[j][2 * x + e] - m_new) : 0.f;
+          rs += p[j][e];
+        }
+      rs += __shfl_xor_sync(0xffffffffu, rs, 1);
+      rs += __shfl_xor_sync(0xffffffffu, rs, 2);
+      corr[x] = active ? cr : 1.f;
+      if (active) {
+        l_run[x] = __fmaf_rn(l_run[x], cr, rs);
+        m_run[x] = m_new;
+      }
+      pa[x][0] = pack_bf2(p[0][0], p[0][1]);
+      pa[x][1] = pack_bf2(p[1][0], p[1][1]);
+    }
+#pragma unroll
+    for (int t = 0; t < NT; ++t) {
+      o[t][0] *= corr[0];
+      o[t][1] *= corr[0];
+      o[t][2] *= corr[1];
+      o[t][3] *= corr[1];
+    }
+    {
+      const int mi = lane >> 3, ri = lane & 7;
+      const int row = (mi & 1) * 8 + ri;
+#pragma unroll
+      for (int dt = 0; dt < NT / 2; ++dt) {
+        const int ch = 2 * dt + (mi >> 1);
+        uint32_t b[4];
+        ldsm_x4_t(vs + row * ROWB + ((ch ^ (row & 7)) << 4), b);
+        mma_bf16_full(o[2 * dt], pa[0][0], pa[1][0], pa[0][1], pa[1][1], b[0], b[1]);
+        mma_bf16_full(o[2 * dt + 1], pa[0][0], pa[1][0], pa[0][1], pa[1][1], b[2], b[3]);
+      }
+    }
+    __syncwarp();
+  }
+  cp_wait<0>();
+  __syncthreads();
+
+  // merge the 4 warp partials of each of the 16 rows in warp order
+  float* red = reinterpret_cast<float*>(smem);                 // [WARPS][16][D]
+  float* mls = red + WARPS * 16 * D;                             // [WARPS][16][2]
+#pragma unroll
+  for (int t = 0; t < NT; ++t) {
+    const int col = t * 8 + 2 * (lane & 3);
+    *reinterpret_cast<float2*>(&red[(warp * 16 + h) * D + col]) = make_float2(o[t][0], o[t][1]);
+    *reinterpret_cast<float2*>(&red[(warp * 16 + 8 + h) * D + col]) = make_float2(o[t][2], o[t][3]);
+  }
+  if ((lane & 3) == 0) {
+    mls[(warp * 16 + h) * 2] = m_run[0];
+    mls[(warp * 16 + h) * 2 + 1] = l_run[0];
+    mls[(warp * 16 + 8 + h) * 2] = m_run[1];
+    mls[(warp * 16 + 8 + h) * 2 + 1] = l_run[1];
+  }
+  float* cws = mls + WARPS * 16 * 2;                             // [16][WARPS + 2]
+  __syncthreads();
+  if (threadIdx.x < 16) {
+    const int slot = threadIdx.x;
+    float M = -INFINITY;
+#pragma unroll
+    for (int w = 0; w < WARPS; ++w) M = fmaxf(M, mls[(w * 16 + slot) * 2]);
+    float L = 0.f;
+#pragma unroll
+    for (int w = 0; w < WARPS; ++w) {
+      const float cw = exp2f(mls[(w * 16 + slot) * 2] - M);
+      L = __fmaf_rn(cw, mls[(w * 16 + slot) * 2 + 1], L);
+      cws[slot * (WARPS + 2) + w] = cw;
+    }
+    cws[slot * (WARPS + 2) + WARPS] = M;
+    cws[slot * (WARPS + 2) + WARPS + 1] = L;
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < 16 * D; i += WARPS * 32) {
+    const int slot = i / D, d = i % D;
+    const int rr = rG + slot;
+    const int n = a.row_pos[rr] + 1;
+    if (w0 >= n) continue;                                     // no positions in this window
+    const float* cs = cws + slot * (WARPS + 2);
+    const float M = cs[WARPS], L = cs[WARPS + 1];
+    float O = 0.f;
+#pragma unroll
+    for (int w = 0; w < WARPS; ++w) O = __fmaf_rn(cs[w], red[(w * 16 + slot) * D + d], O);
+    if (n <= SUPER) {
+      a.out[static_cast<size_t>(rr) * a.ldo + qh * D + d] = __float2bfloat16_rn(O / L);
+    } else {
+      float* wsp = a.ws + ((static_cast<size_t>(rr) * a.NQ + qh) * a.max_splits + ws_idx) * (D + 2);
+      wsp[d] = O;
+      if (d == 0) {
+        wsp[D] = M;
+        wsp[D + 1] = L;
+      }
+    }
+  }
+}
+
 // Merge the per-window partials of rows longer than one window, in order.
 __global__ void attn_combine_kernel(AttnArgs a) {
   pdl_trigger();
@@ -699,12 +933,17 @@ static int launch_attn(const AttnArgs& a, cudaStream_t st, bool pairs) {
                                   smem2));
     RLB_CUDA(cudaFuncSetAttribute(attn_pair_kernel<D, 2>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, smem2s));
+    RLB_CUDA(cudaFuncSetAttribute(attn_head16_kernel<D>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, smem2));
     attr[dev & 63] = true;
   }
   static int n_sm = 0;
   if (!n_sm) RLB_CUDA(cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev));
 
   if (pairs && a.pair_ids) {
+    if (a.n_head16 > 0)
+      RLB_CUDA(launch_k(attn_head16_kernel<D>, dim3(a.max_splits, a.NQ, a.n_head16),
+                        dim3(WARPS * 32), smem2, st, a));
     if (a.n_short > 0)
       RLB_CUDA(launch_k(attn_pair_kernel<D, 2>, dim3(a.max_splits, a.NKV, a.n_short), dim3(64),
                         smem2s, st, a));

@@ -224,6 +224,10 @@ struct rlb_instance {
   // prefill row pairs split by context length (short: <= 2 pages, 2-warp
   // attention CTAs); set per chunk by admit_and_prefill (RLB_ATTN_SPLIT=0: off)
   int* d_pairs = nullptr;
+  int* d_head16 = nullptr;      // first rows of the 16-row prefill runs (K1h)
+  std::vector<int> h_head16;
+  int head16_n = 0;
+  bool attn_head16 = true;      // RLB_ATTN_HEAD16=0: every pair on the pair kernel (A/B)
   // decode attention K/V through TMA boxes of the whole pool (RLB_ATTN_TMA=0
   // at instance creation: per-lane cp.async -- the same bits, the A/B
   // reference of tests/test_gpu_engine.py)
@@ -421,24 +425,52 @@ struct rlb_instance {
   // row pairs (2p, 2p+1) of a prefill chunk (positions pos[0..n)): those
   // whose rows all see <= 2 pages of context first (2-warp attention CTAs),
   // then the rest in row order; the lists belong to the next forward only
+  // Rows in runs of 16 consecutive positions of one sequence go to the
+  // head-packed kernel (K1h, one CTA per 16 rows x query head); the other
+  // pairs to the pair kernel: short ones (<= 2 pages) first, then the rest.
   int build_pairs(const int* pos, size_t n) {
-    pairs_short = pairs_long = 0;
+    pairs_short = pairs_long = head16_n = 0;
     if (!(attn_pairs && attn_split)) return RLB_OK;
     const int np = static_cast<int>((n + 1) / 2);
     h_pairs.resize(np);
+    h_head16.clear();
     int lo = 0, hi = np;
-    for (int z = 0; z < np; ++z) {
+    auto run16 = [&](int z) {      // rows 2z .. 2z+15: consecutive positions
+      const size_t a0 = 2 * static_cast<size_t>(z);
+      if (a0 + 16 > n) return false;
+      for (int k = 1; k < 16; ++k)
+        if (pos[a0 + k] != pos[a0 + k - 1] + 1) return false;
+      return true;
+    };
+    for (int z = 0; z < np;) {
+      if (attn_head16 && run16(z)) {
+        h_head16.push_back(2 * z);
+        z += 8;
+        continue;
+      }
       const size_t a0 = 2 * static_cast<size_t>(z);
       const bool short_pair = pos[a0] < 2 * PAGE && (a0 + 1 >= n || pos[a0 + 1] < 2 * PAGE);
       if (short_pair) h_pairs[lo++] = z;
       else h_pairs[--hi] = z;
+      ++z;
     }
     std::reverse(h_pairs.begin() + hi, h_pairs.end());   // long pairs in row order
     pairs_short = lo;
-    pairs_long = np - lo;
-    RLB_CUDA(cudaMemcpyAsync(d_pairs, h_pairs.data(), np * sizeof(int), cudaMemcpyHostToDevice, st));
-    stats.h2d_bytes += static_cast<int64_t>(np) * 4;
-    if (pairs_short && pairs_long) stats.kernel_launches += m.layers;   // two attention launches
+    pairs_long = np - hi;
+    if (hi > lo) std::copy(h_pairs.begin() + hi, h_pairs.end(), h_pairs.begin() + lo);
+    head16_n = static_cast<int>(h_head16.size());
+    const int nl = pairs_short + pairs_long;
+    if (nl) {
+      RLB_CUDA(cudaMemcpyAsync(d_pairs, h_pairs.data(), nl * sizeof(int), cudaMemcpyHostToDevice, st));
+      stats.h2d_bytes += static_cast<int64_t>(nl) * 4;
+    }
+    if (head16_n) {
+      RLB_CUDA(cudaMemcpyAsync(d_head16, h_head16.data(), head16_n * sizeof(int),
+                               cudaMemcpyHostToDevice, st));
+      stats.h2d_bytes += static_cast<int64_t>(head16_n) * 4;
+    }
+    const int launches = (pairs_short > 0) + (pairs_long > 0) + (head16_n > 0);
+    if (launches > 1) stats.kernel_launches += static_cast<int64_t>(m.layers) * (launches - 1);
     return RLB_OK;
   }
 };
@@ -450,7 +482,7 @@ rlb_instance::~rlb_instance() {
   void* bufs[] = {arena, kv, d_bt, d_seq_tokens, d_seq_len, d_seq_target, d_row_tok, d_row_pos,
                   d_row_slot, d_logit_src, d_logit_slot, d_dec_slots, d_h, d_xn, d_qkv, d_q,
                   d_attn, d_act, d_logits, d_ws, d_ring, d_ring_ctr, d_ring_cur, d_rope,
-                  d_part, d_exp_slots, d_exp_cu, d_exp_out, d_pairs};
+                  d_part, d_exp_slots, d_exp_cu, d_exp_out, d_pairs, d_head16};
   for (void* b : bufs)
     if (b) cudaFree(b);
   if (shadow.arena) cudaFree(shadow.arena);
@@ -537,6 +569,7 @@ int rlb_instance::init() {
   if (const char* ov = std::getenv("RLB_ATTN_PAIRS")) attn_pairs = std::atoi(ov) != 0;
   if (const char* ov = std::getenv("RLB_ATTN_SPLIT")) attn_split = std::atoi(ov) != 0;
   if (const char* ov = std::getenv("RLB_ATTN_TMA")) attn_tma = std::atoi(ov) != 0;
+  if (const char* ov = std::getenv("RLB_ATTN_HEAD16")) attn_head16 = std::atoi(ov) != 0;
   if (const char* ov = std::getenv("RLB_QKV_KPS")) qkv_kps2 = std::atoi(ov) == 2;
   if (const char* ov = std::getenv("RLB_O_KPS")) o_kps2 = std::atoi(ov) == 2;
   if (const char* ov = std::getenv("RLB_SMALL_GU_WAVE")) small_gu_wave = std::atoi(ov) != 0;
@@ -628,6 +661,7 @@ int rlb_instance::init() {
   if ((rc = dalloc(&d_part, part * R))) return rc;
   if ((rc = dalloc(&d_ring, static_cast<size_t>(RING_ROWS) * max_slots))) return rc;
   if ((rc = dalloc(&d_pairs, max_rows / 2 + 1))) return rc;
+  if ((rc = dalloc(&d_head16, max_rows / 16 + 1))) return rc;
   if ((rc = dalloc(&d_exp_slots, max_slots)) || (rc = dalloc(&d_exp_cu, max_slots + 1)) ||
       (rc = dalloc(&d_exp_out, static_cast<size_t>(max_slots) * max_seq)))
     return rc;
@@ -746,10 +780,12 @@ int rlb_instance::forward_layers(int R, bool prefill) {
       a.kv_map = &kv_map;
       a.kv_row0 = static_cast<int64_t>(layer_stride / D) * l;
     }
-    if (prefill && attn_pairs && attn_split && pairs_short + pairs_long > 0) {
+    if (prefill && attn_pairs && attn_split && pairs_short + pairs_long + head16_n > 0) {
       a.pair_ids = d_pairs;
       a.n_short = pairs_short;
       a.n_long = pairs_long;
+      a.head16_ids = d_head16;
+      a.n_head16 = head16_n;
     }
     if ((rc = attention_launch(a, st, prefill && attn_pairs))) return rc;
     if (cl_o && !pair_o(R)) {
@@ -952,7 +988,7 @@ int rlb_instance::admit_and_prefill(int* rows_run) {
                                  max_seq, st)))
       return rc;
     rc = forward_layers(static_cast<int>(n), true);
-    pairs_short = pairs_long = 0;   // the lists belong to this chunk only
+    pairs_short = pairs_long = head16_n = 0;   // the lists belong to this chunk only
     if (rc) return rc;
     if ((rc = head(nl, true))) return rc;
     stats.h2d_bytes += static_cast<int64_t>(n) * 12 + static_cast<int64_t>(nl) * 8;
@@ -1619,7 +1655,7 @@ int rlb_score(rlb_instance* h, const int32_t* tokens, int32_t n, float* out_logi
     // the same pair lists (2-warp short pairs + 4-warp long pairs) as prefill
     if ((rc = h->build_pairs(pos + beg, cnt))) break;
     rc = h->forward_layers(cnt, true);
-    h->pairs_short = h->pairs_long = 0;
+    h->pairs_short = h->pairs_long = h->head16_n = 0;
     if (rc) break;
     for (int lb = 0; lb < cnt; lb += h->max_slots) {
       const int ln = std::min(h->max_slots, cnt - lb);

@@ -67,6 +67,11 @@ struct AttnArgs {
   // pair_ids[n_short, n_short + n_long) the rest; null = every pair, 4 warps
   const int* pair_ids = nullptr;
   int n_short = 0, n_long = 0;
+  // prefill rows in groups of 16 consecutive positions of one sequence
+  // (first row of each), served per query head by attn_head16_kernel; their
+  // pairs are in neither pair list
+  const int* head16_ids = nullptr;
+  int n_head16 = 0;
   // decode K/V loads through TMA: a 3D tensor map over the whole KV pool
   // (make_kv_map) and this layer's first row in it; null = cp.async
   const CUtensorMap* kv_map = nullptr;

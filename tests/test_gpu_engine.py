@@ -456,3 +456,32 @@ def test_bucketed_decode_batches_same_tokens(tiny):
         assert solo.run_to_completion(32)[f"s{i}"] == got[f"r{i}"]
     assert all(len(got[f"r{i}"]) == targets[i] for i in range(len(prompts)))
     assert len(sizes) > 10          # many real batch sizes ...
+
+
+@pytest.mark.parametrize("case", ["mid", "tiny-long"])
+def test_prefill_head16_same_bits(request, monkeypatch, case):
+    """Prefill attention packed by head (16 consecutive rows of one sequence
+    per CTA and query head, K1h) against the pair kernel for every row
+    (RLB_ATTN_HEAD16=0): teacher-forced logits bitwise equal, and after a
+    rollout (varlen prefill of many sequences, odd chunk boundaries, + decode)
+    the KV pool bytewise equal."""
+    if case == "mid":
+        shape, w, _ = request.getfixturevalue("mid")
+        prompts = synth_prompts(12, shape.vocab, 30, 700, seed=37)
+        kw, new = dict(max_slots=16, max_seq_len=1024, max_prefill_rows=1999), 24
+    else:
+        w, _ = request.getfixturevalue("tiny")
+        shape = TINY
+        prompts = synth_prompts(3, TINY.vocab, 2000, 2300, seed=41)
+        kw, new = dict(max_slots=4, max_seq_len=2560, max_prefill_rows=1500), 16
+    out = {}
+    for flag in ("0", "1"):
+        monkeypatch.setenv("RLB_ATTN_HEAD16", flag)
+        inst = _instance(shape, w, **kw)
+        logits = inst.score(prompts[0])
+        toks = _rollout(inst, prompts, new)
+        out[flag] = (logits, toks, _kv_bytes(inst))
+        inst.close()
+    assert np.array_equal(out["0"][0].view(np.uint32), out["1"][0].view(np.uint32))
+    assert out["0"][1] == out["1"][1]
+    assert torch.equal(out["0"][2], out["1"][2])
