@@ -39,6 +39,14 @@ def test_live_rollout_over_tcp(die):
                              daemon=True)
         t.start()
         threads.append(t)
+    # every instance's register message is queued before the manager starts
+    # dispatching, so all three get requests (a late thread under CPU load
+    # would otherwise find the work gone and never reach die_after_tokens)
+    import time
+    t_end = time.monotonic() + 30
+    while srv.events.qsize() < 3:
+        assert time.monotonic() < t_end
+        time.sleep(0.01)
     srv.run_until_done(timeout=60)
     stop.set()
     srv.close()
