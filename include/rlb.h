@@ -98,13 +98,14 @@ int rlb_instance_destroy(rlb_instance* h);
 const char* rlb_last_error(void);
 
 /* Everything that fixes the bits a row's arithmetic produces, as int32s:
- * [0] plan format version, [1] QKV split-K, [2] O split-K, [3] down split-K,
- * [4] attention positions per CTA window, [5] positions per KV page,
- * [6] greedy tie rule (0 = lowest index).  Two instances whose plans are
- * equal produce identical ids for the same request whatever their batch,
- * slot count or tile shapes (those never change a row's bits); a resume
- * across unequal plans is not bit-exact.  Returns the number of ints (7),
- * writes at most cap. */
+ * [0] plan format version (2), [1] QKV split-K, [2] O split-K, [3] down
+ * split-K, [4] attention positions per CTA window, [5] attention warps per
+ * item (page p -> warp p mod warps), [6] positions per KV page, [7] greedy
+ * tie rule (0 = lowest index).  Two instances whose plans are equal produce
+ * identical ids for the same request whatever their batch, slot count or
+ * tile shapes (those never change a row's bits); a resume across unequal
+ * plans is not bit-exact.  Returns the number of ints (8), writes at most
+ * cap. */
 int32_t rlb_numerics_plan(const rlb_instance* h, int32_t* out, int32_t cap);
 
 /* (test hook) The paged KV pool: device base pointer and bytes.  Bitwise

@@ -27,7 +27,12 @@ namespace rlb {
 
 namespace {
 
-constexpr int WARPS = 4;
+#ifndef ATTN_WARPS
+#define ATTN_WARPS 4
+#endif
+// warps per (row, kv head) item: page p of a window goes to warp p mod WARPS,
+// and the partials merge in warp order -- part of the numerics plan
+constexpr int WARPS = ATTN_WARPS;
 constexpr int CHUNK = 16;              // tokens per pipeline stage
 #ifndef ATTN_STAGES
 #define ATTN_STAGES 3
@@ -409,7 +414,7 @@ __global__ void __launch_bounds__(NW * 32, NW == WARPS ? ATTN_PAIR_MINB : 2 * AT
   const int G = a.NQ / a.NKV;
   pdl_trigger();
   pdl_wait();
-  const int rA = 2 * (a.pair_ids ? a.pair_ids[(NW == WARPS ? a.n_short : 0) + blockIdx.z]
+  const int rA = 2 * (a.pair_ids ? a.pair_ids[a.pair_off + blockIdx.z]
                                   : static_cast<int>(blockIdx.z));
   const bool hasB = rA + 1 < a.R;
   const bool shared = hasB && a.row_slot[rA] == a.row_slot[rA + 1];
@@ -910,6 +915,7 @@ __global__ void attn_combine_kernel(AttnArgs a) {
 
 int attention_windows(int max_seq) { return (max_seq + SUPER - 1) / SUPER; }
 int attention_window_positions() { return SUPER; }
+int attention_warps() { return WARPS; }
 
 template <int D>
 static int launch_attn(const AttnArgs& a, cudaStream_t st, bool pairs) {
@@ -931,8 +937,9 @@ static int launch_attn(const AttnArgs& a, cudaStream_t st, bool pairs) {
                                   smem_tma));
     RLB_CUDA(cudaFuncSetAttribute(attn_pair_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   smem2));
-    RLB_CUDA(cudaFuncSetAttribute(attn_pair_kernel<D, 2>,
-                                  cudaFuncAttributeMaxDynamicSharedMemorySize, smem2s));
+    if constexpr (WARPS > 2)
+      RLB_CUDA(cudaFuncSetAttribute(attn_pair_kernel<D, 2>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, smem2s));
     RLB_CUDA(cudaFuncSetAttribute(attn_head16_kernel<D>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, smem2));
     attr[dev & 63] = true;
@@ -944,12 +951,20 @@ static int launch_attn(const AttnArgs& a, cudaStream_t st, bool pairs) {
     if (a.n_head16 > 0)
       RLB_CUDA(launch_k(attn_head16_kernel<D>, dim3(a.max_splits, a.NQ, a.n_head16),
                         dim3(WARPS * 32), smem2, st, a));
-    if (a.n_short > 0)
-      RLB_CUDA(launch_k(attn_pair_kernel<D, 2>, dim3(a.max_splits, a.NKV, a.n_short), dim3(64),
-                        smem2s, st, a));
-    if (a.n_long > 0)
-      RLB_CUDA(launch_k(attn_pair_kernel<D>, dim3(a.max_splits, a.NKV, a.n_long),
-                        dim3(WARPS * 32), smem2, st, a));
+    AttnArgs as = a, al = a;
+    as.pair_off = 0;
+    al.pair_off = a.n_short;
+    if constexpr (WARPS > 2) {
+      if (a.n_short > 0)
+        RLB_CUDA(launch_k(attn_pair_kernel<D, 2>, dim3(a.max_splits, a.NKV, a.n_short), dim3(64),
+                          smem2s, st, as));
+    } else {                      // no narrower variant: short pairs on the same kernel
+      al.pair_off = 0;
+      al.n_long = a.n_short + a.n_long;
+    }
+    if (al.n_long > 0)
+      RLB_CUDA(launch_k(attn_pair_kernel<D>, dim3(a.max_splits, a.NKV, al.n_long),
+                        dim3(WARPS * 32), smem2, st, al));
   } else if (pairs) {
     RLB_CUDA(launch_k(attn_pair_kernel<D>, dim3(a.max_splits, a.NKV, (a.R + 1) / 2),
                       dim3(WARPS * 32), smem2, st, a));

@@ -1197,9 +1197,10 @@ int rlb_kv_pool(rlb_instance* h, void** base, int64_t* bytes) {
 
 int32_t rlb_numerics_plan(const rlb_instance* h, int32_t* out, int32_t cap) {
   if (!h) return 0;
-  const int32_t plan[7] = {1, h->sp_qkv, h->sp_o, h->sp_down, attention_window_positions(), PAGE, 0};
-  for (int i = 0; i < 7 && i < cap && out; ++i) out[i] = plan[i];
-  return 7;
+  const int32_t plan[8] = {2, h->sp_qkv, h->sp_o, h->sp_down, attention_window_positions(),
+                           attention_warps(), PAGE, 0};
+  for (int i = 0; i < 8 && i < cap && out; ++i) out[i] = plan[i];
+  return 8;
 }
 
 int rlb_load_weights(rlb_instance* h, const void* const* hf_ptrs, int32_t n_tensors,

@@ -67,6 +67,7 @@ struct AttnArgs {
   // pair_ids[n_short, n_short + n_long) the rest; null = every pair, 4 warps
   const int* pair_ids = nullptr;
   int n_short = 0, n_long = 0;
+  int pair_off = 0;                 // (set by the launcher) first pair id of a launch
   // prefill rows in groups of 16 consecutive positions of one sequence
   // (first row of each), served per query head by attn_head16_kernel; their
   // pairs are in neither pair list
@@ -81,6 +82,7 @@ struct AttnArgs {
 int attention_launch(const AttnArgs& a, cudaStream_t st, bool row_pairs = false);
 int attention_windows(int max_seq);   // CTA windows per row (AttnArgs.max_splits)
 int attention_window_positions();     // positions per CTA window (numerics plan)
+int attention_warps();                // warps per attention item (numerics plan)
 
 int embed_launch(const bf16* embed, int H, const int* tok, int R, float* h, cudaStream_t st);
 int resid_norm_launch(float* h, const float* part, int S, int Mp, const int* src_rows, int R,

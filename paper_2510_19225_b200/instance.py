@@ -293,8 +293,8 @@ class RolloutInstance:
             out.append((seq[:npr[i]].tolist(), seq[npr[i]:].tolist()))
         return out
 
-    PLAN_FIELDS = ("format", "split_qkv", "split_o", "split_down", "attn_window", "page",
-                   "tie_rule")
+    PLAN_FIELDS = ("format", "split_qkv", "split_o", "split_down", "attn_window", "attn_warps",
+                   "page", "tie_rule")
 
     @property
     def plan(self) -> str:
@@ -302,7 +302,8 @@ class RolloutInstance:
         row's arithmetic.  A resume is bit-exact only between equal plans."""
         buf = (ctypes.c_int32 * 8)()
         n = _lib.lib().rlb_numerics_plan(self._h, buf, 8)
-        return ".".join(f"{k}{buf[i]}" for i, k in zip(range(n), ("v", "q", "o", "d", "w", "p", "t")))
+        return ".".join(f"{k}{buf[i]}"
+                        for i, k in zip(range(n), ("v", "q", "o", "d", "w", "a", "p", "t")))
 
     def status(self) -> dict:
         """protocol `status` payload (+ the numerics plan, an extra field the
