@@ -4,13 +4,13 @@
 // context the configs use (<= 1408 + prefix) that is one CTA per (row, kv head)
 // and no combine pass.  The GQA group (G <= 8 query heads sharing the kv head)
 // forms the M rows of the MMA, so K and V are read from HBM exactly once.
-// Positions are cut into 64-token pages; warp w owns pages w, w+4, w+8, ...
-// of the window and streams them in 16-token chunks through a STAGES-deep
-// cp.async ring (XOR-swizzled rows, ldmatrix / ldmatrix.trans fragments,
-// zero-fill past the context end):
+// Positions are cut into 64-token pages; warp w of the WARPS (2) owns pages
+// w, w+WARPS, ... of the window and streams them in 16-token chunks through
+// a STAGES-deep ring (TMA boxes of the pool's tensor map, or cp.async;
+// XOR-swizzled rows, ldmatrix / ldmatrix.trans fragments):
 //     S = Q K^T (fp32) -> scale, mask -> online softmax in chunk order
 //     -> P (bf16, the S accumulator layout reused as the A operand) -> O += P V
-// The four warp partials are merged in warp order, then normalised (or, for
+// The warp partials are merged in warp order, then normalised (or, for
 // windows beyond the first, written as (O, m, l) and merged in window order).
 //
 // Determinism: every reduction order (quad shuffles, chunk order, warp order,
@@ -28,10 +28,13 @@ namespace rlb {
 namespace {
 
 #ifndef ATTN_WARPS
-#define ATTN_WARPS 4
+#define ATTN_WARPS 2
 #endif
 // warps per (row, kv head) item: page p of a window goes to warp p mod WARPS,
-// and the partials merge in warp order -- part of the numerics plan
+// and the partials merge in warp order -- part of the numerics plan.
+// Measured (bench.py, one box): 2 warps at 4 decode CTAs / 6 prefill pair
+// CTAs per SM beat 4 warps at 2 / 3 (decode attention 67.4 vs 71.2 us at
+// context ~770, prefill -4%) and 1 warp at 8 / 12 (73.3 us).
 constexpr int WARPS = ATTN_WARPS;
 constexpr int CHUNK = 16;              // tokens per pipeline stage
 #ifndef ATTN_STAGES
@@ -77,7 +80,7 @@ __device__ __forceinline__ void mma_bf16(float (&d)[4], uint32_t a0, uint32_t a2
 }  // namespace
 
 #ifndef ATTN_MINB
-#define ATTN_MINB 2   // resident CTAs per SM the register budget is cut for
+#define ATTN_MINB 4   // resident CTAs per SM the register budget is cut for
 #endif
 
 // Everything one (window, kv head, row) item needs before its K/V stream:
@@ -138,7 +141,7 @@ __device__ __forceinline__ uint32_t kv_off(int row, int ch) {
 }
 
 // One item: stream the window's K/V pages through the warps' cp.async rings
-// (S = QK^T, online softmax, O += PV on the tensor cores), merge the four warp
+// (S = QK^T, online softmax, O += PV on the tensor cores), merge the warp
 // partials in warp order, write the row's output (or the window partial).
 // Called by every thread of the CTA (it synchronises the CTA).
 template <int D, bool TMA = false>
@@ -390,13 +393,14 @@ __device__ __forceinline__ void mma_bf16_full(float (&d)[4], uint32_t a0, uint32
 #define ATTN_PAIR_STAGES 2     // prefill rows: a shallower ring, more resident CTAs
 #endif
 #ifndef ATTN_PAIR_MINB
-#define ATTN_PAIR_MINB 3
+#define ATTN_PAIR_MINB 6
 #endif
-// NW = 2: the short-pair variant -- rows with <= 2 pages of context only
-// have pages in warp slots 0 and 1, so two physical warps do all the work and
-// slots 2, 3 enter the merge as the empty partials (m = -inf, l = 0, o = 0)
-// an idle warp of the 4-warp kernel contributes: the same merge, the same
-// bits, at half the CTA footprint.
+// NW = 2 < WARPS (built only when WARPS > 2): the short-pair variant --
+// rows with <= 2 pages of context only have pages in warp slots 0 and 1, so
+// two physical warps do all the work and the other slots enter the merge as
+// the empty partials (m = -inf, l = 0, o = 0) an idle warp of the full
+// kernel contributes: the same merge, the same bits, at a smaller footprint.
+// With WARPS = 2 (the default) every pair runs on the full kernel.
 template <int D, int NW = WARPS>
 __global__ void __launch_bounds__(NW * 32, NW == WARPS ? ATTN_PAIR_MINB : 2 * ATTN_PAIR_MINB)
     attn_pair_kernel(AttnArgs a) {
@@ -592,7 +596,7 @@ __global__ void __launch_bounds__(NW * 32, NW == WARPS ? ATTN_PAIR_MINB : 2 * AT
         mls[(warp * 16 + 8 + h) * 2] = m_run[1];
         mls[(warp * 16 + 8 + h) * 2 + 1] = l_run[1];
       }
-      if constexpr (NW < WARPS) {   // the idle slots' partials, as the 4-warp kernel has them
+      if constexpr (NW < WARPS) {   // the idle slots' partials, as the full kernel has them
         for (int w = NW + warp; w < WARPS; w += NW) {
 #pragma unroll
           for (int t = 0; t < NT; ++t) {

@@ -98,7 +98,7 @@ def test_live_refuses_a_mismatched_numerics_plan():
     mgr = threading.Thread(target=srv.run_until_done, kwargs=dict(timeout=60), daemon=True)
     mgr.start()
     import time
-    for k, plan in enumerate(["v2.q1.o3.d5.w2048.a4.p64.t0", "v2.q1.o2.d5.w2048.a4.p64.t0"]):
+    for k, plan in enumerate(["v2.q1.o3.d5.w2048.a2.p64.t0", "v2.q1.o2.d5.w2048.a2.p64.t0"]):
         inst = FakeInstance(vocab=997, max_slots=4, plan=plan)
         t = threading.Thread(target=serve_instance, args=(srv.address, inst, f"i{k}"),
                              kwargs=dict(open_endpoint=lambda ep, v: ep, n_steps=3, stop=stop),
