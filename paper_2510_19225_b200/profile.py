@@ -49,6 +49,10 @@ def calibrate_profile(instance, batch_sizes: Iterable[int], *, prompt_len: int =
     import random
     rng = random.Random(seed)
     vocab = instance.shape.vocab
+    cap = getattr(instance, "max_seq_len", None)
+    if cap is not None and prompt_len + steps + 1 > cap:
+        raise ValueError(f"calibration needs {prompt_len + steps + 1} positions, "
+                         f"the instance holds {cap}")
     points = []
     for b in sorted(set(int(x) for x in batch_sizes)):
         if b <= 0:

@@ -24,11 +24,12 @@ the manager:
 `dispatch` routes held requests with the reference's `select_instance`
 (`balancer.py:80-92`) and `route_to` (`manager.py:258-259`).  It is the
 reference `dispatch` loop (`manager.py:208-222`) with one change: the
-per-iteration snapshot holds the pending queues only, because JSQ reads
+snapshot `select_instance` sees is each serving instance's pending-queue
+depth (taken once, bumped as requests are routed), because JSQ reads
 `m_pending` alone -- the reference rebuilds every serving instance's
-executing list for each routed request, O(routed x executing), which costs
-~1 s when 1,024 requests are re-routed onto survivors running 3,072
-(config 3).  Routing decisions and `route` events are identical
+pending and executing lists for each routed request, O(routed x executing),
+which costs ~1 s when 1,024 requests are re-routed onto survivors running
+3,072 (config 3).  Routing decisions and `route` events are identical
 (`tests/test_responses.py::test_dispatch_matches_reference`).
 """
 from __future__ import annotations
