@@ -310,6 +310,20 @@ struct rlb_instance {
     p.dbg = d_dbg;
     return gemm_launch_pairp(a, b128, EPI_PARTIAL, p, st);
   }
+  // Prefill chunks: the pair tile's splits summed on its cluster and added
+  // into h (EPI_SUMRES) instead of [S][R][H] partial slabs through HBM and a
+  // resid_norm that sums them -- the same adds in the same order, so the
+  // same bits (RLB_SUMRES=0 / RLB_SUMRES_ROWS=<min rows> for A/B).
+  bool sumres_on = true;
+  int sumres_rows = 4096;
+  size_t part_floats = 0;   // capacity of d_part
+  bool use_sumres(int R, int splits) const {
+    return sumres_on && R >= sumres_rows && pairp_sumres_scratch(splits) <= part_floats;
+  }
+  int proj_sumres(const CUtensorMap& a, const CUtensorMap& b128, int splits, int R, int N, int K) {
+    GemmParams p{R, N, K, nullptr, d_h, N, splits, d_part};
+    return gemm_launch_pairp(a, b128, EPI_SUMRES, p, st);
+  }
   int n_sm = 148;
   bool small_gu_wave = true;   // RLB_SMALL_GU_WAVE=0: 128-wide SwiGLU tiles at <= 128 rows
   bool bm_override = false;   // RLB_BM set: the fixed decode-batch tiles below
@@ -376,7 +390,9 @@ struct rlb_instance {
   int pairp = 2 | 4 | 8 | 16;   // + bit 16: QKV (RoPE epilogue) in prefill chunks
   bool pairp_prefill = true;
   bool cl_down_large = false;
-  bool last_cl_down = true;   // mode of the last forward (its head sums the partials)
+  bool last_cl_down = true;   // the last forward's down output is already in h (else the
+                              // head sums its partials)
+  bool down_summed = true;
   // split-K O / down: sum the splits inside a cluster and add into h in the
   // GEMM epilogue (true), or write fp32 partials that the following RMSNorm
   // kernel sums in split order (false)
@@ -576,6 +592,8 @@ int rlb_instance::init() {
   if (const char* ov = std::getenv("RLB_SORT_ROWS")) sort_rows = std::atoi(ov) != 0;
   if (const char* ov = std::getenv("RLB_PAIRP")) pairp = std::atoi(ov);
   if (const char* ov = std::getenv("RLB_PAIRP_PREFILL")) pairp_prefill = std::atoi(ov) != 0;
+  if (const char* ov = std::getenv("RLB_SUMRES")) sumres_on = std::atoi(ov) != 0;
+  if (const char* ov = std::getenv("RLB_SUMRES_ROWS")) sumres_rows = std::atoi(ov);
   if (const char* ov = std::getenv("RLB_BM")) {   // "qkv,o,gate_up,down" (tuning; process-wide)
     int a = 0, b = 0, c = 0, d = 0;
     if (std::sscanf(ov, "%d,%d,%d,%d", &a, &b, &c, &d) == 4) {
@@ -658,7 +676,11 @@ int rlb_instance::init() {
   if ((rc = dalloc(&d_logits, static_cast<size_t>(logit_rows) * V))) return rc;
   if ((rc = dalloc(&d_ws, R * ws_row / sizeof(float)))) return rc;
   const size_t part = std::max({static_cast<size_t>(sp_o) * H, static_cast<size_t>(sp_down) * H});
-  if ((rc = dalloc(&d_part, part * R))) return rc;
+  part_floats = part * R;
+  // chunks that run the split-sum epilogue need its per-CTA scratch
+  if (sumres_on && R >= static_cast<size_t>(sumres_rows))
+    part_floats = std::max({part_floats, pairp_sumres_scratch(sp_o), pairp_sumres_scratch(sp_down)});
+  if ((rc = dalloc(&d_part, part_floats))) return rc;
   if ((rc = dalloc(&d_ring, static_cast<size_t>(RING_ROWS) * max_slots))) return rc;
   if ((rc = dalloc(&d_pairs, max_rows / 2 + 1))) return rc;
   if ((rc = dalloc(&d_head16, max_rows / 16 + 1))) return rc;
@@ -794,6 +816,11 @@ int rlb_instance::forward_layers(int R, bool prefill) {
           (rc = resid_norm_launch(d_h, nullptr, 0, R, nullptr, R, w.ln2, H, m.rms_eps, d_xn, false,
                                   st)))
         return rc;
+    } else if (pair_o(R) && use_sumres(R, sp_o)) {
+      if ((rc = proj_sumres(m_attn, w.m_o, sp_o, R, H, NQ * D)) ||
+          (rc = resid_norm_launch(d_h, nullptr, 0, R, nullptr, R, w.ln2, H, m.rms_eps, d_xn, false,
+                                  st)))
+        return rc;
     } else {
       if ((rc = pair_o(R) ? proj_pairp(m_attn, w.m_o, sp_o, R, H, NQ * D)
                           : o_partials(tp, w, R)) ||
@@ -811,7 +838,13 @@ int rlb_instance::forward_layers(int R, bool prefill) {
       }
     }
     const bool last = l + 1 == m.layers;
-    if (tp.cl_down) {
+    down_summed = tp.cl_down || (pair_down(R) && use_sumres(R, sp_down));
+    if (down_summed && !tp.cl_down) {
+      if ((rc = proj_sumres(m_act, w.m_down, sp_down, R, H, F))) return rc;
+      if (!last && (rc = resid_norm_launch(d_h, nullptr, 0, R, nullptr, R, L[l + 1].ln1, H,
+                                           m.rms_eps, d_xn, false, st)))
+        return rc;
+    } else if (tp.cl_down) {
       if ((rc = proj(m_act, w.m_down, BN_DOWN, sp_down, EPI_RESADD, R, H, F, nullptr, d_h, H,
                      tp.bm_down)))
         return rc;
@@ -830,7 +863,7 @@ int rlb_instance::forward_layers(int R, bool prefill) {
     }
   }
   pending_rows = R;
-  last_cl_down = tp.cl_down;
+  last_cl_down = down_summed;
   return RLB_OK;
 }
 

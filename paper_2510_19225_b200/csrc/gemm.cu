@@ -787,14 +787,20 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
 // EPI_PARTIAL (split-K, grid-stride over (m, n, split) tiles) gives one
 // pipeline stage to per-warp staging of the fp32 partial (32 rows x 32
 // columns at a time, written back as full 128-byte row segments).
+// EPI_SUMRES runs a pair tile's splits back to back on one cluster and
+// keeps their running sum (acc = p0; acc += p1 ... += p[S-1]) in the CTA's
+// L2-resident scratch tile; the last split adds it into the fp32 residual h
+// -- the bits resid_norm_kernel<S> produces from EPI_PARTIAL slabs, without
+// the [S][M][N] slabs in HBM.
 template <int EPI>
 struct PairPCfg {
+  static constexpr bool kStaged = EPI == EPI_PARTIAL || EPI == EPI_SUMRES;
   static constexpr int A_BYTES = HM * BK * 2;
   static constexpr int B_BYTES = 128 * BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int STAGES = EPI == EPI_PARTIAL ? 5 : 6;
+  static constexpr int STAGES = kStaged ? 5 : 6;
   static constexpr int XPITCH = 36;                                // staged fp32 row (floats)
-  static constexpr int XSTAGE = EPI == EPI_PARTIAL ? 8 * 32 * XPITCH * 4 : 0;
+  static constexpr int XSTAGE = kStaged ? 8 * 32 * XPITCH * 4 : 0;
   static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 2048 + XSTAGE;   // + barriers, argmax exchange
   static constexpr uint32_t TMEM_COLS = 512;
 };
@@ -823,13 +829,32 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   const int m_tiles = (p.M + 255) / 256, n_tiles = (p.N + BN - 1) / BN;
   // split-K: split z covers K blocks [z*nkt/S, (z+1)*nkt/S) -- the single-SM
   // kernel's partition, so every partial has the same bits
-  const int S = EPI == EPI_PARTIAL ? p.splits : 1;
+  const int S = (EPI == EPI_PARTIAL || EPI == EPI_SUMRES) ? p.splits : 1;
   const int ntiles = m_tiles * n_tiles * S;
   const int nkt = p.K / BK;
-  auto krange = [&](int t, int& kb0, int& nk) {
-    const int z = t / (m_tiles * n_tiles);
+  auto krange = [&](int z, int& kb0, int& nk) {
     kb0 = z * nkt / S;
     nk = (z + 1) * nkt / S - kb0;
+  };
+  // the cluster's j-th work unit: (m tile, n tile, split).  Grid-stride over
+  // (m, n, split) with the split slowest; EPI_SUMRES: grid-stride over pair
+  // tiles, each tile's splits consecutively and the n tiles of an m tile on
+  // neighbouring clusters (they stream the same A rows through L2 together)
+  auto unit = [&](int j, int& mt, int& nt, int& z) {
+    if constexpr (EPI == EPI_SUMRES) {
+      const int tile = cid + (j / S) * ncl;
+      if (tile >= m_tiles * n_tiles) return false;
+      nt = tile % n_tiles;
+      mt = tile / n_tiles;
+      z = j % S;
+    } else {
+      const int t = cid + j * ncl;
+      if (t >= ntiles) return false;
+      mt = t % m_tiles;
+      nt = (t / m_tiles) % n_tiles;
+      z = t / (m_tiles * n_tiles);
+    }
+    return true;
   };
 
   if (warp == 0 && lane == 0) {
@@ -856,11 +881,10 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
 
   if (warp == 0) {
     if (lane == 0) {
-      int g = 0;
-      for (int t = cid; t < ntiles; t += ncl) {
-        const int mt = t % m_tiles, nt = (t / m_tiles) % n_tiles;
+      int g = 0, mt, nt, z;
+      for (int j = 0; unit(j, mt, nt, z); ++j) {
         int kb0, nk;
-        krange(t, kb0, nk);
+        krange(z, kb0, nk);
         for (int kb = 0; kb < nk; ++kb, ++g) {
           const int s = g % C::STAGES;
           const uint32_t ph = (g / C::STAGES) & 1;
@@ -877,13 +901,13 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   } else if (warp == 1) {
     if (lane == 0 && r == 0) {
       constexpr uint32_t idesc = umma_idesc_bf16(256, BN);
-      int g = 0, i = 0;
-      for (int t = cid; t < ntiles; t += ncl, ++i) {
+      int g = 0, mt, nt, z;
+      for (int i = 0; unit(i, mt, nt, z); ++i) {
         const int b = i & 1;
         mbar_wait_cluster(smem_u32(&tempty[b]), ((i >> 1) & 1) ^ 1);
         tc_fence_after();
         int kb0, nk;
-        krange(t, kb0, nk);
+        krange(z, kb0, nk);
         for (int kb = 0; kb < nk; ++kb, ++g) {
           const int s = g % C::STAGES;
           const uint32_t ph = (g / C::STAGES) & 1;
@@ -903,10 +927,9 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     const int q = warp & 3;                    // TMEM lane quadrant (rows)
     const int ch = (warp - 4) >> 2;            // column half of the 256-column tile
     const uint32_t leader_tempty = dsmem_addr(smem_u32(&tempty[0]), 0);
-    int i = 0;
-    for (int t = cid; t < ntiles; t += ncl, ++i) {
+    int mt, nt, z;
+    for (int i = 0; unit(i, mt, nt, z); ++i) {
       const int b = i & 1;
-      const int mt = t % m_tiles, nt = (t / m_tiles) % n_tiles;
       const int m = mt * 256 + r * HM + q * 32 + lane;
       const bool live = m < p.M;
       const bool warp_dead = mt * 256 + r * HM + q * 32 >= p.M;
@@ -980,7 +1003,6 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         // per store instruction out)
         float* xs = reinterpret_cast<float*>(smem + C::STAGES * C::STAGE_BYTES + 2048) +
                     (warp - 4) * 32 * C::XPITCH;
-        const int z = t / (m_tiles * n_tiles);
         float* base = p.ws + static_cast<size_t>(z) * p.M * p.N;
         const int mrow0 = mt * 256 + r * HM + q * 32;
 #pragma unroll 1
@@ -1002,6 +1024,68 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
             if (mm < p.M && n < p.N)
               *reinterpret_cast<float4*>(base + static_cast<size_t>(mm) * p.N + n) =
                   *reinterpret_cast<const float4*>(xs + rr * C::XPITCH + (lane & 7) * 4);
+          }
+          __syncwarp();
+        }
+      } else if constexpr (EPI == EPI_SUMRES) {
+        // 32 x 32 blocks through the warp's staging tile as EPI_PARTIAL.  The
+        // running sum of the tile's splits lives in the CTA's scratch tile:
+        // split 0 stores p0, split z adds p_z to it, the last split adds its
+        // sum into h -- ((p0 + p1) + ...) + p[S-1], resid_norm's order.  A
+        // scratch element is written and read by one thread; a block's loads
+        // are issued before its stores.
+        float* xs = reinterpret_cast<float*>(smem + C::STAGES * C::STAGE_BYTES + 2048) +
+                    (warp - 4) * 32 * C::XPITCH;
+        float* scr = p.ws + static_cast<size_t>(blockIdx.x) * (128 * 256);
+        float* hres = reinterpret_cast<float*>(p.out);
+        const int mrow0 = mt * 256 + r * HM + q * 32;
+        const bool fin = z == S - 1;
+#pragma unroll 1
+        for (int c = 0; c < (warp_dead ? 0 : 128); c += 32) {
+          uint32_t rv[32];
+          tmem_ld32(tbase + c, rv);
+          tmem_ld_wait();
+          float4* s4 = reinterpret_cast<float4*>(xs + lane * C::XPITCH);
+#pragma unroll
+          for (int e = 0; e < 8; ++e)
+            s4[e] = make_float4(__uint_as_float(rv[4 * e]), __uint_as_float(rv[4 * e + 1]),
+                                __uint_as_float(rv[4 * e + 2]), __uint_as_float(rv[4 * e + 3]));
+          __syncwarp();
+          const int lc = ch * 128 + c + (lane & 7) * 4;     // column within the CTA tile
+          const int n = nt * BN + lc;
+          const float* xrow = xs + (lane >> 3) * C::XPITCH + (lane & 7) * 4;
+          float* srow = scr + static_cast<size_t>(q * 32 + (lane >> 3)) * 256 + lc;
+          float* hrow = hres + static_cast<size_t>(mrow0 + (lane >> 3)) * p.ldo + n;
+          float4 a[8], hv[8];
+          if (z > 0) {
+#pragma unroll
+            for (int e = 0; e < 8; ++e) a[e] = __ldcg(reinterpret_cast<const float4*>(srow + e * 4 * 256));
+          }
+          if (fin) {
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+              const bool ok = mrow0 + e * 4 + (lane >> 3) < p.M && n < p.N;
+              hv[e] = ok ? *reinterpret_cast<const float4*>(hrow + static_cast<size_t>(e) * 4 * p.ldo)
+                         : make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+          }
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            const float4 v = *reinterpret_cast<const float4*>(xrow + e * 4 * C::XPITCH);
+            if (z > 0) {
+              a[e].x += v.x;
+              a[e].y += v.y;
+              a[e].z += v.z;
+              a[e].w += v.w;
+            } else {
+              a[e] = v;
+            }
+            if (!fin) {
+              __stcg(reinterpret_cast<float4*>(srow + e * 4 * 256), a[e]);
+            } else if (mrow0 + e * 4 + (lane >> 3) < p.M && n < p.N) {
+              *reinterpret_cast<float4*>(hrow + static_cast<size_t>(e) * 4 * p.ldo) =
+                  make_float4(hv[e].x + a[e].x, hv[e].y + a[e].y, hv[e].z + a[e].z, hv[e].w + a[e].w);
+            }
           }
           __syncwarp();
         }
@@ -1126,6 +1210,8 @@ int gemm_prepare() {
                                 cudaFuncAttributeMaxDynamicSharedMemorySize, PairPCfg<EPI_ROPE>::SMEM));
   RLB_CUDA(cudaFuncSetAttribute(gemm_pairp_tc<EPI_PARTIAL>,
                                 cudaFuncAttributeMaxDynamicSharedMemorySize, PairPCfg<EPI_PARTIAL>::SMEM));
+  RLB_CUDA(cudaFuncSetAttribute(gemm_pairp_tc<EPI_SUMRES>,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize, PairPCfg<EPI_SUMRES>::SMEM));
   done[dev & 63] = true;
   return RLB_OK;
 }
@@ -1220,16 +1306,32 @@ int gemm_launch(const CUtensorMap& a, const CUtensorMap& b, int block_n, int epi
 }
 
 // Persistent 2-SM pair tiles (256 x 256 per cluster, double-buffered TMEM).
+int pairp_units(int epi, int M, int N, int splits) {
+  const int tiles = ((M + 255) / 256) * ((N + 255) / 256);
+  return epi == EPI_PARTIAL ? tiles * splits : tiles;
+}
+
+size_t pairp_sumres_scratch(int splits) {
+  int dev = 0, n_sm = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess ||
+      cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
+    n_sm = 148;
+  return splits > 1 ? static_cast<size_t>(n_sm / 2) * 2 * 128 * 256 : 0;
+}
+
 int gemm_launch_pairp(const CUtensorMap& a, const CUtensorMap& b128, int epi, const GemmParams& p,
                       cudaStream_t st) {
   if (p.M <= 0) return RLB_OK;
-  RLB_CHECK(p.K % BK == 0 && (p.splits == 1 || epi == EPI_PARTIAL), RLB_ERR_ARG,
+  const bool split_epi = epi == EPI_PARTIAL || epi == EPI_SUMRES;
+  RLB_CHECK(p.K % BK == 0 && (p.splits == 1 || split_epi), RLB_ERR_ARG,
             "persistent pair GEMM: K multiple of 64, split-K only with fp32 partials");
   RLB_CHECK(epi == EPI_SWIGLU || epi == EPI_ARGMAX ||
                 (epi == EPI_ROPE && p.splits == 1 && p.bias != nullptr && p.N % 256 == 0 &&
                  (p.rope.d == 64 || p.rope.d == 128)) ||
-                (epi == EPI_PARTIAL && p.ws != nullptr && p.splits >= 1 && p.K / BK >= p.splits),
+                (split_epi && p.ws != nullptr && p.splits >= 1 && p.K / BK >= p.splits) ,
             RLB_ERR_ARG, "persistent pair GEMM epilogues: SwiGLU, argmax, RoPE, fp32 partials");
+  RLB_CHECK(epi != EPI_SUMRES || (p.out != nullptr && p.N % 4 == 0 && p.ldo % 4 == 0),
+            RLB_ERR_ARG, "split-sum pair GEMM: fp32 residual rows, 16-byte aligned");
   RLB_CHECK(epi != EPI_SWIGLU || p.N % 256 == 0, RLB_ERR_ARG, "SwiGLU pair tiles are 256 wide");
   static int n_sm = 0;
   if (!n_sm) {
@@ -1237,12 +1339,11 @@ int gemm_launch_pairp(const CUtensorMap& a, const CUtensorMap& b128, int epi, co
     RLB_CUDA(cudaGetDevice(&dev));
     RLB_CUDA(cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev));
   }
-  const int ntiles = ((p.M + 255) / 256) * ((p.N + 255) / 256) * (epi == EPI_PARTIAL ? p.splits : 1);
-  const int clusters = std::min(ntiles, n_sm / 2);
+  const int clusters = std::min(pairp_units(epi, p.M, p.N, p.splits), n_sm / 2);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(2 * clusters, 1, 1);
   cfg.blockDim = dim3(GEMM_THREADS);
-  cfg.dynamicSmemBytes = epi == EPI_PARTIAL ? PairPCfg<EPI_PARTIAL>::SMEM : PairPCfg<EPI_SWIGLU>::SMEM;
+  cfg.dynamicSmemBytes = split_epi ? PairPCfg<EPI_PARTIAL>::SMEM : PairPCfg<EPI_SWIGLU>::SMEM;
   cfg.stream = st;
   cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -1255,6 +1356,7 @@ int gemm_launch_pairp(const CUtensorMap& a, const CUtensorMap& b128, int epi, co
   cfg.numAttrs = pdl_enabled(RLB_PDL_CLASS) ? 2 : 1;
   if (epi == EPI_SWIGLU) RLB_CUDA(cudaLaunchKernelEx(&cfg, gemm_pairp_tc<EPI_SWIGLU>, a, b128, p));
   else if (epi == EPI_PARTIAL) RLB_CUDA(cudaLaunchKernelEx(&cfg, gemm_pairp_tc<EPI_PARTIAL>, a, b128, p));
+  else if (epi == EPI_SUMRES) RLB_CUDA(cudaLaunchKernelEx(&cfg, gemm_pairp_tc<EPI_SUMRES>, a, b128, p));
   else if (epi == EPI_ROPE) RLB_CUDA(cudaLaunchKernelEx(&cfg, gemm_pairp_tc<EPI_ROPE>, a, b128, p));
   else RLB_CUDA(cudaLaunchKernelEx(&cfg, gemm_pairp_tc<EPI_ARGMAX>, a, b128, p));
   return RLB_OK;

@@ -10,7 +10,7 @@ namespace rlb {
 constexpr int PAGE = 64;      // tokens per KV page
 
 enum Epi { EPI_BF16 = 0, EPI_RESADD = 1, EPI_SWIGLU = 2, EPI_F32 = 3, EPI_ARGMAX = 4,
-           EPI_PARTIAL = 5, EPI_ROPE = 6 };
+           EPI_PARTIAL = 5, EPI_ROPE = 6, EPI_SUMRES = 7 };
 // Split-K epilogues reduced inside a (1,1,splits) thread-block cluster
 // through distributed shared memory (BN = 128): RESADD (h += sum) and ROPE.
 constexpr bool cluster_epi(int epi) { return epi == EPI_RESADD || epi == EPI_ROPE; }
@@ -35,7 +35,8 @@ struct GemmParams {
   void* out;
   int ldo;
   int splits;     // split-K factor (1 = no split)
-  float* ws;      // EPI_PARTIAL: fp32 partials [splits][M][N]
+  float* ws;      // EPI_PARTIAL: fp32 partials [splits][M][N]; EPI_SUMRES: per-CTA
+                  // running-sum tiles [CTA][128][256] (out = the fp32 residual h)
   unsigned long long* dbg;  // optional: globaltimer stamps of CTA 0 (latency breakdown)
   RopeDst rope;   // EPI_ROPE only
 };
@@ -52,6 +53,8 @@ int make_kmajor_map3(CUtensorMap* map, const void* ptr, int64_t rows, int64_t k,
 int make_kv_map(CUtensorMap* map, const void* kv, int64_t rows, int head_dim);
 int gemm_launch_pairp(const CUtensorMap& a, const CUtensorMap& b128, int epi, const GemmParams& p,
                       cudaStream_t st);
+int pairp_units(int epi, int M, int N, int splits);   // work units of one pair-GEMM launch
+size_t pairp_sumres_scratch(int splits);              // EPI_SUMRES scratch (floats)
 
 // ---- elementwise / attention launchers (kernels.cu) ----
 struct AttnArgs {

@@ -397,15 +397,6 @@ def _kv_bytes(inst):
     return buf
 
 
-def _kv_bytes(inst):
-    from paper_2510_19225_b200 import _lib
-    p, n = inst.kv_pool()
-    buf = torch.empty(n, dtype=torch.uint8, device="cuda")
-    _lib.check(_lib.lib().rlb_copy_bytes(0, buf.data_ptr(), p, n, None))
-    torch.cuda.synchronize()
-    return buf
-
-
 @pytest.mark.parametrize("case", ["mid-3", "mid-300", "tiny-long"])
 def test_attention_tma_same_bits(request, monkeypatch, case):
     """Decode attention with K/V chunks through TMA boxes of the KV pool
@@ -477,6 +468,29 @@ def test_prefill_head16_same_bits(request, monkeypatch, case):
     out = {}
     for flag in ("0", "1"):
         monkeypatch.setenv("RLB_ATTN_HEAD16", flag)
+        inst = _instance(shape, w, **kw)
+        logits = inst.score(prompts[0])
+        toks = _rollout(inst, prompts, new)
+        out[flag] = (logits, toks, _kv_bytes(inst))
+        inst.close()
+    assert np.array_equal(out["0"][0].view(np.uint32), out["1"][0].view(np.uint32))
+    assert out["0"][1] == out["1"][1]
+    assert torch.equal(out["0"][2], out["1"][2])
+
+
+def test_prefill_split_sum_same_bits(mid, monkeypatch):
+    """Prefill O / down with the pair tile's splits summed on its cluster and
+    added into h (EPI_SUMRES) against the [S][R][H] partial slabs summed by
+    resid_norm (RLB_SUMRES=0): teacher-forced logits bitwise equal and, after
+    a rollout with ragged chunks (rows not a multiple of 256), the KV pool
+    bytewise equal -- so a resumed request still continues bit-identically."""
+    shape, w, _ = mid
+    prompts = synth_prompts(14, shape.vocab, 600, 900, seed=53)
+    kw, new = dict(max_slots=16, max_seq_len=1024, max_prefill_rows=2999), 16
+    out = {}
+    monkeypatch.setenv("RLB_SUMRES_ROWS", "513")
+    for flag in ("0", "1"):
+        monkeypatch.setenv("RLB_SUMRES", flag)
         inst = _instance(shape, w, **kw)
         logits = inst.score(prompts[0])
         toks = _rollout(inst, prompts, new)
