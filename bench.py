@@ -62,7 +62,8 @@ def parse():
     ap.add_argument("--new-tokens", type=int, default=NEW_TOKENS)
     ap.add_argument("--flush-steps", type=int, default=64, help="decode steps per rlb_step call")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--prefill-rows", type=int, default=16384, help="token rows per prefill chunk")
+    ap.add_argument("--prefill-rows", type=int, default=18944,
+                    help="token rows per prefill chunk (74 x 256: whole pair-tile waves)")
     ap.add_argument("--split-o", type=int, default=0, help="O split-K (0 = measured default)")
     ap.add_argument("--split-down", type=int, default=0, help="down split-K (0 = measured default)")
     ap.add_argument("--profile-at", type=float, default=0.5,

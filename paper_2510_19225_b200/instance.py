@@ -47,10 +47,12 @@ class PullResult:
 
 class RolloutInstance:
     def __init__(self, shape: ModelShape, device: int = 0, *, max_slots: int = 512,
-                 max_seq_len: int = 1536, max_prefill_rows: int = 16384, graph_steps: int = 8,
+                 max_seq_len: int = 1536, max_prefill_rows: int = 18944, graph_steps: int = 8,
                  num_pages: int = 0, split_o: int = 0, split_down: int = 0):
-        """split_o / split_down: split-K factors of the O / down projections
-        (0 = the measured default).  They are part of the numerics plan:
+        """max_prefill_rows: token rows per prefill chunk; 18,944 = 74 x 256
+        puts the same number of 256-row pair tiles on each of the 74 SM
+        pairs in every prefill GEMM.  split_o / split_down: split-K factors of
+        the O / down projections (0 = the measured default).  They are part of the numerics plan:
         instances exchanging requests must agree on it (`plan`)."""
         self.shape = shape
         self.device = device
