@@ -320,8 +320,12 @@ struct rlb_instance {
   bool use_sumres(int R, int splits) const {
     return sumres_on && R >= sumres_rows && pairp_sumres_scratch(splits) <= part_floats;
   }
+  // Splits of <= 1,024 K (O) keep the running sum in TMEM: their MMAs are
+  // shorter than the L2 scratch round trips (RLB_SUMRES_TMEM=0/1 overrides).
+  int sumres_tmem = -1;
   int proj_sumres(const CUtensorMap& a, const CUtensorMap& b128, int splits, int R, int N, int K) {
     GemmParams p{R, N, K, nullptr, d_h, N, splits, d_part};
+    p.sum_tmem = sumres_tmem >= 0 ? sumres_tmem : (K / splits <= 1024 ? 1 : 0);
     return gemm_launch_pairp(a, b128, EPI_SUMRES, p, st);
   }
   int n_sm = 148;
@@ -594,6 +598,7 @@ int rlb_instance::init() {
   if (const char* ov = std::getenv("RLB_PAIRP_PREFILL")) pairp_prefill = std::atoi(ov) != 0;
   if (const char* ov = std::getenv("RLB_SUMRES")) sumres_on = std::atoi(ov) != 0;
   if (const char* ov = std::getenv("RLB_SUMRES_ROWS")) sumres_rows = std::atoi(ov);
+  if (const char* ov = std::getenv("RLB_SUMRES_TMEM")) sumres_tmem = std::atoi(ov) != 0;
   if (const char* ov = std::getenv("RLB_BM")) {   // "qkv,o,gate_up,down" (tuning; process-wide)
     int a = 0, b = 0, c = 0, d = 0;
     if (std::sscanf(ov, "%d,%d,%d,%d", &a, &b, &c, &d) == 4) {

@@ -927,6 +927,15 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     const int q = warp & 3;                    // TMEM lane quadrant (rows)
     const int ch = (warp - 4) >> 2;            // column half of the 256-column tile
     const uint32_t leader_tempty = dsmem_addr(smem_u32(&tempty[0]), 0);
+    // hand TMEM buffer bb back to the leader's MMA thread (one arrival per warp)
+    auto release = [&](int bb) {
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) {
+        if (r == 0) mbar_arrive(smem_u32(&tempty[bb]));
+        else mbar_arrive_cluster(leader_tempty + bb * 8);
+      }
+    };
     int mt, nt, z;
     for (int i = 0; unit(i, mt, nt, z); ++i) {
       const int b = i & 1;
@@ -1028,6 +1037,68 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           __syncwarp();
         }
       } else if constexpr (EPI == EPI_SUMRES) {
+       if (p.sum_tmem) {
+        // Running sum in TMEM (splits of a few K blocks, where the L2 scratch
+        // traffic below would outlast the MMAs): unit i's buffer holds p_z;
+        // for z >= 1 the sum of the previous unit's buffer (s_{z-1}) and this
+        // one is stored over p_z and the previous buffer goes back to the
+        // MMA thread; the last split then adds its buffer into h.  Each
+        // buffer use is released exactly once (by the next unit of its tile,
+        // or by itself when it is the last split).
+        const uint32_t tprev = tmem + (b ^ 1) * BN + ch * 128 + (static_cast<uint32_t>(q * 32) << 16);
+        if (z > 0) {
+#pragma unroll 1
+          for (int c = 0; c < (warp_dead ? 0 : 128); c += 32) {
+            uint32_t ra[32], rc[32];
+            tmem_ld32(tprev + c, ra);
+            tmem_ld32(tbase + c, rc);
+            tmem_ld_wait();
+#pragma unroll
+            for (int e = 0; e < 32; ++e)
+              ra[e] = __float_as_uint(__uint_as_float(ra[e]) + __uint_as_float(rc[e]));
+            tmem_st32(tbase + c, ra);
+          }
+          tmem_st_wait();
+          release(b ^ 1);
+        }
+        if (z == S - 1) {
+          float* xs = reinterpret_cast<float*>(smem + C::STAGES * C::STAGE_BYTES + 2048) +
+                      (warp - 4) * 32 * C::XPITCH;
+          float* hres = reinterpret_cast<float*>(p.out);
+          const int mrow0 = mt * 256 + r * HM + q * 32;
+#pragma unroll 1
+          for (int c = 0; c < (warp_dead ? 0 : 128); c += 32) {
+            uint32_t rv[32];
+            tmem_ld32(tbase + c, rv);
+            tmem_ld_wait();
+            float4* s4 = reinterpret_cast<float4*>(xs + lane * C::XPITCH);
+#pragma unroll
+            for (int e = 0; e < 8; ++e)
+              s4[e] = make_float4(__uint_as_float(rv[4 * e]), __uint_as_float(rv[4 * e + 1]),
+                                  __uint_as_float(rv[4 * e + 2]), __uint_as_float(rv[4 * e + 3]));
+            __syncwarp();
+            const int n = nt * BN + ch * 128 + c + (lane & 7) * 4;
+            const float* xrow = xs + (lane >> 3) * C::XPITCH + (lane & 7) * 4;
+            float* hrow = hres + static_cast<size_t>(mrow0 + (lane >> 3)) * p.ldo + n;
+            float4 hv[8];
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+              const bool ok = mrow0 + e * 4 + (lane >> 3) < p.M && n < p.N;
+              hv[e] = ok ? *reinterpret_cast<const float4*>(hrow + static_cast<size_t>(e) * 4 * p.ldo)
+                         : make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+              const float4 a = *reinterpret_cast<const float4*>(xrow + e * 4 * C::XPITCH);
+              if (mrow0 + e * 4 + (lane >> 3) < p.M && n < p.N)
+                *reinterpret_cast<float4*>(hrow + static_cast<size_t>(e) * 4 * p.ldo) =
+                    make_float4(hv[e].x + a.x, hv[e].y + a.y, hv[e].z + a.z, hv[e].w + a.w);
+            }
+            __syncwarp();
+          }
+          release(b);
+        }
+       } else {
         // 32 x 32 blocks through the warp's staging tile as EPI_PARTIAL.  The
         // running sum of the tile's splits lives in the CTA's scratch tile:
         // split 0 stores p0, split z adds p_z to it, the last split adds its
@@ -1089,13 +1160,9 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           }
           __syncwarp();
         }
+       }
       }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) {
-        if (r == 0) mbar_arrive(smem_u32(&tempty[b]));
-        else mbar_arrive_cluster(leader_tempty + b * 8);
-      }
+      if (EPI != EPI_SUMRES || !p.sum_tmem) release(b);
     }
   }
   tc_fence_before();

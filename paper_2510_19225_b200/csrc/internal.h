@@ -39,6 +39,7 @@ struct GemmParams {
                   // running-sum tiles [CTA][128][256] (out = the fp32 residual h)
   unsigned long long* dbg;  // optional: globaltimer stamps of CTA 0 (latency breakdown)
   RopeDst rope;   // EPI_ROPE only
+  int sum_tmem = 0;   // EPI_SUMRES: running sum in TMEM (short splits), else in L2 scratch
 };
 
 int make_kmajor_map(CUtensorMap* map, const void* ptr, int64_t rows, int64_t k, int box_rows);

@@ -478,24 +478,40 @@ def test_prefill_head16_same_bits(request, monkeypatch, case):
     assert torch.equal(out["0"][2], out["1"][2])
 
 
-def test_prefill_split_sum_same_bits(mid, monkeypatch):
+@pytest.mark.parametrize("case", ["mid", "7b-width"])
+def test_prefill_split_sum_same_bits(request, monkeypatch, case):
     """Prefill O / down with the pair tile's splits summed on its cluster and
     added into h (EPI_SUMRES) against the [S][R][H] partial slabs summed by
     resid_norm (RLB_SUMRES=0): teacher-forced logits bitwise equal and, after
     a rollout with ragged chunks (rows not a multiple of 256), the KV pool
-    bytewise equal -- so a resumed request still continues bit-identically."""
-    shape, w, _ = mid
-    prompts = synth_prompts(14, shape.vocab, 600, 900, seed=53)
+    bytewise equal -- so a resumed request still continues bit-identically.
+    1.5B widths (splits 3 / 5) and 7B widths (splits 4 / 4, 14 n tiles)."""
+    if case == "mid":
+        shape, w, _ = request.getfixturevalue("mid")
+        n = 14
+    else:
+        from paper_2510_19225_b200.shapes import ModelShape
+        shape = ModelShape("qwen2.5-7b-2L-v8192", vocab=8192, hidden=3584, layers=2,
+                           n_q_heads=28, n_kv_heads=4, head_dim=128, ffn=18_944, tied=False)
+        w = synth_hf_weights(shape, seed=3, device="cuda")
+        n = 8
+    prompts = synth_prompts(n, shape.vocab, 600, 900, seed=53)
     kw, new = dict(max_slots=16, max_seq_len=1024, max_prefill_rows=2999), 16
     out = {}
     monkeypatch.setenv("RLB_SUMRES_ROWS", "513")
-    for flag in ("0", "1"):
-        monkeypatch.setenv("RLB_SUMRES", flag)
+    # slabs; running sums in L2 scratch; in TMEM; the default (TMEM for O)
+    for flag in ("0", "1:0", "1:1", "1"):
+        monkeypatch.setenv("RLB_SUMRES", flag[0])
+        if ":" in flag:
+            monkeypatch.setenv("RLB_SUMRES_TMEM", flag[2])
+        else:
+            monkeypatch.delenv("RLB_SUMRES_TMEM", raising=False)
         inst = _instance(shape, w, **kw)
         logits = inst.score(prompts[0])
         toks = _rollout(inst, prompts, new)
         out[flag] = (logits, toks, _kv_bytes(inst))
         inst.close()
-    assert np.array_equal(out["0"][0].view(np.uint32), out["1"][0].view(np.uint32))
-    assert out["0"][1] == out["1"][1]
-    assert torch.equal(out["0"][2], out["1"][2])
+    for flag in ("1:0", "1:1", "1"):
+        assert np.array_equal(out["0"][0].view(np.uint32), out[flag][0].view(np.uint32)), flag
+        assert out["0"][1] == out[flag][1], flag
+        assert torch.equal(out["0"][2], out[flag][2]), flag
