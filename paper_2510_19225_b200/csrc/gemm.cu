@@ -1037,6 +1037,11 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           __syncwarp();
         }
       } else if constexpr (EPI == EPI_SUMRES) {
+       // the h rows the last split adds into: into L2 one unit ahead (the
+       // last split's pass is otherwise a chain of HBM round trips)
+       if (z == (S > 1 ? S - 2 : 0) && live && nt * BN + ch * 128 + 128 <= p.N)
+         l2_prefetch_bulk(reinterpret_cast<const float*>(p.out) + static_cast<size_t>(m) * p.ldo +
+                              nt * BN + ch * 128, 128 * sizeof(float));
        if (p.sum_tmem) {
         // Running sum in TMEM (splits of a few K blocks, where the L2 scratch
         // traffic below would outlast the MMAs): unit i's buffer holds p_z;
