@@ -478,7 +478,7 @@ def test_prefill_head16_same_bits(request, monkeypatch, case):
     assert torch.equal(out["0"][2], out["1"][2])
 
 
-@pytest.mark.parametrize("case", ["mid", "7b-width"])
+@pytest.mark.parametrize("case", ["mid", "7b-width", "odd-width"])
 def test_prefill_split_sum_same_bits(request, monkeypatch, case):
     """Prefill O / down with the pair tile's splits summed on its cluster and
     added into h (EPI_SUMRES) against the [S][R][H] partial slabs summed by
@@ -486,9 +486,19 @@ def test_prefill_split_sum_same_bits(request, monkeypatch, case):
     a rollout with ragged chunks (rows not a multiple of 256), the KV pool
     bytewise equal -- so a resumed request still continues bit-identically.
     1.5B widths (splits 3 / 5) and 7B widths (splits 4 / 4, 14 n tiles)."""
+    extra = {}
     if case == "mid":
         shape, w, _ = request.getfixturevalue("mid")
         n = 14
+    elif case == "odd-width":
+        # hidden 640: the last 256-column pair tile is half outside N; splits
+        # 2 / 3 forced through the instance config
+        from paper_2510_19225_b200.shapes import ModelShape
+        shape = ModelShape("odd-2L-d640", vocab=4096, hidden=640, layers=2, n_q_heads=5,
+                           n_kv_heads=1, head_dim=128, ffn=1792, tied=True)
+        w = synth_hf_weights(shape, seed=5, device="cuda")
+        n = 14
+        extra = dict(split_o=2, split_down=3)
     else:
         from paper_2510_19225_b200.shapes import ModelShape
         shape = ModelShape("qwen2.5-7b-2L-v8192", vocab=8192, hidden=3584, layers=2,
@@ -496,7 +506,7 @@ def test_prefill_split_sum_same_bits(request, monkeypatch, case):
         w = synth_hf_weights(shape, seed=3, device="cuda")
         n = 8
     prompts = synth_prompts(n, shape.vocab, 600, 900, seed=53)
-    kw, new = dict(max_slots=16, max_seq_len=1024, max_prefill_rows=2999), 16
+    kw, new = dict(max_slots=16, max_seq_len=1024, max_prefill_rows=2999, **extra), 16
     out = {}
     monkeypatch.setenv("RLB_SUMRES_ROWS", "513")
     # slabs; running sums in L2 scratch; in TMEM; the default (TMEM for O)
