@@ -32,17 +32,21 @@
 #include <unordered_map>
 
 // Programmatic dependent launch per kernel class (1 GEMM, 2 attention, 4 row
-// kernels, 8 small kernels), RLB_PDL_MASK (default: all); RLB_NO_PDL=1 turns
-// it off.  Every kernel waits (griddepcontrol.wait) before touching memory
-// its predecessors write; the GEMM producer streams its first weight stages
-// before waiting.  Measured on B200 (1.5B shape): decode step at 512 rows
-// 3.50 -> 3.37 ms, tokens bit-identical to the non-PDL build.
+// kernels, 8 small kernels), RLB_PDL_MASK (default 11: all but the RMSNorm
+// row kernels); RLB_NO_PDL=1 turns it off.  Every kernel waits
+// (griddepcontrol.wait) before touching memory its predecessors write; the
+// GEMM producer streams its first weight stages before waiting.  Measured on
+// B200 (1.5B shape): decode step at 512 rows 3.50 -> 3.37 ms with PDL, tokens
+// bit-identical to the non-PDL build; launching the RMSNorms without it (so
+// they do not take SM slots while the GEMM before them drains, the GEMM after
+// them still launches early) -0.57% decode over 5 A/B pairs
+// (scripts/r2_gpu_au.sh, r2_gpu_av.sh).
 bool pdl_enabled(int cls) {
   static const int mask = [] {
     const char* off = std::getenv("RLB_NO_PDL");
     if (off && off[0] == '1') return 0;
     const char* m = std::getenv("RLB_PDL_MASK");
-    return m ? std::atoi(m) : 15;
+    return m ? std::atoi(m) : 11;
   }();
   return (mask & cls) != 0;
 }
