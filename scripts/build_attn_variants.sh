@@ -7,8 +7,10 @@ make -s -j8
 NV="/usr/local/cuda/bin/nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Iinclude --expt-relaxed-constexpr"
 for v in "$@"; do
   tag=${v%%:*}; flags=${v#*:}
-  $NV $flags -c paper_2510_19225_b200/csrc/attention.cu -o build/attention_$tag.o
-  objs=$(ls build/*.o | grep -v "attention" | tr '\n' ' ')
-  $NV -shared -o paper_2510_19225_b200/librlb_$tag.so build/attention_$tag.o $objs -lcudart -ldl
+  tmp=$(mktemp -d)
+  $NV $flags -c paper_2510_19225_b200/csrc/attention.cu -o $tmp/attention.o
+  objs="build/engine.o build/gemm.o build/kernels.o build/pull.o build/rowops.o"
+  $NV -shared -o paper_2510_19225_b200/librlb_$tag.so $tmp/attention.o $objs -lcudart -ldl
+  rm -rf $tmp
   echo built paper_2510_19225_b200/librlb_$tag.so
 done
